@@ -1,0 +1,27 @@
+# In-tree build of the three native libraries.
+#   paper_cs_0609090_b200/libldpc.so  -- the product: CUDA kernels for sm_100a + C ABI (include/ldpc.h)
+#   oracle/liboracle.so                -- CPU oracle (test infrastructure only)
+#   ldpcgen/libldpcgen.so              -- seeded input generators
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+LIB := paper_cs_0609090_b200/libldpc.so
+SRCS := paper_cs_0609090_b200/csrc/ldpc_api.cu
+HDRS := $(wildcard paper_cs_0609090_b200/csrc/*.cuh) include/ldpc.h
+
+all: $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so
+
+$(LIB): $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lcudart 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+oracle/liboracle.so: oracle/oracle.c oracle/engine.inc
+	gcc -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -o $@ oracle/oracle.c -lpthread
+
+ldpcgen/libldpcgen.so: ldpcgen/ldpcgen.c
+	gcc -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -o $@ ldpcgen/ldpcgen.c -lm -lpthread
+
+clean:
+	rm -f $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so
+
+.PHONY: all clean
+$(shell mkdir -p build)

@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark: single-scan min-sum LDPC decoding on B200 (one process per GPU).
+
+Default workload (N=1): BASELINE.json configs[1] = config 2 (QC 35x59, Z=127,
+DTMB shape, int16 Q3 LLRs at 1.5 dB, offset min-sum, <= 15 iterations with
+per-frame early stop, 8192 frames per GPU).  `--config k` selects another of the
+five BASELINE configs.  A "step" is one ldpc_decode_batch of the whole per-GPU
+batch (all iterations, syndrome checks, outputs) on inputs already in HBM.
+
+Prints ONE JSON line (rank 0).  Under torchrun each rank decodes its own frame
+shard (global frames [r*F, (r+1)*F)), weak scaling, and the bit/frame error
+counters are all-reduced over NCCL after the timed region.
+`--impl reference` times the CPU oracle (the paper's method as plain C) instead.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ldpcgen as g  # noqa: E402
+
+METRIC = "decoded info Gbit/s and edge-updates/s at 1/2/4/8 B200; % HBM roofline"
+UNIT = "Gbit/s"
+L2_FLUSH_BYTES = 256 << 20
+
+# Algorithmic bytes per edge-update (PAPER.md P:331-335 persistent-data model:
+# read Z^(k-1) and Z^(0), write Z^(k), read+write the compact state per check):
+# bytes/iter/frame = N (w_Z0 + 2 w_L) + 2 M w_state.
+W_BYTES = {1: (2, 2, 4), 2: (2, 2, 4), 3: (1, 2, 2.375), 4: (2, 2, 4), 5: (4, 4, 12)}
+# Algorithmic integer operations per edge-update of the method:
+# rebuild L_old (select magnitude, apply sign), q = Z - L_old, |q|, two-minimum
+# update (2 compares), sign product, new message (select, sign), Z += L.
+ALG_OPS_PER_EU = 10
+
+
+def describe(cfg, code):
+    kinds = {g.LLR_I16: "int16 Q3", g.LLR_I8: "int8 Q2", g.LLR_F32: "fp32"}
+    var = (f"offset {cfg.offset_raw} LSB" if cfg.variant == "offset" else f"normalized alpha={cfg.alpha}")
+    stop = "early stop" if cfg.early_stop else "fixed"
+    return (f"cfg{cfg.idx}: {cfg.code_kind} N={code.n_vars} M={code.n_checks} E={code.n_edges}, {kinds[cfg.llr_kind]} "
+            f"LLRs at {cfg.ebn0_db} dB, {var}, {cfg.max_iter} it {stop}, {cfg.msg_format} messages, "
+            f"{cfg.frames} frames/GPU")
+
+
+def bytes_per_eu(cfg, code):
+    wz, wl, ws = W_BYTES[cfg.idx]
+    return (code.n_vars * (wz + 2 * wl) + 2 * code.n_checks * ws) / code.n_edges
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_dev{device_index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[4 + i] and "Not" not in r[4 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_oracle_throughput(cfg, code, engine, budget_s, nthreads=0, start_frames=16):
+    """Time the oracle as it stands on the host's cores over a bounded sample of the
+    workload (frames from the same generator); returns (info Gbit/s, EU/s, frames, threads, seconds)."""
+    import oracle
+    mode = "f32" if cfg.llr_kind == g.LLR_F32 else "int"
+    nt = nthreads or oracle.hardware_threads()
+    F = max(start_frames, nt)
+    while True:
+        llr = cfg.llrs(code, 0, F)
+        z = llr if mode == "f32" else llr.astype(np.int32)
+        t0 = time.perf_counter()
+        r = oracle.decode(code, z, engine, mode, cfg.max_iter, cfg.early_stop, cfg.offset_raw if mode == "int" else 0,
+                          cfg.clamp if mode == "int" else 0, cfg.alpha, nthreads=nt)
+        dt = time.perf_counter() - t0
+        if dt >= budget_s * 0.5 or F >= 4096:
+            eu = float(r.iters.sum()) * code.n_edges
+            return F * code.K / dt / 1e9, eu / dt, F, r.threads, dt
+        F = int(min(4096, F * max(2.0, budget_s * 0.6 / max(dt, 1e-3))))
+
+
+def run_reference(args, cfg, code, rank, world):
+    """--impl reference: the CPU oracle (compact single-scan, the paper's method) timed on host cores."""
+    if rank != 0:
+        return
+    import oracle
+    nt = oracle.hardware_threads()
+    budget = max(1.0, 120.0 / max(1, args.steps + args.warmup))
+    # size the per-step sample once
+    _, _, F, _, _ = cpu_oracle_throughput(cfg, code, "compact", min(budget, 5.0), nt)
+    llr = cfg.llrs(code, 0, F)
+    mode = "f32" if cfg.llr_kind == g.LLR_F32 else "int"
+    z = llr if mode == "f32" else llr.astype(np.int32)
+    times, eus = [], []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = oracle.decode(code, z, "compact", mode, cfg.max_iter, cfg.early_stop, cfg.offset_raw if mode == "int" else 0,
+                          cfg.clamp if mode == "int" else 0, cfg.alpha, nthreads=nt)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            eus.append(float(r.iters.sum()) * code.n_edges)
+    tot = sum(times)
+    value = args.steps * F * code.K / tot / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32" if mode == "int" else "f32",
+            "data": "synthetic", "edge_updates_per_s": sum(eus) / tot,
+            "config": {"workload": describe(cfg, code), "frames_per_step": F, "engine": "oracle compact single-scan"},
+            "cpu_baseline": {"kind": "oracle", "value": value, "unit": UNIT, "cores": nt,
+                             "sample": f"{F} frames of the workload per step, all host threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=0, help="override frames per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = g.CONFIGS[args.config]
+    if args.frames:
+        cfg.frames = args.frames
+    code = cfg.code()
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, code, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_cs_0609090_b200 as P
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    F = cfg.frames
+    f0 = rank * F
+    llr_host = cfg.llrs(code, f0, F)                      # this rank's global frame shard
+    llr = torch.from_numpy(llr_host).to(dev)
+    dec = P.Decoder(code, local)
+    params = P.params_for_config(cfg)
+    out = dec.alloc_outputs(F, params.llr_type, posteriors=True)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        dec.decode(llr, params, out)
+    torch.cuda.synchronize(dev)
+    launches_per_step = P.ldpc_last_launch_count()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)                             # L2 flush between steps (not timed)
+        evs[i][0].record(stream)
+        dec.decode(llr, params, out)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+
+    # iterations / error counters of the last step (all steps decode the same frames)
+    counters = dec.count_errors(out)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    c = counters.cpu().numpy().tolist()
+    sum_iters = c[4]
+    eu_per_step = float(sum_iters) * code.n_edges               # all ranks
+    info_bits_per_step = float(world) * F * code.K
+    value = info_bits_per_step * args.steps / (total_ms * 1e-3) / 1e9
+    eu_s = eu_per_step * args.steps / (total_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (the decode is one resident launch, or the
+    # per-iteration streaming launches): measured per-step on this rank's stream
+    peaks, peak_src = load_peaks()
+    my_eu = float(out.iterations.sum().item()) * code.n_edges
+    my_ms = statistics.mean(step_ms)
+    resident = launches_per_step == 1
+    if resident:
+        clk = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        peak_ops = 148 * 128 * 2 * clk * 1e6 / 1e12     # 16x2 SIMD int ops/s (TOP/s), DESIGN.md §5.2
+        achieved = ALG_OPS_PER_EU * my_eu / (my_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
+                "frac": achieved / peak_ops, "traffic": None,
+                "hbm_model": {"bytes_per_eu": bytes_per_eu(cfg, code),
+                              "achieved_gbs": bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 1e9,
+                              "peak_gbs": peaks["hbm_gbs"],
+                              "frac": bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}}
+    else:
+        ach = bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": None}
+    roof["peak_source"] = peak_src
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg.idx}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            roof["traffic"] = json.load(f).get("dram_bytes_per_launch")
+
+    # ---- end to end through the C ABI with host buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        lh = torch.from_numpy(llr_host).pin_memory()
+        hbh = torch.empty((F, dec.wpf), dtype=torch.int32).pin_memory()
+        okh = torch.empty(F, dtype=torch.uint8).pin_memory()
+        ith = torch.empty(F, dtype=torch.int32).pin_memory()
+        for _ in range(2):
+            dec.decode_host(lh, params, hbh, okh, ith)
+        torch.cuda.synchronize(dev)
+        e_ms = []
+        for i in range(max(3, min(args.steps, 10))):
+            flush.fill_(i & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dec.decode_host(lh, params, hbh, okh, ith)
+            b.record(stream)
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        te = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": info_bits_per_step * len(e_ms) / (float(te.item()) * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(llr_host.nbytes),
+               "d2h_bytes_per_step": int(hbh.numel() * 4 + okh.numel() + ith.numel() * 4),
+               "ms_per_step": float(te.item()) / len(e_ms)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gb, eus, Fs, nt, dt = cpu_oracle_throughput(cfg, code, "compact", args.cpu_budget)
+        gb2, eus2, Fs2, nt2, dt2 = cpu_oracle_throughput(cfg, code, "twoscan", args.cpu_budget / 2)
+        cpu = {"value": gb, "unit": UNIT, "cores": nt, "kind": "oracle",
+               "sample": f"{Fs} frames of the workload (compact single-scan oracle, {dt:.1f} s, all host threads)",
+               "edge_updates_per_s": eus,
+               "twoscan": {"value": gb2, "edge_updates_per_s": eus2, "frames": Fs2},
+               "singlescan_over_twoscan": gb / gb2 if gb2 else None,
+               "paper_claim": "single-scan min-sum more than twice as fast as two-scan (PAPER.md P:29-30)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32" if cfg.llr_kind == g.LLR_F32 else ("int16x2" if cfg.llr_kind == g.LLR_I16 else "int8->int16x2"),
+                "data": "synthetic", "edge_updates_per_s": eu_s,
+                "config": {"workload": describe(cfg, code), "frames_per_gpu": F, "global_frames": F * world,
+                           "parallelism": f"dp{world} (frames sharded, counters all-reduced over NCCL)",
+                           "info_bits_per_frame": code.K, "l2": "flushed between timed steps (256 MiB write)",
+                           "code_sha256": code.sha256()[:16]},
+                "errors": {"bit_errors": c[0], "frame_errors": c[1], "undetected": c[2], "not_converged": c[3],
+                           "mean_iterations": sum_iters / (F * world)},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,412 @@
+// k_stream.cuh -- streaming single-scan min-sum kernels for long codes.
+//
+// Used when one frame pair's posterior double buffer does not fit in shared
+// memory (e.g. N = 64800).  Frames are tiled TILE-wide and stored
+// frame-interleaved ([tile][n][lane], 128 B per variable per warp) so every
+// gather, state access and accumulation of a warp is one coalesced 128-byte
+// line.  One launch per iteration; a warp processes whole check rows for the
+// 32 lanes of its tile using only check->variable addressing (PAPER.md
+// P:219-224); Z^(k)_n += L^(k)_mn is a coalesced global reduction
+// (RED) into an accumulator that was initialised to Z^(0)_n by the previous
+// iteration's launch (three rotating posterior buffers: read Z^(k-1),
+// accumulate Z^(k), initialise the buffer for Z^(k+1)).
+//
+// Integer path: two frames per lane (16x2 SIMD).  Accumulators are kept in
+// "V form" (value = hi * 65536 + lo as a 32-bit integer) so that a 32-bit
+// integer RED adds both 16-bit lanes exactly; gathers convert back to the
+// packed per-half form.  fp32 path: one frame per lane, RED.F32.
+#pragma once
+#include "rowcore.cuh"
+
+namespace ldpc {
+
+__device__ __forceinline__ uint32_t to_vform(uint32_t p) { return p - ((p & 0x8000u) << 1); }
+__device__ __forceinline__ uint32_t from_vform(uint32_t v) { return v + ((v & 0x8000u) << 1); }
+
+struct StreamArgs {
+    int N, M, ntiles, nframes, K, Qsat, wpf;
+    uint32_t nbeta2, q2;
+    float alpha, beta;           // fp32 variant: |L| <= max(alpha*min - beta, 0)
+    const int32_t *row_ptr, *col_idx;
+    const void *llr;
+    uint32_t *Z0;                // [tile][N][32]
+    uint32_t *Lb[3];             // rotating posterior buffers [tile][N][32]
+    uint32_t *st;                // [tile][words][M][32]
+    uint32_t *synd;              // [tile][32]: syndrome-fail bits found during the current launch
+    uint32_t *done;              // [tile][32]: frames frozen (early stop)
+    int32_t *it_ws;              // [tile*TILE] iterations used per frame
+    uint8_t *ok_ws;              // [tile*TILE] syndrome ok per frame (frozen frames)
+    uint32_t *hard_bits;
+    void *post;
+    uint8_t *ok;
+    int32_t *iters;
+};
+
+// -------------------------------------------------------------- integer path
+// ingest: user [F][N] -> Z0 (V form, doubled, saturated) and Lb[0] (packed form
+// for the first read is not needed: all buffers are V form), Lb[1] = Z0.
+template <typename TIN>
+__global__ void k_stream_ingest_i(const StreamArgs a) {
+    const int tile = blockIdx.y, lane = threadIdx.x & 31;
+    const int f0 = tile * 64 + 2 * lane, f1 = f0 + 1;
+    const TIN *llr = (const TIN *)a.llr;
+    for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < a.N; n += gridDim.x * (blockDim.x >> 5)) {
+        int zl = 0, zh = 0;
+        if (f0 < a.nframes) zl = max(-a.Qsat, min(a.Qsat, (int)llr[(size_t)f0 * a.N + n]));
+        if (f1 < a.nframes) zh = max(-a.Qsat, min(a.Qsat, (int)llr[(size_t)f1 * a.N + n]));
+        const uint32_t v = to_vform(pack2(2 * zl, 2 * zh));
+        const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
+        a.Z0[idx] = v;
+        a.Lb[0][idx] = v;
+        a.Lb[1][idx] = v;
+    }
+}
+
+template <int DC, int FMT, bool ES>
+__device__ __forceinline__ void stream_row_i(const StreamArgs &a, int tile, int lane, int m, int e0,
+                                             const uint32_t *Lp, uint32_t *La, bool first_iter, uint32_t keep,
+                                             uint32_t &synd) {
+    uint32_t L[DC];
+    size_t idx[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        const int n = __ldg(a.col_idx + e0 + j);
+        idx[j] = ((size_t)tile * a.N + n) * 32 + lane;
+    }
+#pragma unroll
+    for (int j = 0; j < DC; ++j) L[j] = from_vform(__ldcg(Lp + idx[j]));
+    if (ES) synd |= row_parity<DC>(L);
+    uint32_t *stb = a.st + (size_t)tile * StateIO<FMT>::kWords * a.M * 32 + lane;
+    const size_t sstride = (size_t)a.M * 32;
+    uint32_t q[DC];
+    RowState st;
+    if (first_iter) {
+#pragma unroll
+        for (int j = 0; j < DC; ++j) q[j] = L[j];
+    } else {
+        st = StateIO<FMT>::load(stb, sstride, (size_t)m * 32);
+        rebuild_q<DC>(L, st, q);
+    }
+    uint32_t rn[DC];
+    new_state<DC>(q, a.nbeta2, a.q2, st, rn);
+    StateIO<FMT>::store(stb, sstride, (size_t)m * 32, st);
+#pragma unroll
+    for (int j = 0; j < DC; ++j) atomicAdd(La + idx[j], to_vform(rn[j] & ~keep));
+}
+
+template <int FMT, bool ES>
+__global__ void __launch_bounds__(256) k_stream_iter_i(const StreamArgs a, int k) {
+    const int tile = blockIdx.y, lane = threadIdx.x & 31;
+    const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nwg = gridDim.x * (blockDim.x >> 5);
+    const uint32_t *Lp = a.Lb[(k - 1) % 3];
+    uint32_t *La = a.Lb[k % 3];
+    uint32_t *Ln = a.Lb[(k + 1) % 3];
+    uint32_t keep = 0;                                   // 0xFFFF halves: frame frozen
+    if (ES) {
+        const uint32_t d = a.done[tile * 32 + lane];
+        keep = ((d & 1) ? 0x0000FFFFu : 0u) | ((d & 2) ? 0xFFFF0000u : 0u);
+        if (__all_sync(0xFFFFFFFFu, d == 3)) return;
+    }
+    // initialise the accumulator of the next iteration (it held Z^(k-2))
+    if (k < a.K) {
+        for (int n = wg; n < a.N; n += nwg) {
+            const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
+            uint32_t v = __ldcg(a.Z0 + idx);
+            if (ES && keep) v = to_vform(sel(keep, from_vform(__ldcg(Ln + idx)), from_vform(v)));
+            __stcg(Ln + idx, v);
+        }
+    }
+    uint32_t synd = 0;
+    const bool first_iter = (k == 1);
+    for (int m = wg; m < a.M; m += nwg) {
+        const int e0 = __ldg(a.row_ptr + m), dc = __ldg(a.row_ptr + m + 1) - e0;
+        switch (dc) {
+        case 2: stream_row_i<2, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
+        case 3: stream_row_i<3, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
+        case 4: stream_row_i<4, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
+        case 5: stream_row_i<5, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
+        case 6: stream_row_i<6, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
+        case 7: stream_row_i<7, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
+        case 8: stream_row_i<8, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
+        }
+    }
+    if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
+}
+
+// syndrome of the buffer read by iteration k (final check)
+template <bool PAIR>
+__global__ void __launch_bounds__(256) k_stream_syndrome(const StreamArgs a, int bufidx) {
+    const int tile = blockIdx.y, lane = threadIdx.x & 31;
+    const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nwg = gridDim.x * (blockDim.x >> 5);
+    const uint32_t *Lp = a.Lb[bufidx];
+    uint32_t synd = 0;
+    for (int m = wg; m < a.M; m += nwg) {
+        const int e0 = __ldg(a.row_ptr + m), e1 = __ldg(a.row_ptr + m + 1);
+        uint32_t p = 0;
+        for (int e = e0; e < e1; ++e) {
+            const size_t idx = ((size_t)tile * a.N + __ldg(a.col_idx + e)) * 32 + lane;
+            if (PAIR) p ^= vadd(from_vform(__ldcg(Lp + idx)), 0xFFFFFFFFu);
+            else p ^= (__int_as_float(__ldcg(Lp + idx)) <= 0.0f) ? 1u : 0u;
+        }
+        synd |= PAIR ? (p & 0x80008000u) : (p & 1u);
+    }
+    if (synd) atomicOr(a.synd + tile * 32 + lane, synd);
+}
+
+// early-stop bookkeeping after iteration k: frames whose Z^(k-1) passed the
+// syndrome test are frozen with iterations_used = k-1.
+template <bool PAIR>
+__global__ void k_stream_freeze(const StreamArgs a, int k) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.ntiles * 32) return;
+    const uint32_t s = a.synd[i];
+    uint32_t d = a.done[i];
+    const int tile = i >> 5, lane = i & 31;
+    if (PAIR) {
+        for (int h = 0; h < 2; ++h) {
+            const int f = tile * 64 + 2 * lane + h;
+            const bool fail = h ? (s & 0x80000000u) : (s & 0x8000u);
+            if (!(d & (1u << h)) && !fail && f < a.nframes) {
+                d |= 1u << h;
+                a.it_ws[f] = k - 1;
+                a.ok_ws[f] = 1;
+            }
+        }
+    } else {
+        const int f = tile * 32 + lane;
+        if (!(d & 1) && !(s & 1) && f < a.nframes) { d |= 1; a.it_ws[f] = k - 1; a.ok_ws[f] = 1; }
+    }
+    a.done[i] = d;
+    a.synd[i] = 0;
+}
+
+// outputs: frame-major posteriors and hard bits from the tiled buffers.  A block
+// handles one tile x 32 variables, transposing through shared memory.
+template <bool PAIR>
+__global__ void __launch_bounds__(256) k_stream_output(const StreamArgs a) {
+    __shared__ uint32_t sh[32][33];
+    __shared__ uint32_t sh2[32][33];
+    const int tile = blockIdx.y, n0 = blockIdx.x * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;   // 8 warps
+    const int tw = PAIR ? 64 : 32;
+    // stage: sh[v][lane] = value of variable n0+v for the tile's lane (per-frame buffer choice)
+    for (int v = warp; v < 32; v += 8) {
+        const int n = n0 + v;
+        uint32_t val = 0, val2 = 0;
+        if (n < a.N) {
+            const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
+            if (PAIR) {
+                const int f0 = tile * 64 + 2 * lane;
+                const int k0 = f0 < a.nframes ? a.it_ws[f0] : a.K;
+                const int k1 = f0 + 1 < a.nframes ? a.it_ws[f0 + 1] : a.K;
+                val = from_vform(__ldcg(a.Lb[k0 % 3] + idx));
+                val2 = from_vform(__ldcg(a.Lb[k1 % 3] + idx));
+                val = (val & 0xFFFFu) | (val2 & 0xFFFF0000u);
+            } else {
+                const int f = tile * 32 + lane;
+                const int kk = f < a.nframes ? a.it_ws[f] : a.K;
+                val = __ldcg(a.Lb[kk % 3] + idx);
+            }
+        }
+        sh[v][lane] = val;
+        (void)sh2;
+    }
+    __syncthreads();
+    // each warp handles frames; lane = variable offset
+    for (int fl = warp; fl < tw; fl += 8) {
+        const int f = tile * tw + fl;
+        if (f >= a.nframes) continue;
+        const int n = n0 + lane;
+        bool hb = false;
+        if (PAIR) {
+            const uint32_t w = sh[lane][fl >> 1];
+            const int v = (fl & 1) ? hi16(w) : lo16(w);
+            hb = v <= 0;
+            if (n < a.N && a.post) ((int16_t *)a.post)[(size_t)f * a.N + n] = (int16_t)(v >> 1);
+        } else {
+            const float v = __int_as_float(sh[lane][fl]);
+            hb = v <= 0.0f;
+            if (n < a.N && a.post) ((float *)a.post)[(size_t)f * a.N + n] = v;
+        }
+        const uint32_t word = __ballot_sync(0xFFFFFFFFu, hb && n < a.N);
+        if (lane == 0) a.hard_bits[(size_t)f * a.wpf + blockIdx.x] = word;
+        if (blockIdx.x == 0 && lane == 0) {
+            a.ok[f] = a.ok_ws[f];
+            if (a.iters) a.iters[f] = a.it_ws[f];
+        }
+    }
+}
+
+// frames not frozen by early stop: iterations = K, ok from the final syndrome
+template <bool PAIR>
+__global__ void k_stream_finalize_flags(const StreamArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.ntiles * 32) return;
+    const uint32_t s = a.synd[i], d = a.done[i];
+    const int tile = i >> 5, lane = i & 31;
+    const int nh = PAIR ? 2 : 1;
+    for (int h = 0; h < nh; ++h) {
+        const int f = PAIR ? tile * 64 + 2 * lane + h : tile * 32 + lane;
+        if (f >= a.nframes || (d & (1u << h))) continue;
+        const bool fail = PAIR ? (h ? (s & 0x80000000u) : (s & 0x8000u)) : (s & 1u);
+        a.it_ws[f] = a.K;
+        a.ok_ws[f] = fail ? 0 : 1;
+    }
+}
+
+// -------------------------------------------------------------- fp32 path
+__global__ void k_stream_ingest_f(const StreamArgs a) {
+    const int tile = blockIdx.y, lane = threadIdx.x & 31;
+    const int f = tile * 32 + lane;
+    const float *llr = (const float *)a.llr;
+    for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < a.N; n += gridDim.x * (blockDim.x >> 5)) {
+        float z = 0.0f;
+        if (f < a.nframes) z = llr[(size_t)f * a.N + n];
+        z = z + 0.0f;                                   // canonicalise -0.0 (reading D13)
+        const uint32_t v = __float_as_uint(z);
+        const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
+        a.Z0[idx] = v;
+        a.Lb[0][idx] = v;
+        a.Lb[1][idx] = v;
+    }
+}
+
+// One row, one frame per lane, fp32 (reading D11: one RN rounding per operation,
+// no FMA contraction: __fsub_rn / __fmul_rn).
+template <int DC, bool ES>
+__device__ __forceinline__ void stream_row_f(const StreamArgs &a, int tile, int lane, int m, int e0,
+                                             const float *Lp, float *La, bool first_iter, bool frozen,
+                                             uint32_t &synd) {
+    float L[DC];
+    size_t idx[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) idx[j] = ((size_t)tile * a.N + __ldg(a.col_idx + e0 + j)) * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < DC; ++j) L[j] = __ldcg(Lp + idx[j]);
+    if (ES) {
+        uint32_t p = 0;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) p ^= L[j] <= 0.0f ? 1u : 0u;
+        synd |= p;
+    }
+    uint32_t *stb = a.st + (size_t)tile * 3 * a.M * 32 + lane;
+    const size_t ss = (size_t)a.M * 32, so = (size_t)m * 32;
+    float q[DC];
+    if (first_iter) {
+#pragma unroll
+        for (int j = 0; j < DC; ++j) q[j] = L[j];
+    } else {
+        const float A = __uint_as_float(__ldcg(stb + so)), B = __uint_as_float(__ldcg(stb + ss + so));
+        const uint32_t W = __ldcg(stb + 2 * ss + so);
+        const int idx0 = (int)(W >> 16);
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            const float mag = (j == idx0) ? B : A;                         // f(A,B,n,ñ)
+            const float lold = ((W >> j) & 1u) ? -mag : mag;               // s_mn f(...)
+            q[j] = __fsub_rn(L[j], lold);                                  // Z_n' - L_mn'
+        }
+    }
+    float m1 = fabsf(q[0]), m2 = 0.0f;
+    int i1 = 0;
+    bool have2 = false;
+    uint32_t sq = q[0] < 0.0f ? 1u : 0u;
+#pragma unroll
+    for (int j = 1; j < DC; ++j) {
+        const float x = fabsf(q[j]);
+        sq |= (q[j] < 0.0f ? 1u : 0u) << j;
+        if (x < m1) { m2 = m1; have2 = true; m1 = x; i1 = j; }
+        else if (!have2 || x < m2) { m2 = x; have2 = true; }
+    }
+    const uint32_t par = __popc(sq) & 1u;
+    float A = __fsub_rn(__fmul_rn(a.alpha, m1), a.beta);
+    A = A < 0.0f ? 0.0f : A;
+    float B = __fsub_rn(__fmul_rn(a.alpha, m2), a.beta);
+    B = B < 0.0f ? 0.0f : B;
+    const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;             // s = prod of the others
+    __stcg(stb + so, __float_as_uint(A));
+    __stcg(stb + ss + so, __float_as_uint(B));
+    __stcg(stb + 2 * ss + so, sg | ((uint32_t)i1 << 16));
+    if (frozen) return;
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        const float mag = (j == i1) ? B : A;
+        atomicAdd(La + idx[j], ((sg >> j) & 1u) ? -mag : mag);             // Z^(k)_n += L^(k)_mn
+    }
+}
+
+template <bool ES>
+__global__ void __launch_bounds__(256) k_stream_iter_f(const StreamArgs a, int k) {
+    const int tile = blockIdx.y, lane = threadIdx.x & 31;
+    const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nwg = gridDim.x * (blockDim.x >> 5);
+    const float *Lp = (const float *)a.Lb[(k - 1) % 3];
+    float *La = (float *)a.Lb[k % 3];
+    uint32_t *Ln = a.Lb[(k + 1) % 3];
+    bool frozen = false;
+    if (ES) {
+        frozen = (a.done[tile * 32 + lane] & 1u) != 0;
+        if (__all_sync(0xFFFFFFFFu, frozen)) return;
+    }
+    if (k < a.K) {
+        for (int n = wg; n < a.N; n += nwg) {
+            const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
+            if (!frozen) __stcg(Ln + idx, __ldcg(a.Z0 + idx));
+        }
+    }
+    uint32_t synd = 0;
+    const bool first_iter = (k == 1);
+    for (int m = wg; m < a.M; m += nwg) {
+        const int e0 = __ldg(a.row_ptr + m), dc = __ldg(a.row_ptr + m + 1) - e0;
+        switch (dc) {
+        case 2: stream_row_f<2, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 3: stream_row_f<3, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 4: stream_row_f<4, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 5: stream_row_f<5, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 6: stream_row_f<6, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 7: stream_row_f<7, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 8: stream_row_f<8, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 9: stream_row_f<9, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 10: stream_row_f<10, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 11: stream_row_f<11, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 12: stream_row_f<12, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 13: stream_row_f<13, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 14: stream_row_f<14, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 15: stream_row_f<15, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        case 16: stream_row_f<16, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
+        }
+    }
+    if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
+}
+
+// -------------------------------------------------------------- error counters
+__global__ void k_count_errors(int64_t nframes, int wpf, const uint32_t *hb, const uint8_t *ok, const int32_t *it,
+                               unsigned long long *cnt) {
+    unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nframes; f += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long be = 0;
+        for (int w = 0; w < wpf; ++w) be += __popc(hb[f * wpf + w]);
+        c0 += be;
+        c1 += be ? 1 : 0;
+        c2 += (be && ok[f]) ? 1 : 0;
+        c3 += ok[f] ? 0 : 1;
+        c4 += it ? (unsigned long long)it[f] : 0ull;
+    }
+    for (int o = 16; o; o >>= 1) {
+        c0 += __shfl_xor_sync(0xFFFFFFFFu, c0, o);
+        c1 += __shfl_xor_sync(0xFFFFFFFFu, c1, o);
+        c2 += __shfl_xor_sync(0xFFFFFFFFu, c2, o);
+        c3 += __shfl_xor_sync(0xFFFFFFFFu, c3, o);
+        c4 += __shfl_xor_sync(0xFFFFFFFFu, c4, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (c0) atomicAdd(cnt + 0, c0);
+        if (c1) atomicAdd(cnt + 1, c1);
+        if (c2) atomicAdd(cnt + 2, c2);
+        if (c3) atomicAdd(cnt + 3, c3);
+        if (c4) atomicAdd(cnt + 4, c4);
+    }
+}
+
+}  // namespace ldpc

@@ -1,0 +1,753 @@
+// ldpc_api.cu -- C ABI of libldpc.so (declarations and contracts: include/ldpc.h).
+//
+// Host side: validation of H (SPEC-style invariants), the
+// device code structure (check->variable addressing only), the
+// conflict-free row schedule / QC circulant table used by the resident kernel,
+// path selection and launches.  No torch types, no allocation in decode calls.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ldpc.h"
+#include "k_resident.cuh"
+#include "k_stream.cuh"
+
+using namespace ldpc;
+
+namespace {
+
+thread_local std::string g_detail;
+thread_local int32_t g_launches = 0;
+
+ldpc_status fail(ldpc_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_detail = buf;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                            \
+    do {                                                                                          \
+        cudaError_t _e = (expr);                                                                  \
+        if (_e != cudaSuccess) return fail(LDPC_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+struct ldpc_code {
+    int device = 0;
+    int sm_count = 0;
+    size_t smem_optin = 0;
+    int N = 0, M = 0;
+    int64_t E = 0;
+    int max_dc = 0, max_dv = 0;
+    // device CSR (stream kernels)
+    int32_t *d_row_ptr = nullptr, *d_col_idx = nullptr;
+    // resident schedule
+    bool qc = false;
+    int Z = 0, mb = 0, nb = 0;
+    int nbatch = 0, res_threads = 0;
+    bool res_ok = false;        // resident path possible (smem, degrees)
+    size_t res_smem = 0;
+    int nqent = 0;
+    uint32_t *d_qent = nullptr;
+    int32_t *d_qbptr = nullptr;
+    int32_t *d_bptr = nullptr, *d_colT = nullptr;
+    uint8_t *d_dcT = nullptr;
+    cudaStream_t aux[2] = {nullptr, nullptr};
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+};
+
+// ------------------------------------------------------------------ create
+static ldpc_status validate_desc(const ldpc_code_desc *d, std::vector<int> &coldeg) {
+    if (!d || !d->row_ptr || !d->col_idx) return fail(LDPC_ERR_INVALID_ARG, "NULL descriptor or CSR pointer");
+    const int N = d->n_vars, M = d->n_checks;
+    if (N < 2 || M < 1) return fail(LDPC_ERR_INVALID_CODE, "need n_vars >= 2 and n_checks >= 1 (got %d, %d)", N, M);
+    if (d->row_ptr[0] != 0) return fail(LDPC_ERR_INVALID_CODE, "row_ptr[0] = %d, must be 0", d->row_ptr[0]);
+    coldeg.assign(N, 0);
+    for (int m = 0; m < M; ++m) {
+        const int32_t a = d->row_ptr[m], b = d->row_ptr[m + 1];
+        if (b < a) return fail(LDPC_ERR_INVALID_CODE, "row_ptr decreases at row %d", m);
+        if (b - a < 2) return fail(LDPC_ERR_INVALID_CODE, "row %d: degree %d < 2", m, b - a);
+        for (int32_t e = a; e < b; ++e) {
+            const int32_t c = d->col_idx[e];
+            if (c < 0 || c >= N) return fail(LDPC_ERR_INVALID_CODE, "row %d: column %d out of range [0,%d)", m, c, N);
+            if (e > a && c <= d->col_idx[e - 1]) {
+                if (c == d->col_idx[e - 1]) return fail(LDPC_ERR_INVALID_CODE, "row %d: duplicate column %d", m, c);
+                return fail(LDPC_ERR_INVALID_CODE, "row %d: columns not strictly increasing at %d", m, c);
+            }
+            coldeg[c]++;
+        }
+    }
+    for (int n = 0; n < N; ++n)
+        if (coldeg[n] == 0) return fail(LDPC_ERR_INVALID_CODE, "column %d has degree 0", n);
+    if (d->qc_z > 0) {
+        const int Z = d->qc_z;
+        if (!d->qc_shift) return fail(LDPC_ERR_INVALID_ARG, "qc_z > 0 but qc_shift is NULL");
+        if ((int64_t)d->qc_rows * Z != M || (int64_t)d->qc_cols * Z != N)
+            return fail(LDPC_ERR_INVALID_CODE, "QC shape %dx%d (Z=%d) inconsistent with M=%d N=%d", d->qc_rows,
+                        d->qc_cols, Z, M, N);
+        std::vector<int32_t> row;
+        for (int i = 0; i < d->qc_rows; ++i) {
+            for (int j = 0; j < d->qc_cols; ++j) {
+                const int s = d->qc_shift[(size_t)i * d->qc_cols + j];
+                if (s < -1 || s >= Z) return fail(LDPC_ERR_INVALID_CODE, "QC shift (%d,%d) = %d out of range", i, j, s);
+            }
+            for (int r = 0; r < Z; ++r) {
+                row.clear();
+                for (int j = 0; j < d->qc_cols; ++j) {
+                    const int s = d->qc_shift[(size_t)i * d->qc_cols + j];
+                    if (s >= 0) row.push_back(j * Z + (r + s) % Z);
+                }
+                std::sort(row.begin(), row.end());
+                const int m = i * Z + r;
+                const int32_t a = d->row_ptr[m], b = d->row_ptr[m + 1];
+                if ((int)row.size() != b - a || !std::equal(row.begin(), row.end(), d->col_idx + a))
+                    return fail(LDPC_ERR_INVALID_CODE, "row %d differs from the QC shift-table expansion", m);
+            }
+        }
+    }
+    return LDPC_OK;
+}
+
+template <typename T>
+static ldpc_status upload(T **dst, const T *src, size_t n) {
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc((void **)dst, n * sizeof(T));
+    if (e != cudaSuccess) return fail(LDPC_ERR_NO_MEMORY, "cudaMalloc(%zu): %s", n * sizeof(T), cudaGetErrorString(e));
+    if (src) CUDA_TRY(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+    return LDPC_OK;
+}
+
+static void free_code(ldpc_code *c) {
+    if (!c) return;
+    cudaFree(c->d_row_ptr);
+    cudaFree(c->d_col_idx);
+    cudaFree(c->d_qent);
+    cudaFree(c->d_qbptr);
+    cudaFree(c->d_bptr);
+    cudaFree(c->d_colT);
+    cudaFree(c->d_dcT);
+    for (auto &s : c->aux)
+        if (s) cudaStreamDestroy(s);
+    for (auto &e : c->ev)
+        if (e) cudaEventDestroy(e);
+    delete c;
+}
+
+extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_device, ldpc_code **out) {
+    g_detail.clear();
+    if (!out) return fail(LDPC_ERR_INVALID_ARG, "out is NULL");
+    std::vector<int> coldeg;
+    ldpc_status st = validate_desc(desc, coldeg);
+    if (st != LDPC_OK) return st;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev)
+        return fail(LDPC_ERR_CUDA, "CUDA device %d not available (%d devices)", cuda_device, ndev);
+    DeviceGuard guard(cuda_device);
+    ldpc_code *c = new ldpc_code();
+    c->device = cuda_device;
+    c->N = desc->n_vars;
+    c->M = desc->n_checks;
+    c->E = desc->row_ptr[c->M];
+    for (int m = 0; m < c->M; ++m) c->max_dc = std::max(c->max_dc, desc->row_ptr[m + 1] - desc->row_ptr[m]);
+    for (int n = 0; n < c->N; ++n) c->max_dv = std::max(c->max_dv, coldeg[n]);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) {
+        free_code(c);
+        return fail(LDPC_ERR_CUDA, "cudaGetDeviceProperties failed");
+    }
+    c->sm_count = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    if ((st = upload(&c->d_row_ptr, desc->row_ptr, (size_t)c->M + 1)) != LDPC_OK ||
+        (st = upload(&c->d_col_idx, desc->col_idx, (size_t)c->E)) != LDPC_OK) {
+        free_code(c);
+        return st;
+    }
+    const int N = c->N, M = c->M;
+    // ---------- resident schedule (only when a frame pair's double buffer fits in shared memory)
+    if (c->max_dc <= kMaxDC && (size_t)2 * N * 4 + 16384 <= c->smem_optin) {
+        if (desc->qc_z > 0 && desc->qc_z <= 256 && N < 65536) {
+            c->qc = true;
+            c->Z = desc->qc_z;
+            c->mb = desc->qc_rows;
+            c->nb = desc->qc_cols;
+            std::vector<uint32_t> qent;
+            std::vector<int32_t> qbptr(1, 0);
+            std::vector<char> seen(c->nb, 0);
+            for (int i = 0; i < c->mb; ++i) {
+                for (int j = 0; j < c->nb; ++j) {
+                    const int s = desc->qc_shift[(size_t)i * c->nb + j];
+                    if (s < 0) continue;
+                    const uint32_t first = seen[j] ? 0u : 1u;
+                    seen[j] = 1;
+                    qent.push_back((uint32_t)(j * c->Z) | ((uint32_t)s << 16) | (first << 31));
+                }
+                qbptr.push_back((int32_t)qent.size());
+            }
+            c->nqent = (int)qent.size();
+            c->nbatch = c->mb;
+            c->res_threads = ((c->Z + 31) / 32) * 32;
+            if ((st = upload(&c->d_qent, qent.data(), qent.size())) != LDPC_OK ||
+                (st = upload(&c->d_qbptr, qbptr.data(), qbptr.size())) != LDPC_OK) {
+                free_code(c);
+                return st;
+            }
+            c->res_smem = (size_t)2 * N * 4 + (size_t)c->nqent * 4 + (size_t)(c->nbatch + 1) * 4;
+        } else {
+            // greedy colouring: rows of one colour share no variable
+            std::vector<std::vector<int>> classes;
+            std::vector<std::vector<uint64_t>> used;   // per colour: bitset over variables
+            std::vector<int> color(M);
+            const size_t words = ((size_t)N + 63) / 64;
+            for (int m = 0; m < M; ++m) {
+                int cc = 0;
+                for (;; ++cc) {
+                    if (cc == (int)classes.size()) {
+                        classes.emplace_back();
+                        used.emplace_back(words, 0ull);
+                    }
+                    bool okc = true;
+                    for (int32_t e = desc->row_ptr[m]; e < desc->row_ptr[m + 1] && okc; ++e) {
+                        const int n = desc->col_idx[e];
+                        if (used[cc][n >> 6] >> (n & 63) & 1ull) okc = false;
+                    }
+                    if (okc && classes[cc].size() < 256) break;
+                }
+                classes[cc].push_back(m);
+                for (int32_t e = desc->row_ptr[m]; e < desc->row_ptr[m + 1]; ++e) {
+                    const int n = desc->col_idx[e];
+                    used[cc][n >> 6] |= 1ull << (n & 63);
+                }
+            }
+            std::vector<int32_t> bptr(1, 0), colT((size_t)kMaxDC * M, -1);
+            std::vector<uint8_t> dcT(M);
+            std::vector<char> seen(N, 0);
+            int p = 0, maxb = 0;
+            for (auto &cl : classes) {
+                for (int m : cl) {
+                    const int32_t a = desc->row_ptr[m], b = desc->row_ptr[m + 1];
+                    dcT[p] = (uint8_t)(b - a);
+                    for (int32_t e = a; e < b; ++e) {
+                        const int n = desc->col_idx[e];
+                        uint32_t v = (uint32_t)n;
+                        if (!seen[n]) { v |= 0x80000000u; seen[n] = 1; }
+                        colT[(size_t)(e - a) * M + p] = (int32_t)v;
+                    }
+                    ++p;
+                }
+                bptr.push_back(p);
+                maxb = std::max(maxb, (int)cl.size());
+            }
+            c->nbatch = (int)classes.size();
+            c->res_threads = ((maxb + 31) / 32) * 32;
+            if ((st = upload(&c->d_bptr, bptr.data(), bptr.size())) != LDPC_OK ||
+                (st = upload(&c->d_colT, colT.data(), colT.size())) != LDPC_OK ||
+                (st = upload(&c->d_dcT, dcT.data(), dcT.size())) != LDPC_OK) {
+                free_code(c);
+                return st;
+            }
+            c->res_smem = (size_t)2 * N * 4;
+        }
+        c->res_ok = c->res_smem <= c->smem_optin && c->res_threads <= 256;
+    }
+    for (auto &s : c->aux)
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+            free_code(c);
+            return fail(LDPC_ERR_CUDA, "cudaStreamCreate failed");
+        }
+    for (auto &e : c->ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            free_code(c);
+            return fail(LDPC_ERR_CUDA, "cudaEventCreate failed");
+        }
+    *out = c;
+    return LDPC_OK;
+}
+
+extern "C" void ldpc_code_destroy(ldpc_code *code) {
+    if (!code) return;
+    DeviceGuard guard(code->device);
+    free_code(code);
+}
+
+extern "C" ldpc_status ldpc_code_query(const ldpc_code *c, int32_t *n_vars, int32_t *n_checks, int64_t *n_edges,
+                                       int32_t *max_dc, int32_t *max_dv) {
+    if (!c) return fail(LDPC_ERR_INVALID_ARG, "code is NULL");
+    if (n_vars) *n_vars = c->N;
+    if (n_checks) *n_checks = c->M;
+    if (n_edges) *n_edges = c->E;
+    if (max_dc) *max_dc = c->max_dc;
+    if (max_dv) *max_dv = c->max_dv;
+    return LDPC_OK;
+}
+
+// ------------------------------------------------------------------ planning
+namespace {
+
+enum Path { PATH_RESIDENT = 0, PATH_STREAM_I = 1, PATH_STREAM_F = 2 };
+
+struct Plan {
+    Path path;
+    int Q = 0, beta = 0, fmt = FMT_C16;
+    float alpha = 1.f, betaf = 0.f;
+    // resident
+    int grid = 0;
+    size_t slot_words = 0;
+    // stream
+    int tile = 64, ntiles = 0;
+    size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
+    size_t ws_bytes = 0;
+};
+
+template <bool QC, bool ES, int FMT, typename TIN>
+cudaError_t res_occupancy(const ldpc_code *c, int *blocks) {
+    auto kern = k_resident<QC, ES, FMT, TIN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kern, c->res_threads, c->res_smem);
+}
+
+template <bool QC, bool ES, int FMT>
+cudaError_t res_occupancy_t(const ldpc_code *c, int llr_type, int *blocks) {
+    return llr_type == LDPC_LLR_I8 ? res_occupancy<QC, ES, FMT, int8_t>(c, blocks)
+                                   : res_occupancy<QC, ES, FMT, int16_t>(c, blocks);
+}
+
+cudaError_t res_occupancy_any(const ldpc_code *c, const ldpc_decode_params *p, int fmt, int *blocks) {
+    const bool es = p->early_stop != 0;
+    if (c->qc) {
+        if (es) return fmt == FMT_C16 ? res_occupancy_t<true, true, FMT_C16>(c, p->llr_type, blocks)
+                                      : res_occupancy_t<true, true, FMT_1BIT>(c, p->llr_type, blocks);
+        return fmt == FMT_C16 ? res_occupancy_t<true, false, FMT_C16>(c, p->llr_type, blocks)
+                              : res_occupancy_t<true, false, FMT_1BIT>(c, p->llr_type, blocks);
+    }
+    if (es) return fmt == FMT_C16 ? res_occupancy_t<false, true, FMT_C16>(c, p->llr_type, blocks)
+                                  : res_occupancy_t<false, true, FMT_1BIT>(c, p->llr_type, blocks);
+    return fmt == FMT_C16 ? res_occupancy_t<false, false, FMT_C16>(c, p->llr_type, blocks)
+                          : res_occupancy_t<false, false, FMT_1BIT>(c, p->llr_type, blocks);
+}
+
+ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p, Plan &pl) {
+    if (!c) return fail(LDPC_ERR_INVALID_ARG, "code is NULL");
+    if (!p) return fail(LDPC_ERR_INVALID_ARG, "params is NULL");
+    if (F < 0) return fail(LDPC_ERR_INVALID_ARG, "n_frames < 0");
+    if (F > (int64_t)1 << 31) return fail(LDPC_ERR_UNSUPPORTED, "n_frames > 2^31");
+    if (p->max_iter < 1) return fail(LDPC_ERR_INVALID_ARG, "max_iter must be >= 1");
+    if (p->early_stop != 0 && p->early_stop != 1) return fail(LDPC_ERR_INVALID_ARG, "early_stop must be 0 or 1");
+    if (p->reserved != 0) return fail(LDPC_ERR_INVALID_ARG, "reserved must be 0");
+    if (p->msg_format != LDPC_MSG_COMPACT && p->msg_format != LDPC_MSG_1BIT)
+        return fail(LDPC_ERR_INVALID_ARG, "bad msg_format %d", p->msg_format);
+    if (p->variant != LDPC_MINSUM_OFFSET && p->variant != LDPC_MINSUM_NORMALIZED)
+        return fail(LDPC_ERR_INVALID_ARG, "bad variant %d", p->variant);
+    if (p->llr_type == LDPC_LLR_F32) {
+        if (p->msg_format == LDPC_MSG_1BIT) return fail(LDPC_ERR_UNSUPPORTED, "1-bit messages need integer LLRs");
+        if (c->max_dc > 16) return fail(LDPC_ERR_UNSUPPORTED, "F32 path supports row degree <= 16 (max %d)", c->max_dc);
+        if (p->variant == LDPC_MINSUM_NORMALIZED) {
+            if (!(p->alpha > 0.f && p->alpha <= 1.f)) return fail(LDPC_ERR_INVALID_ARG, "alpha must be in (0,1]");
+            pl.alpha = p->alpha;
+            pl.betaf = 0.f;
+        } else {
+            if (!(p->offset_f >= 0.f)) return fail(LDPC_ERR_INVALID_ARG, "offset_f must be >= 0");
+            pl.alpha = 1.f;
+            pl.betaf = p->offset_f;
+        }
+        pl.path = PATH_STREAM_F;
+        pl.tile = 32;
+    } else if (p->llr_type == LDPC_LLR_I16 || p->llr_type == LDPC_LLR_I8) {
+        if (p->variant == LDPC_MINSUM_NORMALIZED && p->alpha != 1.f)
+            return fail(LDPC_ERR_UNSUPPORTED, "normalized min-sum with integer LLRs is not implemented (use F32)");
+        if (p->offset_raw < 0 || p->offset_raw > 16383) return fail(LDPC_ERR_INVALID_ARG, "offset_raw out of range");
+        if (c->max_dc > kMaxDC) return fail(LDPC_ERR_UNSUPPORTED, "integer paths support row degree <= %d (max %d)", kMaxDC, c->max_dc);
+        pl.fmt = p->msg_format == LDPC_MSG_1BIT ? FMT_1BIT : FMT_C16;
+        pl.Q = p->clamp_raw > 0 ? p->clamp_raw : (p->llr_type == LDPC_LLR_I16 ? 511 : 127);
+        const int qmax = pl.fmt == FMT_1BIT ? 127 : 511;
+        if (pl.Q > qmax) return fail(LDPC_ERR_UNSUPPORTED, "clamp Q=%d exceeds %d for this message format", pl.Q, qmax);
+        if ((int64_t)2 * pl.Q * (c->max_dv + 2) > 32767)
+            return fail(LDPC_ERR_UNSUPPORTED, "2*Q*(max_dv+2) = %lld > 32767: posteriors would overflow 16-bit lanes",
+                        (long long)2 * pl.Q * (c->max_dv + 2));
+        pl.beta = p->offset_raw;
+        // LDPC_FORCE_STREAM=1 (test hook) routes integer decodes through the streaming kernels
+        const char *force = getenv("LDPC_FORCE_STREAM");
+        pl.path = (c->res_ok && !(force && force[0] == '1')) ? PATH_RESIDENT : PATH_STREAM_I;
+        pl.tile = 64;
+    } else {
+        return fail(LDPC_ERR_INVALID_ARG, "bad llr_type %d", p->llr_type);
+    }
+    const int64_t npairs = (F + 1) / 2;
+    if (pl.path == PATH_RESIDENT) {
+        int blocks = 0;
+        cudaError_t e = res_occupancy_any(c, p, pl.fmt, &blocks);
+        if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "occupancy query: %s", cudaGetErrorString(e));
+        if (blocks < 1) return fail(LDPC_ERR_UNSUPPORTED, "resident kernel does not fit on an SM");
+        pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)blocks * c->sm_count);
+        pl.slot_words = (size_t)c->N + (size_t)(pl.fmt == FMT_C16 ? 3 : 2) * c->M;
+        pl.slot_words = (pl.slot_words + 63) & ~(size_t)63;
+        pl.ws_bytes = align256((size_t)pl.grid * pl.slot_words * 4);
+    } else {
+        pl.ntiles = (int)((F + pl.tile - 1) / pl.tile);
+        const size_t plane = (size_t)pl.ntiles * c->N * 32 * 4;
+        const int sw = pl.path == PATH_STREAM_F ? 3 : (pl.fmt == FMT_C16 ? 3 : 2);
+        size_t off = 0;
+        pl.off_z0 = off; off += align256(plane);
+        for (int i = 0; i < 3; ++i) { pl.off_lb[i] = off; off += align256(plane); }
+        pl.off_st = off; off += align256((size_t)pl.ntiles * sw * c->M * 32 * 4);
+        pl.off_synd = off; off += align256((size_t)pl.ntiles * 32 * 4);
+        pl.off_done = off; off += align256((size_t)pl.ntiles * 32 * 4);
+        pl.off_it = off; off += align256((size_t)pl.ntiles * pl.tile * 4);
+        pl.off_ok = off; off += align256((size_t)pl.ntiles * pl.tile);
+        pl.ws_bytes = off;
+    }
+    return LDPC_OK;
+}
+
+template <bool QC, bool ES, int FMT, typename TIN>
+cudaError_t launch_res(const ldpc_code *c, const Plan &pl, const ResArgs &a, cudaStream_t s) {
+    auto kern = k_resident<QC, ES, FMT, TIN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem);
+    if (e != cudaSuccess) return e;
+    kern<<<pl.grid, c->res_threads, c->res_smem, s>>>(a);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+template <bool QC, bool ES, int FMT>
+cudaError_t launch_res_t(const ldpc_code *c, const Plan &pl, const ResArgs &a, int llr_type, cudaStream_t s) {
+    return llr_type == LDPC_LLR_I8 ? launch_res<QC, ES, FMT, int8_t>(c, pl, a, s)
+                                   : launch_res<QC, ES, FMT, int16_t>(c, pl, a, s);
+}
+
+cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_params *p, int64_t F,
+                         const void *llr, uint32_t *hb, void *post, uint8_t *ok, int32_t *it, void *ws,
+                         cudaStream_t s) {
+    ResArgs a{};
+    a.N = c->N;
+    a.M = c->M;
+    a.npairs = (int)((F + 1) / 2);
+    a.nframes = (int)F;
+    a.K = p->max_iter;
+    a.Qsat = pl.Q;
+    a.wpf = (c->N + 31) / 32;
+    a.nbeta2 = pack2(-2 * pl.beta, -2 * pl.beta);
+    a.q2 = pack2(2 * pl.Q, 2 * pl.Q);
+    a.llr = llr;
+    a.hard_bits = hb;
+    a.post = (int16_t *)post;
+    a.ok = ok;
+    a.iters = it;
+    a.ws = (uint32_t *)ws;
+    a.slot_words = pl.slot_words;
+    a.nbatch = c->nbatch;
+    a.bptr = c->d_bptr;
+    a.colT = c->d_colT;
+    a.dcT = c->d_dcT;
+    a.Z = c->Z;
+    a.qent = c->d_qent;
+    a.qbptr = c->d_qbptr;
+    a.nqent = c->nqent;
+    const bool es = p->early_stop != 0;
+    const int t = p->llr_type;
+    if (c->qc) {
+        if (es) return pl.fmt == FMT_C16 ? launch_res_t<true, true, FMT_C16>(c, pl, a, t, s)
+                                         : launch_res_t<true, true, FMT_1BIT>(c, pl, a, t, s);
+        return pl.fmt == FMT_C16 ? launch_res_t<true, false, FMT_C16>(c, pl, a, t, s)
+                                 : launch_res_t<true, false, FMT_1BIT>(c, pl, a, t, s);
+    }
+    if (es) return pl.fmt == FMT_C16 ? launch_res_t<false, true, FMT_C16>(c, pl, a, t, s)
+                                     : launch_res_t<false, true, FMT_1BIT>(c, pl, a, t, s);
+    return pl.fmt == FMT_C16 ? launch_res_t<false, false, FMT_C16>(c, pl, a, t, s)
+                             : launch_res_t<false, false, FMT_1BIT>(c, pl, a, t, s);
+}
+
+template <typename F>
+cudaError_t launch(F f) {
+    f();
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_params *p, int64_t F, const void *llr,
+                       uint32_t *hb, void *post, uint8_t *ok, int32_t *it, void *ws, cudaStream_t s) {
+    char *w = (char *)ws;
+    StreamArgs a{};
+    a.N = c->N;
+    a.M = c->M;
+    a.ntiles = pl.ntiles;
+    a.nframes = (int)F;
+    a.K = p->max_iter;
+    a.Qsat = pl.Q;
+    a.wpf = (c->N + 31) / 32;
+    a.nbeta2 = pack2(-2 * pl.beta, -2 * pl.beta);
+    a.q2 = pack2(2 * pl.Q, 2 * pl.Q);
+    a.alpha = pl.alpha;
+    a.beta = pl.betaf;
+    a.row_ptr = c->d_row_ptr;
+    a.col_idx = c->d_col_idx;
+    a.llr = llr;
+    a.Z0 = (uint32_t *)(w + pl.off_z0);
+    for (int i = 0; i < 3; ++i) a.Lb[i] = (uint32_t *)(w + pl.off_lb[i]);
+    a.st = (uint32_t *)(w + pl.off_st);
+    a.synd = (uint32_t *)(w + pl.off_synd);
+    a.done = (uint32_t *)(w + pl.off_done);
+    a.it_ws = (int32_t *)(w + pl.off_it);
+    a.ok_ws = (uint8_t *)(w + pl.off_ok);
+    a.hard_bits = hb;
+    a.post = post;
+    a.ok = ok;
+    a.iters = it;
+    cudaError_t e;
+    // synd, done (contiguous) and per-frame flags
+    if ((e = cudaMemsetAsync(a.synd, 0, pl.off_it - pl.off_synd, s)) != cudaSuccess) return e;
+    const bool es = p->early_stop != 0;
+    const bool pair = pl.path == PATH_STREAM_I;
+    const int nwarps_per_block = 8;
+    dim3 gi((unsigned)std::min<int64_t>(((int64_t)c->N + 7) / 8, 1024), (unsigned)pl.ntiles);
+    // ~8 rows per warp per launch
+    const int rows_per_block = nwarps_per_block * 8;
+    dim3 gr((unsigned)std::max(1, (c->M + rows_per_block - 1) / rows_per_block), (unsigned)pl.ntiles);
+    if (pair) {
+        if (p->llr_type == LDPC_LLR_I8) e = launch([&] { k_stream_ingest_i<int8_t><<<gi, 256, 0, s>>>(a); });
+        else e = launch([&] { k_stream_ingest_i<int16_t><<<gi, 256, 0, s>>>(a); });
+    } else {
+        e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); });
+    }
+    if (e != cudaSuccess) return e;
+    const unsigned fgrid = (unsigned)((pl.ntiles * 32 + 255) / 256);
+    for (int k = 1; k <= p->max_iter; ++k) {
+        if (pair) {
+            if (pl.fmt == FMT_C16) {
+                if (es) e = launch([&] { k_stream_iter_i<FMT_C16, true><<<gr, 256, 0, s>>>(a, k); });
+                else e = launch([&] { k_stream_iter_i<FMT_C16, false><<<gr, 256, 0, s>>>(a, k); });
+            } else {
+                if (es) e = launch([&] { k_stream_iter_i<FMT_1BIT, true><<<gr, 256, 0, s>>>(a, k); });
+                else e = launch([&] { k_stream_iter_i<FMT_1BIT, false><<<gr, 256, 0, s>>>(a, k); });
+            }
+        } else {
+            if (es) e = launch([&] { k_stream_iter_f<true><<<gr, 256, 0, s>>>(a, k); });
+            else e = launch([&] { k_stream_iter_f<false><<<gr, 256, 0, s>>>(a, k); });
+        }
+        if (e != cudaSuccess) return e;
+        if (es) {
+            if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); });
+            else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); });
+            if (e != cudaSuccess) return e;
+        }
+    }
+    const int kb = p->max_iter % 3;
+    if (pair) e = launch([&] { k_stream_syndrome<true><<<gr, 256, 0, s>>>(a, kb); });
+    else e = launch([&] { k_stream_syndrome<false><<<gr, 256, 0, s>>>(a, kb); });
+    if (e != cudaSuccess) return e;
+    if (pair) e = launch([&] { k_stream_finalize_flags<true><<<fgrid, 256, 0, s>>>(a); });
+    else e = launch([&] { k_stream_finalize_flags<false><<<fgrid, 256, 0, s>>>(a); });
+    if (e != cudaSuccess) return e;
+    dim3 go((unsigned)a.wpf, (unsigned)pl.ntiles);
+    if (pair) e = launch([&] { k_stream_output<true><<<go, 256, 0, s>>>(a); });
+    else e = launch([&] { k_stream_output<false><<<go, 256, 0, s>>>(a); });
+    return e;
+}
+
+ldpc_status decode_device(const ldpc_code *c, const ldpc_decode_params *p, int64_t F, const void *llr, uint32_t *hb,
+                          void *post, uint8_t *ok, int32_t *it, void *ws, size_t wsb, cudaStream_t s,
+                          const Plan &pl) {
+    if (F == 0) return LDPC_OK;
+    if (!llr || !hb || !ok) return fail(LDPC_ERR_INVALID_ARG, "llr, hard_bits and syndrome_ok must be non-NULL");
+    if (!ws || wsb < pl.ws_bytes)
+        return fail(LDPC_ERR_INVALID_ARG, "workspace too small: %zu < %zu bytes", wsb, pl.ws_bytes);
+    if (((uintptr_t)ws & 255) != 0) return fail(LDPC_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+    cudaError_t e = pl.path == PATH_RESIDENT ? run_resident(c, pl, p, F, llr, hb, post, ok, it, ws, s)
+                                             : run_stream(c, pl, p, F, llr, hb, post, ok, it, ws, s);
+    if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
+    return LDPC_OK;
+}
+
+}  // namespace
+
+extern "C" ldpc_status ldpc_decode_workspace_size(const ldpc_code *code, int64_t n_frames,
+                                                  const ldpc_decode_params *params, size_t *bytes) {
+    g_detail.clear();
+    if (!bytes) return fail(LDPC_ERR_INVALID_ARG, "bytes is NULL");
+    if (!code) return fail(LDPC_ERR_INVALID_ARG, "code is NULL");
+    DeviceGuard guard(code->device);
+    Plan pl;
+    ldpc_status st = make_plan(code, n_frames, params, pl);
+    if (st != LDPC_OK) return st;
+    *bytes = n_frames == 0 ? 0 : pl.ws_bytes;
+    return LDPC_OK;
+}
+
+extern "C" ldpc_status ldpc_decode_batch(const ldpc_code *code, const ldpc_decode_params *params, int64_t n_frames,
+                                         const void *llr, uint32_t *hard_bits, void *posteriors,
+                                         uint8_t *syndrome_ok, int32_t *iterations_used, void *workspace,
+                                         size_t workspace_bytes, void *stream) {
+    g_detail.clear();
+    g_launches = 0;
+    if (!code) return fail(LDPC_ERR_INVALID_ARG, "code is NULL");
+    DeviceGuard guard(code->device);
+    Plan pl;
+    ldpc_status st = make_plan(code, n_frames, params, pl);
+    if (st != LDPC_OK) return st;
+    return decode_device(code, params, n_frames, llr, hard_bits, posteriors, syndrome_ok, iterations_used, workspace,
+                         workspace_bytes, (cudaStream_t)stream, pl);
+}
+
+// ------------------------------------------------------------------ host I/O
+namespace {
+struct HostLayout {
+    int64_t chunk = 0, nchunks = 0;
+    size_t elt = 2, post_elt = 2, wpf = 0;
+    size_t off_llr = 0, off_hb = 0, off_post = 0, off_ok = 0, off_it = 0, off_ws[2] = {0, 0};
+    size_t chunk_ws = 0, total = 0;
+};
+
+ldpc_status host_layout(const ldpc_code *c, int64_t F, const ldpc_decode_params *p, HostLayout &h) {
+    h.nchunks = F >= 4096 ? 4 : 1;
+    h.chunk = (F + h.nchunks - 1) / h.nchunks;
+    h.chunk = ((h.chunk + 63) / 64) * 64;
+    if (h.chunk == 0) h.chunk = 64;
+    h.nchunks = (F + h.chunk - 1) / h.chunk;
+    Plan pl;
+    ldpc_status st = make_plan(c, h.chunk, p, pl);
+    if (st != LDPC_OK) return st;
+    h.elt = p->llr_type == LDPC_LLR_F32 ? 4 : (p->llr_type == LDPC_LLR_I8 ? 1 : 2);
+    h.post_elt = p->llr_type == LDPC_LLR_F32 ? 4 : 2;
+    h.wpf = ((size_t)c->N + 31) / 32;
+    size_t off = 0;
+    h.off_llr = off; off += align256((size_t)F * c->N * h.elt);
+    h.off_hb = off; off += align256((size_t)F * h.wpf * 4);
+    h.off_post = off; off += align256((size_t)F * c->N * h.post_elt);
+    h.off_ok = off; off += align256((size_t)F);
+    h.off_it = off; off += align256((size_t)F * 4);
+    h.chunk_ws = pl.ws_bytes;
+    h.off_ws[0] = off; off += align256(pl.ws_bytes);
+    h.off_ws[1] = off; off += align256(pl.ws_bytes);
+    h.total = off;
+    return LDPC_OK;
+}
+}  // namespace
+
+extern "C" ldpc_status ldpc_decode_host_workspace_size(const ldpc_code *code, int64_t n_frames,
+                                                       const ldpc_decode_params *params, size_t *bytes) {
+    g_detail.clear();
+    if (!bytes || !code) return fail(LDPC_ERR_INVALID_ARG, "NULL argument");
+    DeviceGuard guard(code->device);
+    if (n_frames == 0) { *bytes = 0; return LDPC_OK; }
+    HostLayout h;
+    ldpc_status st = host_layout(code, n_frames, params, h);
+    if (st != LDPC_OK) return st;
+    *bytes = h.total;
+    return LDPC_OK;
+}
+
+extern "C" ldpc_status ldpc_decode_batch_host(const ldpc_code *code, const ldpc_decode_params *params,
+                                              int64_t n_frames, const void *llr_host, uint32_t *hard_bits_host,
+                                              void *posteriors_host, uint8_t *syndrome_ok_host,
+                                              int32_t *iterations_used_host, void *workspace, size_t workspace_bytes,
+                                              void *stream) {
+    g_detail.clear();
+    g_launches = 0;
+    if (!code) return fail(LDPC_ERR_INVALID_ARG, "code is NULL");
+    if (n_frames == 0) return LDPC_OK;
+    if (!llr_host || !hard_bits_host || !syndrome_ok_host)
+        return fail(LDPC_ERR_INVALID_ARG, "llr, hard_bits and syndrome_ok must be non-NULL");
+    DeviceGuard guard(code->device);
+    HostLayout h;
+    ldpc_status st = host_layout(code, n_frames, params, h);
+    if (st != LDPC_OK) return st;
+    if (!workspace || workspace_bytes < h.total)
+        return fail(LDPC_ERR_INVALID_ARG, "workspace too small: %zu < %zu bytes", workspace_bytes, h.total);
+    if (((uintptr_t)workspace & 255) != 0) return fail(LDPC_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+    char *w = (char *)workspace;
+    cudaStream_t us = (cudaStream_t)stream;
+    CUDA_TRY(cudaEventRecord(code->ev[0], us));
+    for (auto s : code->aux) CUDA_TRY(cudaStreamWaitEvent(s, code->ev[0], 0));
+    int32_t launches = 0;
+    const int N = code->N;
+    for (int64_t ci = 0; ci < h.nchunks; ++ci) {
+        cudaStream_t s = code->aux[ci & 1];
+        const int64_t f0 = ci * h.chunk, nf = std::min<int64_t>(h.chunk, n_frames - f0);
+        char *dl = w + h.off_llr + (size_t)f0 * N * h.elt;
+        uint32_t *dhb = (uint32_t *)(w + h.off_hb) + (size_t)f0 * h.wpf;
+        char *dpost = posteriors_host ? w + h.off_post + (size_t)f0 * N * h.post_elt : nullptr;
+        uint8_t *dok = (uint8_t *)(w + h.off_ok) + f0;
+        int32_t *dit = iterations_used_host ? (int32_t *)(w + h.off_it) + f0 : nullptr;
+        CUDA_TRY(cudaMemcpyAsync(dl, (const char *)llr_host + (size_t)f0 * N * h.elt, (size_t)nf * N * h.elt,
+                                 cudaMemcpyHostToDevice, s));
+        Plan pl;
+        if ((st = make_plan(code, nf, params, pl)) != LDPC_OK) return st;
+        g_launches = 0;
+        st = decode_device(code, params, nf, dl, dhb, dpost, dok, dit, w + h.off_ws[ci & 1], h.chunk_ws, s, pl);
+        if (st != LDPC_OK) return st;
+        launches += g_launches;
+        CUDA_TRY(cudaMemcpyAsync(hard_bits_host + (size_t)f0 * h.wpf, dhb, (size_t)nf * h.wpf * 4,
+                                 cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(syndrome_ok_host + f0, dok, (size_t)nf, cudaMemcpyDeviceToHost, s));
+        if (dpost)
+            CUDA_TRY(cudaMemcpyAsync((char *)posteriors_host + (size_t)f0 * N * h.post_elt, dpost,
+                                     (size_t)nf * N * h.post_elt, cudaMemcpyDeviceToHost, s));
+        if (dit)
+            CUDA_TRY(cudaMemcpyAsync(iterations_used_host + f0, dit, (size_t)nf * 4, cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaEventRecord(code->ev[1], code->aux[0]));
+    CUDA_TRY(cudaEventRecord(code->ev[2], code->aux[1]));
+    CUDA_TRY(cudaStreamWaitEvent(us, code->ev[1], 0));
+    CUDA_TRY(cudaStreamWaitEvent(us, code->ev[2], 0));
+    g_launches = launches;
+    return LDPC_OK;
+}
+
+extern "C" ldpc_status ldpc_count_errors(const ldpc_code *code, int64_t n_frames, const uint32_t *hard_bits,
+                                         const uint8_t *syndrome_ok, const int32_t *iterations_used,
+                                         int64_t *counters, void *stream) {
+    g_detail.clear();
+    if (!code || !hard_bits || !syndrome_ok || !counters) return fail(LDPC_ERR_INVALID_ARG, "NULL argument");
+    if (n_frames == 0) return LDPC_OK;
+    DeviceGuard guard(code->device);
+    const int wpf = (code->N + 31) / 32;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n_frames + 255) / 256, 4096);
+    k_count_errors<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_frames, wpf, hard_bits, syndrome_ok, iterations_used,
+                                                             (unsigned long long *)counters);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "count kernel: %s", cudaGetErrorString(e));
+    return LDPC_OK;
+}
+
+extern "C" int32_t ldpc_last_launch_count(void) { return g_launches; }
+
+extern "C" const char *ldpc_status_string(ldpc_status s) {
+    switch (s) {
+    case LDPC_OK: return "LDPC_OK";
+    case LDPC_ERR_INVALID_ARG: return "LDPC_ERR_INVALID_ARG";
+    case LDPC_ERR_INVALID_CODE: return "LDPC_ERR_INVALID_CODE";
+    case LDPC_ERR_UNSUPPORTED: return "LDPC_ERR_UNSUPPORTED";
+    case LDPC_ERR_CUDA: return "LDPC_ERR_CUDA";
+    case LDPC_ERR_NO_MEMORY: return "LDPC_ERR_NO_MEMORY";
+    }
+    return "LDPC_ERR_UNKNOWN";
+}
+
+extern "C" const char *ldpc_last_error_detail(void) { return g_detail.c_str(); }
+
+extern "C" int32_t ldpc_version(void) { return 100; }

@@ -1,0 +1,149 @@
+// rowcore.cuh -- one check row of the memory-efficient single-scan min-sum
+// iteration (§5, with the offset modification P:347-353),
+// for two frames at once in 16x2 SIMD lanes.
+//
+// Value domain: every LLR-like quantity is held DOUBLED (Lhat = 2 L, Ahat = 2 A,
+// ...).  Doubling lets the magnitude be taken with one VIMNMX as
+// m~ = max(q, ~q) = 2|q| - [q < 0]: m~ orders rows exactly like |q| and
+// |q| = ceil(m~ / 2), so min1 / min2 / argmin come out exact.
+//
+// Compact state of a row (per frame pair), the paper's (A_m, B_m, ñ_m, s_mn):
+//   A, B : doubled magnitudes 2A_m, 2B_m in each 16-bit half (B >= A)
+//   W    : per-edge bits, byte-interleaved so one shift + PRMT expands them to
+//          16-bit masks.  For edge pair i (edges 2i, 2i+1):
+//            byte0 bit i  : s of edge 2i,   frame lo     byte0 bit 4+i : !idx, edge 2i,   lo
+//            byte1 bit i  : s of edge 2i+1, frame lo     byte1 bit 4+i : !idx, edge 2i+1, lo
+//            byte2 bit i  : s of edge 2i,   frame hi     byte2 bit 4+i : !idx, edge 2i,   hi
+//            byte3 bit i  : s of edge 2i+1, frame hi     byte3 bit 4+i : !idx, edge 2i+1, hi
+//          s bit = 1 means L_mn < 0; "!idx" bit = 1 means n != ñ_m.  dc <= 8.
+#pragma once
+#include "simd16.cuh"
+
+namespace ldpc {
+
+struct RowState {
+    uint32_t A, B, W;
+};
+
+// Rebuild L^(k-1)_mn = s f(A, B, n, ñ) and form
+// q_mn = Z^(k-1)_n - L^(k-1)_mn (index reading D8) for all edges.
+template <int DC>
+__device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowState &st, uint32_t (&q)[DC]) {
+    const uint32_t nA = vneg(st.A), nB = vneg(st.B);
+#pragma unroll
+    for (int i = 0; i < (DC + 1) / 2; ++i) {
+        const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte
+        const uint32_t wo = st.W << (3 - i);       // !idx bits of pair i -> bit 7 of each byte
+        {
+            const uint32_t sm = prmt(ws, 0u, 0xAA88u), ni = prmt(wo, 0u, 0xAA88u);
+            const uint32_t mag = sel(ni, st.A, st.B), nmag = sel(ni, nA, nB);
+            q[2 * i] = vadd(L[2 * i], sel(sm, mag, nmag));      // Z - L_old: L_old = s*mag
+        }
+        if (2 * i + 1 < DC) {
+            const uint32_t sm = prmt(ws, 0u, 0xBB99u), ni = prmt(wo, 0u, 0xBB99u);
+            const uint32_t mag = sel(ni, st.A, st.B), nmag = sel(ni, nA, nB);
+            q[2 * i + 1] = vadd(L[2 * i + 1], sel(sm, mag, nmag));
+        }
+    }
+}
+
+// New compact state from the q's and the new messages L^(k)_mn (doubled) to be
+// accumulated into Z^(k)_n:
+//   A = min(max(min1 - beta, 0), Q), B = min(max(min2 - beta, 0), Q)  (readings D5, D6)
+//   ñ = argmin |q| (ties: any minimiser -- unobservable, A = B then; reading D3)
+//   s_mn = prod_{n' != n} sgn(q_mn')  (sgn(0) = +1, reading D1)
+// nbeta2 = packed (-2 beta, -2 beta), q2 = packed (2Q, 2Q).
+template <int DC>
+__device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbeta2, uint32_t q2, RowState &st,
+                                          uint32_t (&r)[DC]) {
+    uint32_t mt[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) mt[j] = vmax(q[j], ~q[j]);   // 2|q| - [q<0]
+    uint32_t m1 = mt[0], m2 = 0x7FFF7FFFu;
+#pragma unroll
+    for (int j = 1; j < DC; ++j) {                             // running two smallest
+        const uint32_t t = vmin(m2, mt[j]);
+        m2 = vmax(m1, t);
+        m1 = vmin(m1, mt[j]);
+    }
+    uint32_t par = q[0];
+#pragma unroll
+    for (int j = 1; j < DC; ++j) par ^= q[j];
+    const uint32_t Pm = signmask(par);                          // product of all signs < 0
+    // doubled magnitudes: 2|q| = m~ + (m~ & 1)
+    const uint32_t a2 = vadd(m1, m1 & 0x00010001u), b2 = vadd(m2, m2 & 0x00010001u);
+    const uint32_t A = vaddmin_relu(a2, nbeta2, q2), B = vaddmin_relu(b2, nbeta2, q2);
+    const uint32_t nA = vneg(A), nB = vneg(B);
+    // message for an edge whose own q is >= 0 carries the sign of the full product
+    const uint32_t Apos = sel(Pm, nA, A), Aneg = sel(Pm, A, nA);
+    const uint32_t Bpos = sel(Pm, nB, B), Bneg = sel(Pm, B, nB);
+    const uint32_t nm1 = vneg(m1);
+    uint32_t W = 0, sqp = 0, nip = 0;
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        const uint32_t ni = vaddmin(mt[j], nm1, 0x00010001u) * 0xFFFFu;   // 0xFFFF: not an argmin
+        const uint32_t sq = signmask(q[j]);                               // 0xFFFF: q < 0
+        r[j] = sel(sq, sel(ni, Aneg, Bneg), sel(ni, Apos, Bpos));
+        if ((j & 1) == 0) {
+            sqp = sq;
+            nip = ni;
+            if (j == DC - 1) {
+                W |= prmt(sqp, 0u, 0x6240u) & (0x01010101u << (j >> 1));
+                W |= prmt(nip, 0u, 0x6240u) & (0x10101010u << (j >> 1));
+            }
+        } else {
+            W |= prmt(sqp, sq, 0x6240u) & (0x01010101u << (j >> 1));
+            W |= prmt(nip, ni, 0x6240u) & (0x10101010u << (j >> 1));
+        }
+    }
+    W ^= Pm & 0x0F0F0F0Fu;                                      // s = sgn(q) * product
+    st.A = A;
+    st.B = B;
+    st.W = W;
+}
+
+// Hard-decision parity of the row for the syndrome (x̂ = 1 iff Z <= 0, P:168-172;
+// H x̂ = 0 test): bit 15 / bit 31 set iff the row's parity is odd.
+template <int DC>
+__device__ __forceinline__ uint32_t row_parity(const uint32_t (&L)[DC]) {
+    uint32_t p = 0;
+#pragma unroll
+    for (int j = 0; j < DC; ++j) p ^= vadd(L[j], 0xFFFFFFFFu);   // sign of (Lhat - 1) = [L <= 0]
+    return p & 0x80008000u;
+}
+
+// ---------------- persistent state formats (workspace words per row-pair)
+// FMT_C16 : 3 words (A, B, W); magnitudes up to 2Q = 1022.
+// FMT_1BIT: 2 words (X = bytes [A_lo, B_lo, A_hi, B_hi], W); magnitudes up to 2Q = 254.
+enum { FMT_C16 = 0, FMT_1BIT = 1 };
+
+template <int FMT>
+struct StateIO {
+    static constexpr int kWords = FMT == FMT_C16 ? 3 : 2;
+    __device__ __forceinline__ static RowState load(const uint32_t *base, size_t stride, size_t idx) {
+        RowState s;
+        if (FMT == FMT_C16) {
+            s.A = __ldcg(base + idx);
+            s.B = __ldcg(base + stride + idx);
+            s.W = __ldcg(base + 2 * stride + idx);
+        } else {
+            const uint32_t X = __ldcg(base + idx);
+            s.A = prmt(X, 0u, 0x4240u);
+            s.B = prmt(X, 0u, 0x4341u);
+            s.W = __ldcg(base + stride + idx);
+        }
+        return s;
+    }
+    __device__ __forceinline__ static void store(uint32_t *base, size_t stride, size_t idx, const RowState &s) {
+        if (FMT == FMT_C16) {
+            __stcg(base + idx, s.A);
+            __stcg(base + stride + idx, s.B);
+            __stcg(base + 2 * stride + idx, s.W);
+        } else {
+            __stcg(base + idx, prmt(s.A, s.B, 0x6240u));
+            __stcg(base + stride + idx, s.W);
+        }
+    }
+};
+
+}  // namespace ldpc

@@ -1,0 +1,44 @@
+// simd16.cuh -- 16x2 integer SIMD helpers for sm_100a (two frames per 32-bit lane).
+//
+// Each 32-bit register holds the same quantity for two frames: frame "lo" in bits
+// 0-15, frame "hi" in bits 16-31, as signed 16-bit values.  The intrinsics below
+// map to single SASS instructions on sm_100a (checked with cuobjdump -sass):
+//   __vadd2 -> VIADD.16x2, __vmins2/__vmaxs2 -> VIMNMX.S16x2,
+//   __viaddmin_s16x2_relu -> VIADDMNMX.S16x2.RELU, prmt -> PRMT, sel -> LOP3.
+#pragma once
+#include <cstdint>
+
+namespace ldpc {
+
+__device__ __forceinline__ uint32_t vadd(uint32_t a, uint32_t b) { return __vadd2(a, b); }
+__device__ __forceinline__ uint32_t vmin(uint32_t a, uint32_t b) { return __vmins2(a, b); }
+__device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxs2(a, b); }
+// -a per half (LOP3 + VIADD)
+__device__ __forceinline__ uint32_t vneg(uint32_t a) { return __vadd2(~a, 0x00010001u); }
+// min(a + b, c) per half, then max(., 0)   (VIADDMNMX.S16x2.RELU)
+__device__ __forceinline__ uint32_t vaddmin_relu(uint32_t a, uint32_t b, uint32_t c) {
+    return __viaddmin_s16x2_relu(a, b, c);
+}
+// min(a + b, c) per half  (VIADDMNMX.S16x2)
+__device__ __forceinline__ uint32_t vaddmin(uint32_t a, uint32_t b, uint32_t c) {
+    return __viaddmin_s16x2(a, b, c);
+}
+// bitwise select: m ? a : b   (one LOP3)
+__device__ __forceinline__ uint32_t sel(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
+// PTX prmt in its generic mode: bit 3 of each selector nibble replicates the sign
+// (bit 7) of the selected byte.  __byte_perm() masks that bit off, hence inline PTX.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+    return d;
+}
+// per-half sign mask: 0xFFFF in each half whose value is negative
+__device__ __forceinline__ uint32_t signmask(uint32_t a) { return prmt(a, 0u, 0xBB99u); }
+// pack two int16 into a word (lo, hi)
+__host__ __device__ __forceinline__ uint32_t pack2(int lo, int hi) {
+    return (uint32_t)(lo & 0xFFFF) | ((uint32_t)hi << 16);
+}
+__device__ __forceinline__ int lo16(uint32_t v) { return (int)(int16_t)(v & 0xFFFFu); }
+__device__ __forceinline__ int hi16(uint32_t v) { return (int)(int16_t)(v >> 16); }
+
+}  // namespace ldpc

@@ -1,0 +1,273 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Integer paths (int16 compact, int8 1-bit): bit-exact posteriors, hard bits,
+syndrome flags and iteration counts (BASELINE.json north star).  fp32 normalized
+path: |dL| <= 1e-4 (1 + |L|), hard bits may differ only where |L| < 1e-3.
+Oracle inputs are the generator's bytes (ldpcgen), never the GPU's.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import ldpcgen as g
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_cs_0609090_b200 as P  # noqa: E402
+
+NT = max(1, min(64, os.cpu_count() or 1))
+_DECODERS = {}
+
+
+def decoder(code):
+    key = id(code)
+    if key not in _DECODERS:
+        _DECODERS[key] = (code, P.Decoder(code, 0))
+    return _DECODERS[key][1]
+
+
+def gpu_decode(code, llr, params, posteriors=True):
+    dec = decoder(code)
+    t = torch.from_numpy(np.ascontiguousarray(llr)).cuda()
+    out = dec.decode(t, params, posteriors=posteriors)
+    torch.cuda.synchronize()
+    hb = out.hard_bits.cpu().numpy().view(np.uint32)
+    post = out.posteriors.cpu().numpy() if out.posteriors is not None else None
+    return post, hb, out.syndrome_ok.cpu().numpy(), out.iterations.cpu().numpy()
+
+
+def oracle_decode_int(code, llr, K, es, beta, Q, frames=None):
+    z = llr if frames is None else llr[frames]
+    return oracle.decode(code, z.astype(np.int32), "compact", "int", K, es, beta, Q, nthreads=NT)
+
+
+def assert_int_parity(code, llr, params, K, es, beta, Q, frames=None):
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    sel = slice(None) if frames is None else frames
+    ref = oracle_decode_int(code, llr, K, es, beta, Q, frames)
+    np.testing.assert_array_equal(it[sel], ref.iters)
+    np.testing.assert_array_equal(ok[sel], ref.ok)
+    np.testing.assert_array_equal(post[sel].astype(np.int32), ref.post)
+    np.testing.assert_array_equal(hb[sel], oracle.pack_bits(ref.bits))
+    return ref
+
+
+def small_codes():
+    return [
+        g.from_dense([[1, 1, 0], [0, 1, 1]], name="toy"),
+        g.regular(96, 3, 6, seed=5),
+        g.regular(48, 3, 6, seed=9, remove_4cycles=False),
+        g.qc(4, 8, 7, np.array([2, 3, 2, 3, 2, 2, 3, 2], np.int32), seed=3),
+        g.qc(6, 12, 37, np.array([3, 4] * 6, np.int32), seed=8),
+        g.dvbs2like(64, 32, 16, 5, 3, seed=4),
+        g.dvbs2like(600, 300, 120, 8, 3, seed=6),
+    ]
+
+
+@pytest.mark.parametrize("code", small_codes(), ids=lambda c: c.name)
+@pytest.mark.parametrize("force_stream", [False, True])
+@pytest.mark.parametrize("fmt", ["compact", "1bit"])
+def test_small_codes_int(code, force_stream, fmt, monkeypatch):
+    if force_stream:
+        monkeypatch.setenv("LDPC_FORCE_STREAM", "1")
+    Q = 511 if fmt == "compact" else 127
+    kind, frac = (g.LLR_I16, 3) if fmt == "compact" else (g.LLR_I8, 2)
+    sigma2 = g.ebn0_to_sigma2(1.5, max(code.rate, 0.3))
+    for F in (1, 2, 67, 130):                       # odd / ragged batches
+        llr = g.llr(100 + F, 0, F, code.n_vars, sigma2, kind, frac, Q)
+        for beta, es, K in ((1, 0, 12), (0, 1, 15), (2, 1, 5)):
+            params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q,
+                                   P.LDPC_LLR_I16 if kind == g.LLR_I16 else P.LDPC_LLR_I8,
+                                   P.LDPC_MSG_COMPACT if fmt == "compact" else P.LDPC_MSG_1BIT)
+            assert_int_parity(code, llr, params, K, es, beta, Q)
+
+
+def _cfg_params(cfg):
+    return P.params_for_config(cfg)
+
+
+def test_cfg1_all_frames():
+    """Config 1: (3,6)-regular N=1008, 2.5 dB, offset 1, 20 iterations, all 1024 frames."""
+    cfg = g.CONFIGS[1]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, cfg.frames)
+    assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, cfg.early_stop, cfg.offset_raw, cfg.clamp)
+
+
+def test_cfg2_parity_subset_and_early_stop():
+    """Config 2 (QC DTMB shape, <=15 iterations, early stop) on 1024 frames at 1.5 dB,
+    plus 512 frames at 2.25 dB where early stop fires at spread-out iterations."""
+    cfg = g.CONFIGS[2]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, cfg.parity_frames)
+    assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, 1, cfg.offset_raw, cfg.clamp)
+    s2 = g.ebn0_to_sigma2(2.25, code.rate)
+    llr = g.llr(cfg.noise_seed + 77, 0, 512, code.n_vars, s2, g.LLR_I16, 3, 511)
+    ref = assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, 1, cfg.offset_raw, cfg.clamp)
+    assert len(np.unique(ref.iters)) >= 4 and ref.ok.mean() > 0.3      # early stop really exercised
+
+
+def test_cfg3_parity_subset():
+    """Config 3: 1-bit messages, int8 Q2 LLRs, 30 iterations (512-frame subset)."""
+    cfg = g.CONFIGS[3]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, 512)
+    assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, 0, cfg.offset_raw, cfg.clamp)
+
+
+def test_cfg4_parity_subset():
+    """Config 4: DVB-S2 shape N=64800, 50 iterations, 64 frames (streaming kernels)."""
+    cfg = g.CONFIGS[4]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, cfg.parity_frames)
+    assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, 0, cfg.offset_raw, cfg.clamp)
+
+
+def _assert_f32_parity(post, hb, ok, ref_post):
+    scale = 1.0 + np.abs(ref_post)
+    assert np.max(np.abs(post.astype(np.float64) - ref_post) / scale) <= 1e-4
+    bits = (post <= 0).astype(np.uint8)
+    ref_bits = (ref_post <= 0).astype(np.uint8)
+    diff = bits != ref_bits
+    assert np.all(np.abs(ref_post[diff]) < 1e-3)
+
+
+def test_cfg5_parity_subset():
+    """Config 5: fp32 normalized (alpha 0.75), 50 iterations, 64 frames, BJ tolerance."""
+    cfg = g.CONFIGS[5]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, cfg.parity_frames)
+    post, hb, ok, it = gpu_decode(code, llr, _cfg_params(cfg))
+    ref = oracle.decode(code, llr, "compact", "f32", cfg.max_iter, 0, alpha=cfg.alpha, nthreads=NT)
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    np.testing.assert_array_equal(it, ref.iters)
+    ref64 = oracle.decode(code, llr.astype(np.float64), "compact", "f64", cfg.max_iter, 0, alpha=cfg.alpha,
+                          nthreads=NT)
+    _assert_f32_parity(post, hb, ok, ref64.post)
+
+
+@pytest.mark.parametrize("code", small_codes()[1:], ids=lambda c: c.name)
+def test_small_codes_f32(code):
+    s2 = g.ebn0_to_sigma2(1.5, max(code.rate, 0.3))
+    for F in (1, 33):
+        llr = g.llr(5 + F, 0, F, code.n_vars, s2, g.LLR_F32)
+        for variant, alpha, beta, es in ((P.LDPC_MINSUM_NORMALIZED, 0.75, 0.0, 0), (P.LDPC_MINSUM_OFFSET, 1.0, 0.25, 1)):
+            params = P.make_params(20, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+            post, hb, ok, it = gpu_decode(code, llr, params)
+            ref = oracle.decode(code, llr, "compact", "f32", 20, es, beta=beta, alpha=alpha, nthreads=NT)
+            _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+
+
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3, 4, 5])
+def test_full_size_sampled_frames(cfg_idx):
+    """At BASELINE.json's full batch size (the launch bench.py times), sampled frames
+    (first, last, and spread) match the oracle decoding them one by one."""
+    cfg = g.CONFIGS[cfg_idx]
+    code = cfg.code()
+    F = cfg.frames
+    llr = cfg.llrs(code, 0, F)
+    post, hb, ok, it = gpu_decode(code, llr, _cfg_params(cfg))
+    picks = np.unique(np.r_[0, 1, F - 2, F - 1, np.linspace(0, F - 1, 12).astype(int)])
+    if cfg.llr_kind == g.LLR_F32:
+        ref = oracle.decode(code, llr[picks], "compact", "f32", cfg.max_iter, 0, alpha=cfg.alpha, nthreads=NT)
+        _assert_f32_parity(post[picks], hb[picks], ok[picks], ref.post.astype(np.float64))
+    else:
+        ref = oracle_decode_int(code, llr, cfg.max_iter, cfg.early_stop, cfg.offset_raw, cfg.clamp, picks)
+        np.testing.assert_array_equal(post[picks].astype(np.int32), ref.post)
+        np.testing.assert_array_equal(hb[picks], oracle.pack_bits(ref.bits))
+        np.testing.assert_array_equal(ok[picks], ref.ok)
+        np.testing.assert_array_equal(it[picks], ref.iters)
+    # properties that hold at any size: converged frames are codewords; iterations within cap
+    conv = ok == 1
+    assert np.all((it >= 0) & (it <= cfg.max_iter))
+    H_rows = [code.col_idx[code.row_ptr[m]:code.row_ptr[m + 1]] for m in range(0, code.n_checks, 97)]
+    bits = np.unpackbits(hb[conv].view(np.uint8), axis=1, bitorder="little")[:, :code.n_vars]
+    for r in H_rows:
+        assert np.all(bits[:, r].sum(axis=1) % 2 == 0)
+
+
+def test_noiseless_and_edge_cases():
+    code = g.CONFIGS[2].code()
+    params = P.make_params(15, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+    llr = np.full((5, code.n_vars), 40, np.int16)
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    assert np.all(it == 0) and np.all(ok == 1) and np.all(hb == 0) and np.all(post == 40)
+    # max_iter = 1
+    cfg = g.CONFIGS[1]
+    c1 = cfg.code()
+    z = cfg.llrs(c1, 0, 9)
+    p1 = P.make_params(1, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+    assert_int_parity(c1, z, p1, 1, 0, 1, 511)
+    # out-of-range channel LLRs are saturated to +-Q on load
+    zb = z.copy()
+    zb[:, :5] = 3000
+    post, hb, ok, it = gpu_decode(c1, zb, p1)
+    ref = oracle_decode_int(c1, np.clip(zb, -511, 511), 1, 0, 1, 511)
+    np.testing.assert_array_equal(post.astype(np.int32), ref.post)
+    # n_frames = 0 is a no-op
+    dec = decoder(c1)
+    ws, nb = dec.workspace(0, p1)
+    P.ldpc_decode_batch(dec.handle, p1, 0, 0, 0, 0, 0, 0, 0, 0, torch.cuda.current_stream().cuda_stream)
+
+
+def test_unsupported_requests():
+    c1 = g.CONFIGS[1].code()
+    dec = decoder(c1)
+    with pytest.raises(P.LdpcError) as e:
+        dec.workspace(8, P.make_params(5, 0, P.LDPC_MINSUM_OFFSET, 1, 0, 1.0, 600, P.LDPC_LLR_I16, P.LDPC_MSG_1BIT))
+    assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+    with pytest.raises(P.LdpcError) as e:
+        dec.workspace(8, P.make_params(5, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0, 0.75, 0, P.LDPC_LLR_I16))
+    assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+    with pytest.raises(P.LdpcError) as e:
+        dec.workspace(8, P.make_params(0, 0))
+    assert e.value.status == P.LDPC_ERR_INVALID_ARG
+
+
+def test_host_api_matches_device_api_and_counters():
+    cfg = g.CONFIGS[2]
+    code = cfg.code()
+    F = 4100
+    llr = cfg.llrs(code, 0, F)
+    params = _cfg_params(cfg)
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    dec = decoder(code)
+    lh = torch.from_numpy(llr).pin_memory()
+    hbh = torch.empty((F, dec.wpf), dtype=torch.int32).pin_memory()
+    okh = torch.empty(F, dtype=torch.uint8).pin_memory()
+    ith = torch.empty(F, dtype=torch.int32).pin_memory()
+    ph = torch.empty((F, code.n_vars), dtype=torch.int16).pin_memory()
+    dec.decode_host(lh, params, hbh, okh, ith, ph)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(hbh.numpy().view(np.uint32), hb)
+    np.testing.assert_array_equal(okh.numpy(), ok)
+    np.testing.assert_array_equal(ith.numpy(), it)
+    np.testing.assert_array_equal(ph.numpy(), post)
+    # error counters (all-zero codeword, reading D14)
+    out = dec.decode(torch.from_numpy(llr).cuda(), params)
+    cnt = dec.count_errors(out).cpu().numpy()
+    nbits = np.array([bin(int(x)).count("1") for x in hb.ravel()]).reshape(hb.shape).sum(axis=1)
+    want = [nbits.sum(), (nbits > 0).sum(), ((nbits > 0) & (ok == 1)).sum(), (ok == 0).sum(), it.sum()]
+    np.testing.assert_array_equal(cnt, want)
+
+
+def test_batch_composition_invariance():
+    """Per-frame outputs do not depend on how frames are batched (the analog of
+    decoding a global frame range on 1 or on W GPUs)."""
+    cfg = g.CONFIGS[1]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, 256)
+    params = _cfg_params(cfg)
+    full = gpu_decode(code, llr, params)
+    parts = [gpu_decode(code, llr[a:a + 64], params) for a in range(0, 256, 64)]
+    for i in range(4):
+        np.testing.assert_array_equal(np.concatenate([p[i] for p in parts]), full[i])
+    again = gpu_decode(code, llr, params)
+    for a, b in zip(full, again):
+        np.testing.assert_array_equal(a, b)

@@ -1,34 +1,46 @@
 // k_resident.cuh -- decode-resident single-scan min-sum kernel (integer LLRs).
 //
 // One CTA decodes one PAIR of frames (two 16-bit SIMD lanes per register) for
-// all iterations without leaving the SM: the posterior double buffer
-// Z^(k-1)_n / Z^(k)_n (reading D7) lives in shared memory
-// (2 * N words), so gathers and the scatter-accumulate of Z^(k)_n += L^(k)_mn
-// never touch HBM.  The compact state (A_m, B_m, ñ_m, s_mn) of every
-// row is kept in this CTA's L2-resident workspace slot, and Z^(0) is copied
-// once per frame pair into the slot.  The grid is persistent (CTAs loop over
-// frame pairs), sized to fill all SMs.
+// all iterations without leaving the SM:
+//   * the posterior double buffer Z^(k-1)_n / Z^(k)_n (
+//     reading D7) lives in shared memory (2 * N words), so the gathers and the
+//     scatter-accumulate Z^(k)_n += L^(k)_mn never touch L2/HBM;
+//   * the compact state (A_m, B_m, ñ_m, s_mn) of every check row -- the paper's
+//     "persistent data" -- lives in Tensor Memory: the thread that owns
+//     a row keeps its state in its own TMEM lane (tcgen05.ld / tcgen05.st);
+//   * Z^(0)_n is packed once per frame pair into this CTA's L2-resident
+//     workspace slot; each iteration starts the accumulator from it with
+//     128-bit copies ("Z^(k)_n = Z^(0)_n").
+// The grid is persistent: CTAs loop over frame pairs, sized to fill all SMs.
 //
 // Rows are processed in conflict-free BATCHES: no two rows of a batch share a
-// variable, so the accumulation into the shared-memory posterior needs no
-// atomics; a barrier separates batches.  For quasi-cyclic codes a batch is one
-// base row (Z circulant rows, thread r = circulant row r, the address of edge
-// (i,j) is jZ + (r + s_ij) mod Z computed on the fly -- no index loads); for
-// other codes the host builds batches by greedy row colouring and the column
-// indices come from a [DC][M] transposed table (coalesced).
-//
-// The first batch touching a variable (host-marked "first" edge) initialises
-// Z^(k)_n = Z^(0)_n + L^(k)_mn instead of accumulating (P:318 + P:322), so no
-// separate initialisation pass or barrier is needed.
+// variable, so the shared-memory accumulation needs no atomics; a barrier
+// separates batches.  For quasi-cyclic codes a batch is one base row (Z
+// circulant rows; thread r = circulant row r; edge (i,j) addresses variable
+// jZ + (r + s_ij) mod Z, computed from the shift table held in the constant
+// bank -- no index loads).  For other codes the host builds batches by greedy
+// row colouring and per-edge byte offsets come from a [DC][M] table.
 #pragma once
 #include "rowcore.cuh"
+#include "tmem.cuh"
 
 namespace ldpc {
 
 constexpr int kMaxDC = 8;
+constexpr int kQcMaxRows = 128;
+constexpr int kQcMaxEnt = 1536;
+
+// QC circulant table, passed by value (kernel parameter = constant bank).
+struct QcTab {
+    int nb;                           // base rows (= batches)
+    uint32_t Z4;                      // 4 * Z (bytes)
+    int32_t bptr[kQcMaxRows + 1];     // base row b = entries [bptr[b], bptr[b+1])
+    uint32_t s4[kQcMaxEnt];           // 4 * shift
+    uint32_t cb4[kQcMaxEnt];          // 4 * first column of the circulant block (j * Z)
+};
 
 struct ResArgs {
-    int N, M, npairs, nframes, K, Qsat, wpf;   // wpf = ceil(N/32) hard-bit words per frame
+    int N, Np, M, npairs, nframes, K, Qsat, wpf;   // Np = N rounded up to 4; wpf = ceil(N/32)
     uint32_t nbeta2, q2;
     const void *llr;
     uint32_t *hard_bits;
@@ -37,14 +49,13 @@ struct ResArgs {
     int32_t *iters;
     uint32_t *ws;
     size_t slot_words;
-    int nbatch;
-    const int32_t *bptr;     // CSR: batch b = schedule positions [bptr[b], bptr[b+1])
-    const int32_t *colT;     // CSR: [kMaxDC][M], bit 31 = first touch of the variable
-    const uint8_t *dcT;      // CSR: degree per schedule position
-    int Z;                   // QC circulant size
-    const uint32_t *qent;    // QC: entries (colbase | shift << 16 | first << 31), grouped by base row
-    const int32_t *qbptr;    // QC: base row b = entries [qbptr[b], qbptr[b+1])
-    int nqent;
+    int nbatch;                       // QC: base rows; CSR: colour batches
+    const int32_t *bptr;              // CSR: batch b = schedule positions [bptr[b], bptr[b+1])
+    const uint32_t *colT;             // CSR: [kMaxDC][M] byte offsets 4*n of each edge
+    const uint8_t *dcT;               // CSR: degree per schedule position
+    int Z;                            // QC circulant size
+    uint32_t tmem_cols;               // TMEM columns allocated per CTA
+    int cols_per_group;               // TMEM columns used by one 128-thread group
 };
 
 template <typename TIN>
@@ -53,71 +64,89 @@ __device__ __forceinline__ int load_llr_sat(const TIN *p, int Q) {
     return max(-Q, min(Q, v));
 }
 
-template <int DC, bool QC, bool ES, int FMT>
-__device__ __forceinline__ void res_row(const ResArgs &a, const uint32_t *__restrict__ Lp, uint32_t *__restrict__ La,
-                                        const uint32_t *__restrict__ z0w, uint32_t *stbase, int p, int r,
-                                        const uint32_t *qe, bool first_iter, uint32_t &synd) {
+__device__ __forceinline__ uint32_t lds(const char *base, uint32_t off) {
+    return *(const uint32_t *)(base + off);
+}
+
+template <int DC, bool QC, bool ES>
+__device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const char *Lpb, char *Lab, int e0,
+                                        uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
     uint32_t off[DC];
-    bool ft[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         if (QC) {
-            const uint32_t e = qe[j];
-            uint32_t x = (uint32_t)r + ((e >> 16) & 0x7FFFu);
-            x = min(x, x - (uint32_t)a.Z);                   // (r + s) mod Z, r + s < 2Z
-            off[j] = (e & 0xFFFFu) + x;
-            ft[j] = (e >> 31) != 0;
+            const uint32_t u = r4 + t.s4[e0 + j];
+            off[j] = min(u - t.Z4, u) + t.cb4[e0 + j];      // 4 * (jZ + (r + s) mod Z)
         } else {
-            const uint32_t c = (uint32_t)__ldg(a.colT + (size_t)j * a.M + p);
-            off[j] = c & 0x7FFFFFFFu;
-            ft[j] = (c >> 31) != 0;
+            off[j] = __ldg(a.colT + (size_t)j * a.M + p);
         }
     }
-    uint32_t z0v[DC];
-#pragma unroll
-    for (int j = 0; j < DC; ++j) z0v[j] = ft[j] ? __ldcg(z0w + off[j]) : 0u;
     uint32_t L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = Lp[off[j]];
+    for (int j = 0; j < DC; ++j) L[j] = lds(Lpb, off[j]);
     if (ES) synd |= row_parity<DC>(L);
     uint32_t q[DC];
-    RowState st;
     if (first_iter) {
 #pragma unroll
-        for (int j = 0; j < DC; ++j) q[j] = L[j];           // L^(0)_mn = 0
+        for (int j = 0; j < DC; ++j) q[j] = L[j];            // L^(0)_mn = 0
     } else {
-        st = StateIO<FMT>::load(stbase, (size_t)a.M, (size_t)p);
         rebuild_q<DC>(L, st, q);
     }
     uint32_t rn[DC];
     new_state<DC>(q, a.nbeta2, a.q2, st, rn);
-    StateIO<FMT>::store(stbase, (size_t)a.M, (size_t)p, st);
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        const uint32_t base = ft[j] ? z0v[j] : La[off[j]];
-        La[off[j]] = vadd(base, rn[j]);                      // Z^(k)_n += L^(k)_mn
+        uint32_t *pa = (uint32_t *)(Lab + off[j]);
+        *pa = vadd(*pa, rn[j]);                              // Z^(k)_n += L^(k)_mn
     }
 }
 
-template <int DC>
-__device__ __forceinline__ uint32_t res_row_parity_qc(const ResArgs &a, const uint32_t *Lp, int r, const uint32_t *qe) {
+template <bool QC, bool ES>
+__device__ __forceinline__ void res_dispatch(int dc, const ResArgs &a, const QcTab &t, const char *Lpb, char *Lab,
+                                             int e0, uint32_t r4, int p, bool first_iter, RowState &st,
+                                             uint32_t &synd) {
+    switch (dc) {
+    case 2: res_row<2, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 3: res_row<3, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 4: res_row<4, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 5: res_row<5, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 6: res_row<6, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 7: res_row<7, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 8: res_row<8, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    }
+}
+
+template <int DC, bool QC>
+__device__ __forceinline__ uint32_t res_parity(const ResArgs &a, const QcTab &t, const char *Lpb, int e0, uint32_t r4,
+                                               int p) {
     uint32_t L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        const uint32_t e = qe[j];
-        uint32_t x = (uint32_t)r + ((e >> 16) & 0x7FFFu);
-        x = min(x, x - (uint32_t)a.Z);
-        L[j] = Lp[(e & 0xFFFFu) + x];
+        uint32_t off;
+        if (QC) {
+            const uint32_t u = r4 + t.s4[e0 + j];
+            off = min(u - t.Z4, u) + t.cb4[e0 + j];
+        } else {
+            off = __ldg(a.colT + (size_t)j * a.M + p);
+        }
+        L[j] = lds(Lpb, off);
     }
     return row_parity<DC>(L);
 }
 
-template <int DC>
-__device__ __forceinline__ uint32_t res_row_parity_csr(const ResArgs &a, const uint32_t *Lp, int p) {
-    uint32_t L[DC];
-#pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = Lp[(uint32_t)__ldg(a.colT + (size_t)j * a.M + p) & 0x7FFFFFFFu];
-    return row_parity<DC>(L);
+template <bool QC>
+__device__ __forceinline__ uint32_t res_parity_dispatch(int dc, const ResArgs &a, const QcTab &t, const char *Lpb,
+                                                        int e0, uint32_t r4, int p) {
+    switch (dc) {
+    case 2: return res_parity<2, QC>(a, t, Lpb, e0, r4, p);
+    case 3: return res_parity<3, QC>(a, t, Lpb, e0, r4, p);
+    case 4: return res_parity<4, QC>(a, t, Lpb, e0, r4, p);
+    case 5: return res_parity<5, QC>(a, t, Lpb, e0, r4, p);
+    case 6: return res_parity<6, QC>(a, t, Lpb, e0, r4, p);
+    case 7: return res_parity<7, QC>(a, t, Lpb, e0, r4, p);
+    case 8: return res_parity<8, QC>(a, t, Lpb, e0, r4, p);
+    }
+    return 0;
 }
 
 // Write outputs of the frames selected by `which` (bit0 = lo frame, bit1 = hi frame)
@@ -150,31 +179,56 @@ __device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc, int f0
     }
 }
 
-template <bool QC, bool ES, int FMT, typename TIN>
-__global__ void __launch_bounds__(256) k_resident(const ResArgs a) {
-    extern __shared__ uint32_t smem[];
-    uint32_t *buf0 = smem, *buf1 = smem + a.N;
-    uint32_t *qtab = smem + 2 * a.N;                 // QC: entries, then base-row pointers
-    int32_t *qbp = (int32_t *)(qtab + a.nqent);
-    const int tid = threadIdx.x;
-    if (QC) {
-        for (int i = tid; i < a.nqent; i += blockDim.x) qtab[i] = a.qent[i];
-        for (int i = tid; i <= a.nbatch; i += blockDim.x) qbp[i] = a.qbptr[i];
+// TMEM columns of batch b for this thread: FMT_C16 uses (A,B) at 2b and W at 2*nb + b;
+// FMT_1BIT uses (X, W) at 2b.  Threads >= 128 use a second column group.
+template <int FMT>
+__device__ __forceinline__ void state_tmem_load(uint32_t tw, int b, int nb, RowState &st) {
+    if (FMT == FMT_C16) {
+        tmem_ld2(tw + 2 * b, st.A, st.B);
+        tmem_ld1(tw + 2 * nb + b, st.W);
+        tmem_wait_ld_dep(st.A, st.B, st.W);
+    } else {
+        uint32_t X;
+        tmem_ld2(tw + 2 * b, X, st.W);
+        tmem_wait_ld_dep(X, st.W, st.W);
+        st.A = prmt(X, 0u, 0x4240u);
+        st.B = prmt(X, 0u, 0x4341u);
     }
-    uint32_t *slot = a.ws + (size_t)blockIdx.x * a.slot_words;
-    uint32_t *z0w = slot;
-    uint32_t *stbase = slot + a.N;
+}
+template <int FMT>
+__device__ __forceinline__ void state_tmem_store(uint32_t tw, int b, int nb, const RowState &st) {
+    if (FMT == FMT_C16) {
+        tmem_st2(tw + 2 * b, st.A, st.B);
+        tmem_st1(tw + 2 * nb + b, st.W);
+    } else {
+        tmem_st2(tw + 2 * b, prmt(st.A, st.B, 0x6240u), st.W);
+    }
+}
+
+template <bool QC, bool ES, int FMT, typename TIN>
+__global__ void __launch_bounds__(256) k_resident(const ResArgs a, const __grid_constant__ QcTab t) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ uint32_t tslot;
+    uint32_t *buf0 = smem, *buf1 = smem + a.Np;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const uint32_t tbase = tmem_alloc_cta(&tslot, a.tmem_cols);
+    const uint32_t tw = tmem_warp_base(tbase) + (uint32_t)((tid >> 7) * a.cols_per_group);
+    uint32_t *z0w = a.ws + (size_t)blockIdx.x * a.slot_words;
     const TIN *llr = (const TIN *)a.llr;
+    const uint32_t r4 = 4u * (uint32_t)tid;
 
     for (int pair = blockIdx.x; pair < a.npairs; pair += gridDim.x) {
         const int f0 = 2 * pair, f1 = f0 + 1;
         const bool hi_valid = f1 < a.nframes;
         __syncthreads();                             // previous pair's outputs read the buffers
-        // ingest: saturate to +-Q, double, pack the pair; Z^(0) -> slot and Z^(k-1) buffer
-        for (int n = tid; n < a.N; n += blockDim.x) {
-            const int zl = load_llr_sat(llr + (size_t)f0 * a.N + n, a.Qsat);
-            const int zh = hi_valid ? load_llr_sat(llr + (size_t)f1 * a.N + n, a.Qsat) : 0;
-            const uint32_t v = pack2(2 * zl, 2 * zh);
+        // ingest: saturate to +-Q, double, pack the pair; Z^(0) -> slot and the read buffer
+        for (int n = tid; n < a.Np; n += nth) {
+            uint32_t v = 0;
+            if (n < a.N) {
+                const int zl = load_llr_sat(llr + (size_t)f0 * a.N + n, a.Qsat);
+                const int zh = hi_valid ? load_llr_sat(llr + (size_t)f1 * a.N + n, a.Qsat) : 0;
+                v = pack2(2 * zl, 2 * zh);
+            }
             __stcg(z0w + n, v);
             buf0[n] = v;
         }
@@ -183,44 +237,34 @@ __global__ void __launch_bounds__(256) k_resident(const ResArgs a) {
         int done = hi_valid ? 0 : 2;
         bool finished = false;
         for (int k = 1; k <= a.K; ++k) {
+            // Z^(k)_n = Z^(0)_n, 128-bit copies from the L2-resident slot
+            {
+                const uint4 *src = (const uint4 *)z0w;
+                uint4 *dst = (uint4 *)La;
+                for (int i = tid; i < (a.Np >> 2); i += nth) dst[i] = __ldcg(src + i);
+            }
+            __syncthreads();
             uint32_t synd = 0;
             const bool first_iter = (k == 1);
+            const char *Lpb = (const char *)Lp;
+            char *Lab = (char *)La;
+#pragma unroll 1
             for (int b = 0; b < a.nbatch; ++b) {
+                RowState st = {0u, 0u, 0u};
+                if (!first_iter) state_tmem_load<FMT>(tw, b, a.nbatch, st);
                 if (QC) {
-                    const int e0 = qbp[b], dc = qbp[b + 1] - e0;
-                    const int r = tid;
-                    if (r < a.Z) {
-                        const uint32_t *qe = qtab + e0;
-                        const int p = b * a.Z + r;
-                        switch (dc) {
-                        case 2: res_row<2, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, r, qe, first_iter, synd); break;
-                        case 3: res_row<3, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, r, qe, first_iter, synd); break;
-                        case 4: res_row<4, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, r, qe, first_iter, synd); break;
-                        case 5: res_row<5, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, r, qe, first_iter, synd); break;
-                        case 6: res_row<6, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, r, qe, first_iter, synd); break;
-                        case 7: res_row<7, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, r, qe, first_iter, synd); break;
-                        case 8: res_row<8, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, r, qe, first_iter, synd); break;
-                        }
-                    }
+                    const int e0 = t.bptr[b], dc = t.bptr[b + 1] - e0;
+                    if (tid < a.Z) res_dispatch<QC, ES>(dc, a, t, Lpb, Lab, e0, r4, 0, first_iter, st, synd);
                 } else {
                     const int p = a.bptr[b] + tid;
-                    if (p < a.bptr[b + 1]) {
-                        const int dc = a.dcT[p];
-                        switch (dc) {
-                        case 2: res_row<2, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, 0, nullptr, first_iter, synd); break;
-                        case 3: res_row<3, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, 0, nullptr, first_iter, synd); break;
-                        case 4: res_row<4, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, 0, nullptr, first_iter, synd); break;
-                        case 5: res_row<5, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, 0, nullptr, first_iter, synd); break;
-                        case 6: res_row<6, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, 0, nullptr, first_iter, synd); break;
-                        case 7: res_row<7, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, 0, nullptr, first_iter, synd); break;
-                        case 8: res_row<8, QC, ES, FMT>(a, Lp, La, z0w, stbase, p, 0, nullptr, first_iter, synd); break;
-                        }
-                    }
+                    if (p < a.bptr[b + 1]) res_dispatch<QC, ES>(a.dcT[p], a, t, Lpb, Lab, 0, 0, p, first_iter, st, synd);
                 }
+                state_tmem_store<FMT>(tw, b, a.nbatch, st);
                 __syncthreads();                     // batch b's accumulations complete
             }
+            tmem_wait_st();
             if (ES) {
-                // syndrome of Z^(k-1) (computed during this scan's gathers; 1-iteration lag)
+                // syndrome of Z^(k-1), gathered during this scan (1-iteration lag)
                 const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
                 const int fail_hi = __syncthreads_or((synd & 0x80000000u) != 0);
                 const int conv = (fail_lo ? 0 : 1) | (fail_hi ? 0 : 2);
@@ -231,39 +275,19 @@ __global__ void __launch_bounds__(256) k_resident(const ResArgs a) {
                 }
                 if (done == 3) { finished = true; break; }
             }
-            uint32_t *t = Lp; Lp = La; La = t;       // Z^(k) becomes the read buffer
+            uint32_t *tmp = Lp; Lp = La; La = tmp;   // Z^(k) becomes the read buffer
         }
         if (!finished) {
             // final syndrome of Z^(K)
             uint32_t synd = 0;
+            const char *Lpb = (const char *)Lp;
             for (int b = 0; b < a.nbatch; ++b) {
                 if (QC) {
-                    const int e0 = qbp[b], dc = qbp[b + 1] - e0;
-                    if (tid < a.Z) {
-                        const uint32_t *qe = qtab + e0;
-                        switch (dc) {
-                        case 2: synd |= res_row_parity_qc<2>(a, Lp, tid, qe); break;
-                        case 3: synd |= res_row_parity_qc<3>(a, Lp, tid, qe); break;
-                        case 4: synd |= res_row_parity_qc<4>(a, Lp, tid, qe); break;
-                        case 5: synd |= res_row_parity_qc<5>(a, Lp, tid, qe); break;
-                        case 6: synd |= res_row_parity_qc<6>(a, Lp, tid, qe); break;
-                        case 7: synd |= res_row_parity_qc<7>(a, Lp, tid, qe); break;
-                        case 8: synd |= res_row_parity_qc<8>(a, Lp, tid, qe); break;
-                        }
-                    }
+                    const int e0 = t.bptr[b], dc = t.bptr[b + 1] - e0;
+                    if (tid < a.Z) synd |= res_parity_dispatch<QC>(dc, a, t, Lpb, e0, r4, 0);
                 } else {
                     const int p = a.bptr[b] + tid;
-                    if (p < a.bptr[b + 1]) {
-                        switch (a.dcT[p]) {
-                        case 2: synd |= res_row_parity_csr<2>(a, Lp, p); break;
-                        case 3: synd |= res_row_parity_csr<3>(a, Lp, p); break;
-                        case 4: synd |= res_row_parity_csr<4>(a, Lp, p); break;
-                        case 5: synd |= res_row_parity_csr<5>(a, Lp, p); break;
-                        case 6: synd |= res_row_parity_csr<6>(a, Lp, p); break;
-                        case 7: synd |= res_row_parity_csr<7>(a, Lp, p); break;
-                        case 8: synd |= res_row_parity_csr<8>(a, Lp, p); break;
-                        }
-                    }
+                    if (p < a.bptr[b + 1]) synd |= res_parity_dispatch<QC>(a.dcT[p], a, t, Lpb, 0, 0, p);
                 }
             }
             const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
@@ -272,6 +296,7 @@ __global__ void __launch_bounds__(256) k_resident(const ResArgs a) {
             if (which) res_write_outputs(a, Lp, f0, which, a.K, fail_lo, fail_hi);
         }
     }
+    tmem_free_cta(tbase, a.tmem_cols);
 }
 
 }  // namespace ldpc

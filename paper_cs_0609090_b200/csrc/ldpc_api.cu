@@ -61,6 +61,7 @@ struct ldpc_code {
     int device = 0;
     int sm_count = 0;
     size_t smem_optin = 0;
+    size_t smem_per_sm = 0;
     int N = 0, M = 0;
     int64_t E = 0;
     int max_dc = 0, max_dv = 0;
@@ -72,10 +73,9 @@ struct ldpc_code {
     int nbatch = 0, res_threads = 0;
     bool res_ok = false;        // resident path possible (smem, degrees)
     size_t res_smem = 0;
-    int nqent = 0;
-    uint32_t *d_qent = nullptr;
-    int32_t *d_qbptr = nullptr;
-    int32_t *d_bptr = nullptr, *d_colT = nullptr;
+    QcTab *qtab = nullptr;      // host copy, passed by value to the kernel (constant bank)
+    int32_t *d_bptr = nullptr;
+    uint32_t *d_colT = nullptr;
     uint8_t *d_dcT = nullptr;
     cudaStream_t aux[2] = {nullptr, nullptr};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -146,8 +146,7 @@ static void free_code(ldpc_code *c) {
     if (!c) return;
     cudaFree(c->d_row_ptr);
     cudaFree(c->d_col_idx);
-    cudaFree(c->d_qent);
-    cudaFree(c->d_qbptr);
+    delete c->qtab;
     cudaFree(c->d_bptr);
     cudaFree(c->d_colT);
     cudaFree(c->d_dcT);
@@ -182,6 +181,7 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
     }
     c->sm_count = prop.multiProcessorCount;
     c->smem_optin = prop.sharedMemPerBlockOptin;
+    c->smem_per_sm = prop.sharedMemPerMultiprocessor;
     if ((st = upload(&c->d_row_ptr, desc->row_ptr, (size_t)c->M + 1)) != LDPC_OK ||
         (st = upload(&c->d_col_idx, desc->col_idx, (size_t)c->E)) != LDPC_OK) {
         free_code(c);
@@ -190,33 +190,31 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
     const int N = c->N, M = c->M;
     // ---------- resident schedule (only when a frame pair's double buffer fits in shared memory)
     if (c->max_dc <= kMaxDC && (size_t)2 * N * 4 + 16384 <= c->smem_optin) {
-        if (desc->qc_z > 0 && desc->qc_z <= 256 && N < 65536) {
+        int nqent = 0;
+        for (int i = 0; desc->qc_z > 0 && i < desc->qc_rows * desc->qc_cols; ++i) nqent += desc->qc_shift[i] >= 0;
+        if (desc->qc_z > 0 && desc->qc_z <= 256 && desc->qc_rows <= kQcMaxRows && nqent <= kQcMaxEnt) {
             c->qc = true;
             c->Z = desc->qc_z;
             c->mb = desc->qc_rows;
             c->nb = desc->qc_cols;
-            std::vector<uint32_t> qent;
-            std::vector<int32_t> qbptr(1, 0);
-            std::vector<char> seen(c->nb, 0);
+            c->qtab = new QcTab();
+            QcTab &t = *c->qtab;
+            t.nb = c->mb;
+            t.Z4 = 4u * (uint32_t)c->Z;
+            int e = 0;
+            t.bptr[0] = 0;
             for (int i = 0; i < c->mb; ++i) {
                 for (int j = 0; j < c->nb; ++j) {
                     const int s = desc->qc_shift[(size_t)i * c->nb + j];
                     if (s < 0) continue;
-                    const uint32_t first = seen[j] ? 0u : 1u;
-                    seen[j] = 1;
-                    qent.push_back((uint32_t)(j * c->Z) | ((uint32_t)s << 16) | (first << 31));
+                    t.s4[e] = 4u * (uint32_t)s;
+                    t.cb4[e] = 4u * (uint32_t)(j * c->Z);
+                    ++e;
                 }
-                qbptr.push_back((int32_t)qent.size());
+                t.bptr[i + 1] = e;
             }
-            c->nqent = (int)qent.size();
             c->nbatch = c->mb;
             c->res_threads = ((c->Z + 31) / 32) * 32;
-            if ((st = upload(&c->d_qent, qent.data(), qent.size())) != LDPC_OK ||
-                (st = upload(&c->d_qbptr, qbptr.data(), qbptr.size())) != LDPC_OK) {
-                free_code(c);
-                return st;
-            }
-            c->res_smem = (size_t)2 * N * 4 + (size_t)c->nqent * 4 + (size_t)(c->nbatch + 1) * 4;
         } else {
             // greedy colouring: rows of one colour share no variable
             std::vector<std::vector<int>> classes;
@@ -243,20 +241,15 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                     used[cc][n >> 6] |= 1ull << (n & 63);
                 }
             }
-            std::vector<int32_t> bptr(1, 0), colT((size_t)kMaxDC * M, -1);
+            std::vector<int32_t> bptr(1, 0);
+            std::vector<uint32_t> colT((size_t)kMaxDC * M, 0u);
             std::vector<uint8_t> dcT(M);
-            std::vector<char> seen(N, 0);
             int p = 0, maxb = 0;
             for (auto &cl : classes) {
                 for (int m : cl) {
                     const int32_t a = desc->row_ptr[m], b = desc->row_ptr[m + 1];
                     dcT[p] = (uint8_t)(b - a);
-                    for (int32_t e = a; e < b; ++e) {
-                        const int n = desc->col_idx[e];
-                        uint32_t v = (uint32_t)n;
-                        if (!seen[n]) { v |= 0x80000000u; seen[n] = 1; }
-                        colT[(size_t)(e - a) * M + p] = (int32_t)v;
-                    }
+                    for (int32_t e = a; e < b; ++e) colT[(size_t)(e - a) * M + p] = 4u * (uint32_t)desc->col_idx[e];
                     ++p;
                 }
                 bptr.push_back(p);
@@ -270,8 +263,8 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                 free_code(c);
                 return st;
             }
-            c->res_smem = (size_t)2 * N * 4;
         }
+        c->res_smem = (size_t)2 * (((size_t)N + 3) & ~(size_t)3) * 4;
         c->res_ok = c->res_smem <= c->smem_optin && c->res_threads <= 256;
     }
     for (auto &s : c->aux)
@@ -317,6 +310,8 @@ struct Plan {
     // resident
     int grid = 0;
     size_t slot_words = 0;
+    uint32_t tmem_cols = 0;
+    int cols_per_group = 0;
     // stream
     int tile = 64, ntiles = 0;
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
@@ -325,10 +320,21 @@ struct Plan {
 
 template <bool QC, bool ES, int FMT, typename TIN>
 cudaError_t res_occupancy(const ldpc_code *c, int *blocks) {
+    // The occupancy API reports 1 block/SM for kernels that allocate TMEM; compute the
+    // limit from the kernel's registers, shared memory and threads instead (TMEM is
+    // accounted for by the caller).
     auto kern = k_resident<QC, ES, FMT, TIN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kern, c->res_threads, c->res_smem);
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, kern)) != cudaSuccess) return e;
+    const size_t per_block_smem = c->res_smem + fa.sharedSizeBytes + 1024;   // + driver reserve
+    int by_smem = (int)(c->smem_per_sm / per_block_smem);
+    int regs = ((fa.numRegs + 7) / 8) * 8 * c->res_threads;
+    int by_regs = regs > 0 ? 65536 / regs : 32;
+    int by_threads = 2048 / c->res_threads;
+    *blocks = std::max(0, std::min(std::min(by_smem, by_regs), std::min(by_threads, 32)));
+    return cudaSuccess;
 }
 
 template <bool QC, bool ES, int FMT>
@@ -399,13 +405,24 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     }
     const int64_t npairs = (F + 1) / 2;
     if (pl.path == PATH_RESIDENT) {
+        // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group
+        pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * c->nbatch;
+        const int groups = (c->res_threads + 127) / 128;
+        uint32_t need = (uint32_t)(pl.cols_per_group * groups), cols = 32;
+        while (cols < need) cols <<= 1;
+        if (cols > 512) return fail(LDPC_ERR_UNSUPPORTED, "compact state needs %u TMEM columns (> 512)", need);
+        pl.tmem_cols = cols;
         int blocks = 0;
         cudaError_t e = res_occupancy_any(c, p, pl.fmt, &blocks);
         if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "occupancy query: %s", cudaGetErrorString(e));
+        if (getenv("LDPC_DEBUG")) fprintf(stderr, "[ldpc] occupancy API: %d blocks/SM\n", blocks);
+        blocks = std::min(blocks, (int)(512 / cols));     // TMEM capacity per SM
         if (blocks < 1) return fail(LDPC_ERR_UNSUPPORTED, "resident kernel does not fit on an SM");
         pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)blocks * c->sm_count);
-        pl.slot_words = (size_t)c->N + (size_t)(pl.fmt == FMT_C16 ? 3 : 2) * c->M;
-        pl.slot_words = (pl.slot_words + 63) & ~(size_t)63;
+        pl.slot_words = ((size_t)c->N + 63) & ~(size_t)63;
+        if (getenv("LDPC_DEBUG"))
+            fprintf(stderr, "[ldpc] resident: threads=%d smem=%zu tmem_cols=%u need=%u occ_blocks=%d grid=%d\n",
+                    c->res_threads, c->res_smem, cols, need, blocks, pl.grid);
         pl.ws_bytes = align256((size_t)pl.grid * pl.slot_words * 4);
     } else {
         pl.ntiles = (int)((F + pl.tile - 1) / pl.tile);
@@ -429,7 +446,8 @@ cudaError_t launch_res(const ldpc_code *c, const Plan &pl, const ResArgs &a, cud
     auto kern = k_resident<QC, ES, FMT, TIN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem);
     if (e != cudaSuccess) return e;
-    kern<<<pl.grid, c->res_threads, c->res_smem, s>>>(a);
+    static const QcTab empty_tab{};
+    kern<<<pl.grid, c->res_threads, c->res_smem, s>>>(a, c->qtab ? *c->qtab : empty_tab);
     ++g_launches;
     return cudaGetLastError();
 }
@@ -445,6 +463,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
                          cudaStream_t s) {
     ResArgs a{};
     a.N = c->N;
+    a.Np = (c->N + 3) & ~3;
     a.M = c->M;
     a.npairs = (int)((F + 1) / 2);
     a.nframes = (int)F;
@@ -465,9 +484,8 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.colT = c->d_colT;
     a.dcT = c->d_dcT;
     a.Z = c->Z;
-    a.qent = c->d_qent;
-    a.qbptr = c->d_qbptr;
-    a.nqent = c->nqent;
+    a.tmem_cols = pl.tmem_cols;
+    a.cols_per_group = pl.cols_per_group;
     const bool es = p->early_stop != 0;
     const int t = p->llr_type;
     if (c->qc) {

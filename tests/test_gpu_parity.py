@@ -158,9 +158,9 @@ def test_small_codes_f32(code):
     for F in (1, 33):
         llr = g.llr(5 + F, 0, F, code.n_vars, s2, g.LLR_F32)
         for variant, alpha, beta, es in ((P.LDPC_MINSUM_NORMALIZED, 0.75, 0.0, 0), (P.LDPC_MINSUM_OFFSET, 1.0, 0.25, 1)):
-            params = P.make_params(20, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+            params = P.make_params(10, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
             post, hb, ok, it = gpu_decode(code, llr, params)
-            ref = oracle.decode(code, llr, "compact", "f32", 20, es, beta=beta, alpha=alpha, nthreads=NT)
+            ref = oracle.decode(code, llr, "compact", "f32", 10, es, beta=beta, alpha=alpha, nthreads=NT)
             _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
 
 

@@ -9,17 +9,18 @@
 //     "persistent data" -- lives in Tensor Memory: the thread that owns
 //     a row keeps its state in its own TMEM lane (tcgen05.ld / tcgen05.st);
 //   * Z^(0)_n is packed once per frame pair into this CTA's L2-resident
-//     workspace slot; each iteration starts the accumulator from it with
-//     128-bit copies ("Z^(k)_n = Z^(0)_n").
+//     workspace slot; each iteration restarts the accumulator from it with one
+//     TMA bulk copy (cp.async.bulk + mbarrier; "Z^(k)_n = Z^(0)_n").
 // The grid is persistent: CTAs loop over frame pairs, sized to fill all SMs.
 //
 // Rows are processed in conflict-free BATCHES: no two rows of a batch share a
 // variable, so the shared-memory accumulation needs no atomics; a barrier
-// separates batches.  For quasi-cyclic codes a batch is one base row (Z
-// circulant rows; thread r = circulant row r; edge (i,j) addresses variable
-// jZ + (r + s_ij) mod Z, computed from the shift table held in the constant
-// bank -- no index loads).  For other codes the host builds batches by greedy
-// row colouring and per-edge byte offsets come from a [DC][M] table.
+// separates batches.  Quasi-cyclic codes: a batch ("super-batch") is one or two
+// base rows with disjoint column blocks, one 128-thread group per base row,
+// thread r = circulant row r; edge (i,j) addresses variable jZ + (r + s_ij) mod Z
+// from the shift table held in the constant bank (no index loads).  Other
+// codes: the host builds batches by greedy row colouring and per-edge byte
+// offsets come from a [DC][M] table.
 #pragma once
 #include "rowcore.cuh"
 #include "tmem.cuh"
@@ -27,16 +28,17 @@
 namespace ldpc {
 
 constexpr int kMaxDC = 8;
-constexpr int kQcMaxRows = 128;
+constexpr int kQcMaxSB = 128;
+constexpr int kQcGroups = 2;
 constexpr int kQcMaxEnt = 1536;
 
 // QC circulant table, passed by value (kernel parameter = constant bank).
 struct QcTab {
-    int nb;                           // base rows (= batches)
-    uint32_t Z4;                      // 4 * Z (bytes)
-    int32_t bptr[kQcMaxRows + 1];     // base row b = entries [bptr[b], bptr[b+1])
-    uint32_t s4[kQcMaxEnt];           // 4 * shift
-    uint32_t cb4[kQcMaxEnt];          // 4 * first column of the circulant block (j * Z)
+    int nsb;                            // super-batches per iteration
+    uint32_t Z4;                        // 4 * Z (bytes)
+    int32_t e0[kQcMaxSB][kQcGroups];    // first entry of the base row handled by group g
+    int32_t dc[kQcMaxSB][kQcGroups];    // its degree (0 = group idle in this super-batch)
+    uint2 ent[kQcMaxEnt];               // (4 * shift, 4 * (j * Z)) per base-matrix entry
 };
 
 struct ResArgs {
@@ -49,13 +51,14 @@ struct ResArgs {
     int32_t *iters;
     uint32_t *ws;
     size_t slot_words;
-    int nbatch;                       // QC: base rows; CSR: colour batches
+    int nbatch;                       // CSR: colour batches (QC: unused, see QcTab::nsb)
     const int32_t *bptr;              // CSR: batch b = schedule positions [bptr[b], bptr[b+1])
     const uint32_t *colT;             // CSR: [kMaxDC][M] byte offsets 4*n of each edge
     const uint8_t *dcT;               // CSR: degree per schedule position
     int Z;                            // QC circulant size
+    int group_threads;                // QC: threads per group (128 with two groups)
     uint32_t tmem_cols;               // TMEM columns allocated per CTA
-    int cols_per_group;               // TMEM columns used by one 128-thread group
+    int cols_per_group;               // TMEM columns used by one group of threads
 };
 
 template <typename TIN>
@@ -64,10 +67,32 @@ __device__ __forceinline__ int load_llr_sat(const TIN *p, int Q) {
     return max(-Q, min(Q, v));
 }
 
-__device__ __forceinline__ uint32_t lds(const char *base, uint32_t off) {
-    return *(const uint32_t *)(base + off);
+// ------------------------------------------------------------ mbarrier / TMA
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// one thread: expect `bytes` and start a bulk global->shared copy completing on the barrier
+__device__ __forceinline__ void tma_bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar) {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(d), "l"(src_gmem), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(b), "r"(phase) : "memory");
+    }
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
+// ------------------------------------------------------------ one check row
 template <int DC, bool QC, bool ES>
 __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const char *Lpb, char *Lab, int e0,
                                         uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
@@ -75,15 +100,16 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         if (QC) {
-            const uint32_t u = r4 + t.s4[e0 + j];
-            off[j] = min(u - t.Z4, u) + t.cb4[e0 + j];      // 4 * (jZ + (r + s) mod Z)
+            const uint2 e = t.ent[e0 + j];
+            const uint32_t u = r4 + e.x;
+            off[j] = min(u - t.Z4, u) + e.y;                // 4 * (jZ + (r + s) mod Z)
         } else {
             off[j] = __ldg(a.colT + (size_t)j * a.M + p);
         }
     }
     uint32_t L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = lds(Lpb, off[j]);
+    for (int j = 0; j < DC; ++j) L[j] = *(const uint32_t *)(Lpb + off[j]);
     if (ES) synd |= row_parity<DC>(L);
     uint32_t q[DC];
     if (first_iter) {
@@ -124,12 +150,13 @@ __device__ __forceinline__ uint32_t res_parity(const ResArgs &a, const QcTab &t,
     for (int j = 0; j < DC; ++j) {
         uint32_t off;
         if (QC) {
-            const uint32_t u = r4 + t.s4[e0 + j];
-            off = min(u - t.Z4, u) + t.cb4[e0 + j];
+            const uint2 e = t.ent[e0 + j];
+            const uint32_t u = r4 + e.x;
+            off = min(u - t.Z4, u) + e.y;
         } else {
             off = __ldg(a.colT + (size_t)j * a.M + p);
         }
-        L[j] = lds(Lpb, off);
+        L[j] = *(const uint32_t *)(Lpb + off);
     }
     return row_parity<DC>(L);
 }
@@ -180,7 +207,7 @@ __device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc, int f0
 }
 
 // TMEM columns of batch b for this thread: FMT_C16 uses (A,B) at 2b and W at 2*nb + b;
-// FMT_1BIT uses (X, W) at 2b.  Threads >= 128 use a second column group.
+// FMT_1BIT uses (X, W) at 2b.
 template <int FMT>
 __device__ __forceinline__ void state_tmem_load(uint32_t tw, int b, int nb, RowState &st) {
     if (FMT == FMT_C16) {
@@ -207,21 +234,29 @@ __device__ __forceinline__ void state_tmem_store(uint32_t tw, int b, int nb, con
 
 template <bool QC, bool ES, int FMT, typename TIN>
 __global__ void __launch_bounds__(256) k_resident(const ResArgs a, const __grid_constant__ QcTab t) {
-    extern __shared__ __align__(16) uint32_t smem[];
+    extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint32_t tslot;
+    __shared__ __align__(8) uint64_t zbar;
     uint32_t *buf0 = smem, *buf1 = smem + a.Np;
     const int tid = threadIdx.x, nth = blockDim.x;
-    const uint32_t tbase = tmem_alloc_cta(&tslot, a.tmem_cols);
-    const uint32_t tw = tmem_warp_base(tbase) + (uint32_t)((tid >> 7) * a.cols_per_group);
+    const int grp = QC ? tid / a.group_threads : tid >> 7;
+    const int rloc = QC ? tid - grp * a.group_threads : tid;
+    const uint32_t r4 = 4u * (uint32_t)rloc;
+    const int nb = QC ? t.nsb : a.nbatch;
+    if (tid == 0) mbar_init(&zbar, 1);
+    const uint32_t tbase = tmem_alloc_cta(&tslot, a.tmem_cols);   // includes a block barrier
+    const uint32_t tw = tmem_warp_base(tbase) + (uint32_t)(grp * a.cols_per_group);
     uint32_t *z0w = a.ws + (size_t)blockIdx.x * a.slot_words;
     const TIN *llr = (const TIN *)a.llr;
-    const uint32_t r4 = 4u * (uint32_t)tid;
+    const uint32_t zbytes = 4u * (uint32_t)a.Np;
+    uint32_t zphase = 0;
 
     for (int pair = blockIdx.x; pair < a.npairs; pair += gridDim.x) {
         const int f0 = 2 * pair, f1 = f0 + 1;
         const bool hi_valid = f1 < a.nframes;
         __syncthreads();                             // previous pair's outputs read the buffers
-        // ingest: saturate to +-Q, double, pack the pair; Z^(0) -> slot and the read buffer
+        // ingest: saturate to +-Q, double, pack the pair; Z^(0) -> slot, Z^(0) buffer and
+        // the first accumulator
         for (int n = tid; n < a.Np; n += nth) {
             uint32_t v = 0;
             if (n < a.N) {
@@ -231,35 +266,32 @@ __global__ void __launch_bounds__(256) k_resident(const ResArgs a, const __grid_
             }
             __stcg(z0w + n, v);
             buf0[n] = v;
+            buf1[n] = v;
         }
+        fence_proxy_async_all();                     // z0w (generic writes) is later read by TMA
         __syncthreads();
-        uint32_t *Lp = buf0, *La = buf1;
         int done = hi_valid ? 0 : 2;
         bool finished = false;
-        for (int k = 1; k <= a.K; ++k) {
-            // Z^(k)_n = Z^(0)_n, 128-bit copies from the L2-resident slot
-            {
-                const uint4 *src = (const uint4 *)z0w;
-                uint4 *dst = (uint4 *)La;
-                for (int i = tid; i < (a.Np >> 2); i += nth) dst[i] = __ldcg(src + i);
-            }
-            __syncthreads();
+        int k = 1;
+        for (; k <= a.K; ++k) {
+            // buffers by iteration parity: Z^(k-1) in Lp, Z^(k) accumulates in La
+            const char *Lpb = (const char *)(((k & 1) ? buf0 : buf1));
+            char *Lab = (char *)(((k & 1) ? buf1 : buf0));
+            if (k > 1) { mbar_wait(&zbar, zphase); zphase ^= 1; }   // La = Z^(0) has landed
             uint32_t synd = 0;
             const bool first_iter = (k == 1);
-            const char *Lpb = (const char *)Lp;
-            char *Lab = (char *)La;
 #pragma unroll 1
-            for (int b = 0; b < a.nbatch; ++b) {
+            for (int b = 0; b < nb; ++b) {
                 RowState st = {0u, 0u, 0u};
-                if (!first_iter) state_tmem_load<FMT>(tw, b, a.nbatch, st);
+                if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
                 if (QC) {
-                    const int e0 = t.bptr[b], dc = t.bptr[b + 1] - e0;
-                    if (tid < a.Z) res_dispatch<QC, ES>(dc, a, t, Lpb, Lab, e0, r4, 0, first_iter, st, synd);
+                    const int dc = t.dc[b][grp];
+                    if (rloc < a.Z && dc) res_dispatch<QC, ES>(dc, a, t, Lpb, Lab, t.e0[b][grp], r4, 0, first_iter, st, synd);
                 } else {
                     const int p = a.bptr[b] + tid;
                     if (p < a.bptr[b + 1]) res_dispatch<QC, ES>(a.dcT[p], a, t, Lpb, Lab, 0, 0, p, first_iter, st, synd);
                 }
-                state_tmem_store<FMT>(tw, b, a.nbatch, st);
+                state_tmem_store<FMT>(tw, b, nb, st);
                 __syncthreads();                     // batch b's accumulations complete
             }
             tmem_wait_st();
@@ -270,21 +302,26 @@ __global__ void __launch_bounds__(256) k_resident(const ResArgs a, const __grid_
                 const int conv = (fail_lo ? 0 : 1) | (fail_hi ? 0 : 2);
                 const int newly = conv & ~done;
                 if (newly) {
-                    res_write_outputs(a, Lp, f0, newly, k - 1, 0, 0);
+                    res_write_outputs(a, (const uint32_t *)Lpb, f0, newly, k - 1, 0, 0);
                     done |= newly;
                 }
                 if (done == 3) { finished = true; break; }
             }
-            uint32_t *tmp = Lp; Lp = La; La = tmp;   // Z^(k) becomes the read buffer
+            if (k < a.K) {
+                // restart the next accumulator (the buffer just read) from Z^(0) by TMA
+                fence_proxy_async_smem();
+                __syncthreads();
+                if (tid == 0) tma_bulk_g2s((void *)Lpb, z0w, zbytes, &zbar);
+            }
         }
         if (!finished) {
             // final syndrome of Z^(K)
+            const char *Lpb = (const char *)(((a.K + 1) & 1) ? buf0 : buf1);
             uint32_t synd = 0;
-            const char *Lpb = (const char *)Lp;
-            for (int b = 0; b < a.nbatch; ++b) {
+            for (int b = 0; b < nb; ++b) {
                 if (QC) {
-                    const int e0 = t.bptr[b], dc = t.bptr[b + 1] - e0;
-                    if (tid < a.Z) synd |= res_parity_dispatch<QC>(dc, a, t, Lpb, e0, r4, 0);
+                    const int dc = t.dc[b][grp];
+                    if (rloc < a.Z && dc) synd |= res_parity_dispatch<QC>(dc, a, t, Lpb, t.e0[b][grp], r4, 0);
                 } else {
                     const int p = a.bptr[b] + tid;
                     if (p < a.bptr[b + 1]) synd |= res_parity_dispatch<QC>(a.dcT[p], a, t, Lpb, 0, 0, p);
@@ -293,7 +330,7 @@ __global__ void __launch_bounds__(256) k_resident(const ResArgs a, const __grid_
             const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
             const int fail_hi = __syncthreads_or((synd & 0x80000000u) != 0);
             const int which = 3 & ~done;
-            if (which) res_write_outputs(a, Lp, f0, which, a.K, fail_lo, fail_hi);
+            if (which) res_write_outputs(a, (const uint32_t *)Lpb, f0, which, a.K, fail_lo, fail_hi);
         }
     }
     tmem_free_cta(tbase, a.tmem_cols);

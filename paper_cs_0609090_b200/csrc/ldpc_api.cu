@@ -70,7 +70,7 @@ struct ldpc_code {
     // resident schedule
     bool qc = false;
     int Z = 0, mb = 0, nb = 0;
-    int nbatch = 0, res_threads = 0;
+    int nbatch = 0, res_threads = 0, group_threads = 0;
     bool res_ok = false;        // resident path possible (smem, degrees)
     size_t res_smem = 0;
     QcTab *qtab = nullptr;      // host copy, passed by value to the kernel (constant bank)
@@ -192,29 +192,81 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
     if (c->max_dc <= kMaxDC && (size_t)2 * N * 4 + 16384 <= c->smem_optin) {
         int nqent = 0;
         for (int i = 0; desc->qc_z > 0 && i < desc->qc_rows * desc->qc_cols; ++i) nqent += desc->qc_shift[i] >= 0;
-        if (desc->qc_z > 0 && desc->qc_z <= 256 && desc->qc_rows <= kQcMaxRows && nqent <= kQcMaxEnt) {
+        if (desc->qc_z > 0 && desc->qc_z <= 256 && desc->qc_rows <= kQcMaxSB && nqent <= kQcMaxEnt) {
             c->qc = true;
             c->Z = desc->qc_z;
             c->mb = desc->qc_rows;
             c->nb = desc->qc_cols;
             c->qtab = new QcTab();
             QcTab &t = *c->qtab;
-            t.nb = c->mb;
             t.Z4 = 4u * (uint32_t)c->Z;
+            std::vector<int> rstart(c->mb + 1, 0);
+            std::vector<std::vector<int>> cols(c->mb);
             int e = 0;
-            t.bptr[0] = 0;
             for (int i = 0; i < c->mb; ++i) {
+                rstart[i] = e;
                 for (int j = 0; j < c->nb; ++j) {
                     const int s = desc->qc_shift[(size_t)i * c->nb + j];
                     if (s < 0) continue;
-                    t.s4[e] = 4u * (uint32_t)s;
-                    t.cb4[e] = 4u * (uint32_t)(j * c->Z);
+                    t.ent[e] = make_uint2(4u * (uint32_t)s, 4u * (uint32_t)(j * c->Z));
+                    cols[i].push_back(j);
                     ++e;
                 }
-                t.bptr[i + 1] = e;
             }
-            c->nbatch = c->mb;
-            c->res_threads = ((c->Z + 31) / 32) * 32;
+            // super-batches: pairs of base rows with disjoint column blocks (their Z rows
+            // each touch distinct variables), processed by two 128-thread groups at once.
+            const int groups = c->Z <= 128 ? 2 : 1;
+            std::vector<std::pair<int, int>> sb;
+            if (groups == 2) {
+                auto disjoint = [&](int x, int y) {
+                    for (int u : cols[x])
+                        for (int v : cols[y])
+                            if (u == v) return false;
+                    return true;
+                };
+                std::vector<std::pair<int, int>> best;
+                size_t best_pairs = 0;
+                uint64_t rs = 0x9E3779B97F4A7C15ull;
+                for (int trial = 0; trial < 64; ++trial) {
+                    std::vector<int> order(c->mb);
+                    for (int i = 0; i < c->mb; ++i) order[i] = i;
+                    if (trial) {
+                        for (int i = c->mb - 1; i > 0; --i) {
+                            rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17;
+                            std::swap(order[i], order[rs % (uint64_t)(i + 1)]);
+                        }
+                    }
+                    std::vector<char> used(c->mb, 0);
+                    std::vector<std::pair<int, int>> cur;
+                    size_t npairs_found = 0;
+                    for (int ii = 0; ii < c->mb; ++ii) {
+                        const int x = order[ii];
+                        if (used[x]) continue;
+                        used[x] = 1;
+                        int y = -1;
+                        for (int jj = ii + 1; jj < c->mb; ++jj)
+                            if (!used[order[jj]] && disjoint(x, order[jj])) { y = order[jj]; break; }
+                        if (y >= 0) { used[y] = 1; ++npairs_found; }
+                        cur.emplace_back(x, y);
+                    }
+                    if (trial == 0 || npairs_found > best_pairs) { best = cur; best_pairs = npairs_found; }
+                }
+                sb = best;
+            } else {
+                for (int i = 0; i < c->mb; ++i) sb.emplace_back(i, -1);
+            }
+            t.nsb = (int)sb.size();
+            for (int b = 0; b < t.nsb; ++b) {
+                const int rows[2] = {sb[b].first, sb[b].second};
+                for (int g = 0; g < kQcGroups; ++g) {
+                    const int i = g < groups ? rows[g] : -1;
+                    t.e0[b][g] = i >= 0 ? rstart[i] : 0;
+                    t.dc[b][g] = i >= 0 ? (int)cols[i].size() : 0;
+                }
+            }
+            c->nbatch = t.nsb;
+            c->group_threads = groups == 2 ? 128 : ((c->Z + 31) / 32) * 32;
+            c->res_threads = groups * c->group_threads;
         } else {
             // greedy colouring: rows of one colour share no variable
             std::vector<std::vector<int>> classes;
@@ -407,7 +459,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (pl.path == PATH_RESIDENT) {
         // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group
         pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * c->nbatch;
-        const int groups = (c->res_threads + 127) / 128;
+        const int groups = c->qc ? c->res_threads / c->group_threads : (c->res_threads + 127) / 128;
         uint32_t need = (uint32_t)(pl.cols_per_group * groups), cols = 32;
         while (cols < need) cols <<= 1;
         if (cols > 512) return fail(LDPC_ERR_UNSUPPORTED, "compact state needs %u TMEM columns (> 512)", need);
@@ -421,8 +473,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)blocks * c->sm_count);
         pl.slot_words = ((size_t)c->N + 63) & ~(size_t)63;
         if (getenv("LDPC_DEBUG"))
-            fprintf(stderr, "[ldpc] resident: threads=%d smem=%zu tmem_cols=%u need=%u occ_blocks=%d grid=%d\n",
-                    c->res_threads, c->res_smem, cols, need, blocks, pl.grid);
+            fprintf(stderr, "[ldpc] resident: threads=%d smem=%zu tmem_cols=%u need=%u occ_blocks=%d grid=%d batches=%d\n",
+                    c->res_threads, c->res_smem, cols, need, blocks, pl.grid, c->nbatch);
         pl.ws_bytes = align256((size_t)pl.grid * pl.slot_words * 4);
     } else {
         pl.ntiles = (int)((F + pl.tile - 1) / pl.tile);
@@ -484,6 +536,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.colT = c->d_colT;
     a.dcT = c->d_dcT;
     a.Z = c->Z;
+    a.group_threads = c->group_threads;
     a.tmem_cols = pl.tmem_cols;
     a.cols_per_group = pl.cols_per_group;
     const bool es = p->early_stop != 0;

@@ -47,6 +47,39 @@ __device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowStat
     }
 }
 
+// Smallest and second smallest of DC packed values (with multiplicity), as a
+// pairwise tree: leaves (min, max), merges m1 = min(a1, b1),
+// m2 = min3(max(a1, b1), a2, b2).  Shorter dependency chains than a running scan.
+template <int DC>
+__device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, uint32_t &m2) {
+    constexpr int NL = (DC + 1) / 2;
+    uint32_t a1[NL], a2[NL];
+#pragma unroll
+    for (int i = 0; i < DC / 2; ++i) {
+        a1[i] = vmin(v[2 * i], v[2 * i + 1]);
+        a2[i] = vmax(v[2 * i], v[2 * i + 1]);
+    }
+    if (DC & 1) {
+        a1[NL - 1] = v[DC - 1];
+        a2[NL - 1] = 0x7FFF7FFFu;
+    }
+#pragma unroll
+    for (int n = NL; n > 1; n = (n + 1) / 2) {
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            const uint32_t x1 = a1[2 * i], y1 = a1[2 * i + 1];
+            a1[i] = vmin(x1, y1);
+            a2[i] = __vimin3_s16x2(vmax(x1, y1), a2[2 * i], a2[2 * i + 1]);
+        }
+        if (n & 1) {
+            a1[n / 2] = a1[n - 1];
+            a2[n / 2] = a2[n - 1];
+        }
+    }
+    m1 = a1[0];
+    m2 = a2[0];
+}
+
 // New compact state from the q's and the new messages L^(k)_mn (doubled) to be
 // accumulated into Z^(k)_n:
 //   A = min(max(min1 - beta, 0), Q), B = min(max(min2 - beta, 0), Q)  (readings D5, D6)
@@ -59,13 +92,8 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbet
     uint32_t mt[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) mt[j] = vmax(q[j], ~q[j]);   // 2|q| - [q<0]
-    uint32_t m1 = mt[0], m2 = 0x7FFF7FFFu;
-#pragma unroll
-    for (int j = 1; j < DC; ++j) {                             // running two smallest
-        const uint32_t t = vmin(m2, mt[j]);
-        m2 = vmax(m1, t);
-        m1 = vmin(m1, mt[j]);
-    }
+    uint32_t m1, m2;
+    two_min<DC>(mt, m1, m2);
     uint32_t par = q[0];
 #pragma unroll
     for (int j = 1; j < DC; ++j) par ^= q[j];

@@ -197,8 +197,8 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    F = cfg.frames
-    f0 = rank * F
+    from paper_cs_0609090_b200.dist import frame_shard, reduce_counters
+    f0, F = frame_shard(rank, world, cfg.frames)
     llr_host = cfg.llrs(code, f0, F)                      # this rank's global frame shard
     llr = torch.from_numpy(llr_host).to(dev)
     dec = P.Decoder(code, local)
@@ -234,9 +234,7 @@ def main():
     # iterations / error counters of the last step (all steps decode the same frames)
     counters = dec.count_errors(out)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    reduce_counters(counters, t)                          # NCCL: SUM counters, MAX elapsed
     total_ms = float(t.item())
     c = counters.cpu().numpy().tolist()
     sum_iters = c[4]

@@ -233,13 +233,13 @@ __device__ __forceinline__ void state_tmem_store(uint32_t tw, int b, int nb, con
 }
 
 template <bool QC, bool ES, int FMT, typename TIN>
-__global__ void __launch_bounds__(256) k_resident(const ResArgs a, const __grid_constant__ QcTab t) {
+__global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __grid_constant__ QcTab t) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint32_t tslot;
     __shared__ __align__(8) uint64_t zbar;
     uint32_t *buf0 = smem, *buf1 = smem + a.Np;
     const int tid = threadIdx.x, nth = blockDim.x;
-    const int grp = QC ? tid / a.group_threads : tid >> 7;
+    const int grp = QC ? (a.group_threads == 128 ? (tid >> 7) : 0) : tid >> 7;
     const int rloc = QC ? tid - grp * a.group_threads : tid;
     const uint32_t r4 = 4u * (uint32_t)rloc;
     const int nb = QC ? t.nsb : a.nbatch;
@@ -285,8 +285,14 @@ __global__ void __launch_bounds__(256) k_resident(const ResArgs a, const __grid_
                 RowState st = {0u, 0u, 0u};
                 if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
                 if (QC) {
-                    const int dc = t.dc[b][grp];
-                    if (rloc < a.Z && dc) res_dispatch<QC, ES>(dc, a, t, Lpb, Lab, t.e0[b][grp], r4, 0, first_iter, st, synd);
+                    // warp-uniform group branch so the table index is uniform
+                    if (grp == 0) {
+                        const int dc = t.dc[b][0];
+                        if (rloc < a.Z && dc) res_dispatch<QC, ES>(dc, a, t, Lpb, Lab, t.e0[b][0], r4, 0, first_iter, st, synd);
+                    } else {
+                        const int dc = t.dc[b][1];
+                        if (rloc < a.Z && dc) res_dispatch<QC, ES>(dc, a, t, Lpb, Lab, t.e0[b][1], r4, 0, first_iter, st, synd);
+                    }
                 } else {
                     const int p = a.bptr[b] + tid;
                     if (p < a.bptr[b + 1]) res_dispatch<QC, ES>(a.dcT[p], a, t, Lpb, Lab, 0, 0, p, first_iter, st, synd);

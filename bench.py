@@ -37,8 +37,8 @@ L2_FLUSH_BYTES = 256 << 20
 W_BYTES = {1: (2, 2, 4), 2: (2, 2, 4), 3: (1, 2, 2.375), 4: (2, 2, 4), 5: (4, 4, 12)}
 # Algorithmic integer operations per edge-update of the method:
 # rebuild L_old (select magnitude, apply sign), q = Z - L_old, |q|, two-minimum
-# update (2 compares), sign product, new message (select, sign), Z += L.
-ALG_OPS_PER_EU = 10
+# update (2 compares), sign product, new message (select, sign, exclusion), Z += L.
+ALG_OPS_PER_EU = 12
 
 
 def describe(cfg, code):

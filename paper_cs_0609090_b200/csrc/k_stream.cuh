@@ -28,6 +28,7 @@ struct StreamArgs {
     uint32_t nbeta2, q2;
     float alpha, beta;           // fp32 variant: |L| <= max(alpha*min - beta, 0)
     const int32_t *row_ptr, *col_idx;
+    const uint4 *rowtab;         // [M][2]: up to 8 column indices per row; dc in bits 28-31 of word 0 (15 = wider row)
     const void *llr;
     uint32_t *Z0;                // [tile][N][32]
     uint32_t *Lb[3];             // rotating posterior buffers [tile][N][32]
@@ -62,46 +63,122 @@ __global__ void k_stream_ingest_i(const StreamArgs a) {
     }
 }
 
-template <int DC, int FMT, bool ES>
-__device__ __forceinline__ void stream_row_i(const StreamArgs &a, int tile, int lane, int m, int e0,
-                                             const uint32_t *Lp, uint32_t *La, bool first_iter, uint32_t keep,
-                                             uint32_t &synd) {
-    uint32_t L[DC];
-    size_t idx[DC];
-#pragma unroll
-    for (int j = 0; j < DC; ++j) {
-        const int n = __ldg(a.col_idx + e0 + j);
-        idx[j] = ((size_t)tile * a.N + n) * 32 + lane;
-    }
-#pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = from_vform(__ldcg(Lp + idx[j]));
-    if (ES) synd |= row_parity<DC>(L);
-    uint32_t *stb = a.st + (size_t)tile * StateIO<FMT>::kWords * a.M * 32 + lane;
-    const size_t sstride = (size_t)a.M * 32;
-    uint32_t q[DC];
-    RowState st;
-    if (first_iter) {
-#pragma unroll
-        for (int j = 0; j < DC; ++j) q[j] = L[j];
+struct RowT {
+    uint32_t c[8];
+    int dc;
+};
+__device__ __forceinline__ RowT load_rowt(const uint4 *rt, int m, int M) {
+    RowT r;
+    if (m < M) {
+        const uint4 x = __ldg(rt + 2 * m), y = __ldg(rt + 2 * m + 1);
+        r.c[0] = x.x & 0x0FFFFFFFu; r.c[1] = x.y; r.c[2] = x.z; r.c[3] = x.w;
+        r.c[4] = y.x; r.c[5] = y.y; r.c[6] = y.z; r.c[7] = y.w;
+        r.dc = (int)(x.x >> 28);
     } else {
-        st = StateIO<FMT>::load(stb, sstride, (size_t)m * 32);
-        rebuild_q<DC>(L, st, q);
-    }
-    uint32_t rn[DC];
-    new_state<DC>(q, a.nbeta2, a.q2, st, rn);
-    StateIO<FMT>::store(stb, sstride, (size_t)m * 32, st);
 #pragma unroll
-    for (int j = 0; j < DC; ++j) atomicAdd(La + idx[j], to_vform(rn[j] & ~keep));
+        for (int j = 0; j < 8; ++j) r.c[j] = 0;
+        r.dc = 0;
+    }
+    return r;
+}
+
+// Copy Z^(0) of this tile into the accumulator of the next iteration with 128-bit
+// loads/stores, 4 in flight per thread (contiguous [n][32] plane segment of the tile).
+__device__ __forceinline__ void stream_init_next(const uint32_t *Z0t, uint32_t *Lnt, int N, int wg, int nwg, int lane) {
+    const uint4 *src = (const uint4 *)Z0t;
+    uint4 *dst = (uint4 *)Lnt;
+    const int total = N * 8;                     // uint4 per tile plane
+    const int step = nwg * 32;
+    int i = wg * 32 + lane;
+    for (; i + 3 * step < total; i += 4 * step) {
+        const uint4 v0 = __ldcg(src + i), v1 = __ldcg(src + i + step), v2 = __ldcg(src + i + 2 * step),
+                    v3 = __ldcg(src + i + 3 * step);
+        __stcg(dst + i, v0);
+        __stcg(dst + i + step, v1);
+        __stcg(dst + i + 2 * step, v2);
+        __stcg(dst + i + 3 * step, v3);
+    }
+    for (; i < total; i += step) __stcg(dst + i, __ldcg(src + i));
+}
+
+// NR check rows of one tile (two frames per lane), all loads issued before any compute.
+template <int DC, int NR, int FMT, bool ES>
+__device__ __forceinline__ void stream_rows_i(const StreamArgs &a, int lane, const int (&m)[NR], const RowT *rt,
+                                              const uint32_t *Lpt, uint32_t *Lat, uint32_t *stt, bool first_iter,
+                                              uint32_t keep, uint32_t &synd) {
+    uint32_t off[NR][DC];
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int j = 0; j < DC; ++j) off[r][j] = rt[r].c[j] * 32u + (uint32_t)lane;
+    const size_t sstride = (size_t)a.M * 32;
+    RowState st[NR];
+    if (!first_iter) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) st[r] = StateIO<FMT>::load(stt + lane, sstride, (size_t)m[r] * 32);
+    }
+    uint32_t L[NR][DC];
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int j = 0; j < DC; ++j) L[r][j] = from_vform(__ldcg(Lpt + off[r][j]));
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        if (ES) synd |= row_parity<DC>(L[r]);
+        uint32_t q[DC];
+        if (first_iter) {
+#pragma unroll
+            for (int j = 0; j < DC; ++j) q[j] = L[r][j];
+        } else {
+            rebuild_q<DC>(L[r], st[r], q);
+        }
+        uint32_t rn[DC];
+        new_state<DC>(q, a.nbeta2, a.q2, st[r], rn);
+        StateIO<FMT>::store(stt + lane, sstride, (size_t)m[r] * 32, st[r]);
+#pragma unroll
+        for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], to_vform(rn[j] & ~keep));
+    }
+}
+
+template <int NR, int FMT, bool ES>
+__device__ __forceinline__ void stream_dispatch_i(int dc, const StreamArgs &a, int lane, const int (&m)[NR],
+                                                  const RowT *rt, const uint32_t *Lpt, uint32_t *Lat,
+                                                  uint32_t *stt, bool first_iter, uint32_t keep, uint32_t &synd) {
+    switch (dc) {
+    case 2: stream_rows_i<2, NR, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 3: stream_rows_i<3, NR, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 4: stream_rows_i<4, NR, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 5: stream_rows_i<5, NR, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 6: stream_rows_i<6, NR, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 7: stream_rows_i<7, NR, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 8: stream_rows_i<8, NR, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    }
 }
 
 template <int FMT, bool ES>
-__global__ void __launch_bounds__(256) k_stream_iter_i(const StreamArgs a, int k) {
+__device__ __forceinline__ void stream_dispatch2_i(int dc, const StreamArgs &a, int lane, const int (&m)[2],
+                                                   const RowT *rt, const uint32_t *Lpt, uint32_t *Lat,
+                                                   uint32_t *stt, bool first_iter, uint32_t keep, uint32_t &synd) {
+    switch (dc) {
+    case 2: stream_rows_i<2, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 3: stream_rows_i<3, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 4: stream_rows_i<4, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 5: stream_rows_i<5, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 6: stream_rows_i<6, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    case 7: stream_rows_i<7, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
+    }
+}
+
+template <int FMT, bool ES>
+__global__ void __launch_bounds__(256, 3) k_stream_iter_i(const StreamArgs a, int k) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nwg = gridDim.x * (blockDim.x >> 5);
-    const uint32_t *Lp = a.Lb[(k - 1) % 3];
-    uint32_t *La = a.Lb[k % 3];
-    uint32_t *Ln = a.Lb[(k + 1) % 3];
+    const size_t plane = (size_t)tile * a.N * 32;
+    const uint32_t *Lpt = a.Lb[(k - 1) % 3] + plane;
+    uint32_t *Lat = a.Lb[k % 3] + plane;
+    uint32_t *Lnt = a.Lb[(k + 1) % 3] + plane;
+    uint32_t *stt = a.st + (size_t)tile * StateIO<FMT>::kWords * a.M * 32;
     uint32_t keep = 0;                                   // 0xFFFF halves: frame frozen
     if (ES) {
         const uint32_t d = a.done[tile * 32 + lane];
@@ -110,26 +187,24 @@ __global__ void __launch_bounds__(256) k_stream_iter_i(const StreamArgs a, int k
     }
     // initialise the accumulator of the next iteration (it held Z^(k-2))
     if (k < a.K) {
-        for (int n = wg; n < a.N; n += nwg) {
-            const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
-            uint32_t v = __ldcg(a.Z0 + idx);
-            if (ES && keep) v = to_vform(sel(keep, from_vform(__ldcg(Ln + idx)), from_vform(v)));
-            __stcg(Ln + idx, v);
+        if (!ES || !__any_sync(0xFFFFFFFFu, keep != 0)) {
+            stream_init_next(a.Z0 + plane, Lnt, a.N, wg, nwg, lane);
+        } else {
+            for (int n = wg; n < a.N; n += nwg) {
+                const size_t idx = (size_t)n * 32 + lane;
+                uint32_t v = __ldcg(a.Z0 + plane + idx);
+                if (keep) v = to_vform(sel(keep, from_vform(__ldcg(Lnt + idx)), from_vform(v)));
+                __stcg(Lnt + idx, v);
+            }
         }
     }
     uint32_t synd = 0;
     const bool first_iter = (k == 1);
+    // row tables of the next row pair are prefetched while the current pair is processed
     for (int m = wg; m < a.M; m += nwg) {
-        const int e0 = __ldg(a.row_ptr + m), dc = __ldg(a.row_ptr + m + 1) - e0;
-        switch (dc) {
-        case 2: stream_row_i<2, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
-        case 3: stream_row_i<3, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
-        case 4: stream_row_i<4, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
-        case 5: stream_row_i<5, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
-        case 6: stream_row_i<6, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
-        case 7: stream_row_i<7, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
-        case 8: stream_row_i<8, FMT, ES>(a, tile, lane, m, e0, Lp, La, first_iter, keep, synd); break;
-        }
+        const RowT rt = load_rowt(a.rowtab, m, a.M);
+        const int mm[1] = {m};
+        stream_dispatch_i<1, FMT, ES>(rt.dc, a, lane, mm, &rt, Lpt, Lat, stt, first_iter, keep, synd);
     }
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
 }
@@ -273,109 +348,160 @@ __global__ void k_stream_ingest_f(const StreamArgs a) {
     }
 }
 
-// One row, one frame per lane, fp32 (reading D11: one RN rounding per operation,
-// no FMA contraction: __fsub_rn / __fmul_rn).
-template <int DC, bool ES>
-__device__ __forceinline__ void stream_row_f(const StreamArgs &a, int tile, int lane, int m, int e0,
-                                             const float *Lp, float *La, bool first_iter, bool frozen,
-                                             uint32_t &synd) {
-    float L[DC];
-    size_t idx[DC];
+// NR rows, one frame per lane, fp32 (reading D11: one RN rounding per operation,
+// no FMA contraction: __fsub_rn / __fmul_rn).  All loads issued before any compute.
+template <int DC, int NR, bool ES>
+__device__ __forceinline__ void stream_rows_f(const StreamArgs &a, int lane, const int (&m)[NR], const RowT *rt,
+                                              const float *Lpt, float *Lat, uint32_t *stt, bool first_iter,
+                                              bool frozen, uint32_t &synd) {
+    uint32_t off[NR][DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) idx[j] = ((size_t)tile * a.N + __ldg(a.col_idx + e0 + j)) * 32 + lane;
-#pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = __ldcg(Lp + idx[j]);
-    if (ES) {
-        uint32_t p = 0;
-#pragma unroll
-        for (int j = 0; j < DC; ++j) p ^= L[j] <= 0.0f ? 1u : 0u;
-        synd |= p;
-    }
-    uint32_t *stb = a.st + (size_t)tile * 3 * a.M * 32 + lane;
-    const size_t ss = (size_t)a.M * 32, so = (size_t)m * 32;
-    float q[DC];
-    if (first_iter) {
-#pragma unroll
-        for (int j = 0; j < DC; ++j) q[j] = L[j];
-    } else {
-        const float A = __uint_as_float(__ldcg(stb + so)), B = __uint_as_float(__ldcg(stb + ss + so));
-        const uint32_t W = __ldcg(stb + 2 * ss + so);
-        const int idx0 = (int)(W >> 16);
+    for (int r = 0; r < NR; ++r)
 #pragma unroll
         for (int j = 0; j < DC; ++j) {
-            const float mag = (j == idx0) ? B : A;                         // f(A,B,n,ñ)
-            const float lold = ((W >> j) & 1u) ? -mag : mag;               // s_mn f(...)
-            q[j] = __fsub_rn(L[j], lold);                                  // Z_n' - L_mn'
+            // rows of degree <= 8 come with their column table; wider rows read the CSR
+            const uint32_t c = DC <= 8 ? rt[r].c[j < 8 ? j : 0] : (uint32_t)__ldg(a.col_idx + __ldg(a.row_ptr + m[r]) + j);
+            off[r][j] = c * 32u + (uint32_t)lane;
+        }
+    const size_t ss = (size_t)a.M * 32;
+    float A0[NR], B0[NR];
+    uint32_t W0[NR];
+    if (!first_iter) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const size_t so = (size_t)m[r] * 32 + lane;
+            A0[r] = __uint_as_float(__ldcg(stt + so));
+            B0[r] = __uint_as_float(__ldcg(stt + ss + so));
+            W0[r] = __ldcg(stt + 2 * ss + so);
         }
     }
-    float m1 = fabsf(q[0]), m2 = 0.0f;
-    int i1 = 0;
-    bool have2 = false;
-    uint32_t sq = q[0] < 0.0f ? 1u : 0u;
+    float L[NR][DC];
 #pragma unroll
-    for (int j = 1; j < DC; ++j) {
-        const float x = fabsf(q[j]);
-        sq |= (q[j] < 0.0f ? 1u : 0u) << j;
-        if (x < m1) { m2 = m1; have2 = true; m1 = x; i1 = j; }
-        else if (!have2 || x < m2) { m2 = x; have2 = true; }
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int j = 0; j < DC; ++j) L[r][j] = __ldcg(Lpt + off[r][j]);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        if (ES) {
+            uint32_t p = 0;
+#pragma unroll
+            for (int j = 0; j < DC; ++j) p ^= L[r][j] <= 0.0f ? 1u : 0u;
+            synd |= p;
+        }
+        float q[DC];
+        if (first_iter) {
+#pragma unroll
+            for (int j = 0; j < DC; ++j) q[j] = L[r][j];
+        } else {
+            const int idx0 = (int)(W0[r] >> 16);
+#pragma unroll
+            for (int j = 0; j < DC; ++j) {
+                const float mag = (j == idx0) ? B0[r] : A0[r];                // f(A,B,n,ñ)
+                const float lold = ((W0[r] >> j) & 1u) ? -mag : mag;          // s_mn f(...)
+                q[j] = __fsub_rn(L[r][j], lold);                               // Z_n' - L_mn'
+            }
+        }
+        float m1 = fabsf(q[0]), m2 = 0.0f;
+        int i1 = 0;
+        bool have2 = false;
+        uint32_t sq = q[0] < 0.0f ? 1u : 0u;
+#pragma unroll
+        for (int j = 1; j < DC; ++j) {
+            const float x = fabsf(q[j]);
+            sq |= (q[j] < 0.0f ? 1u : 0u) << j;
+            if (x < m1) { m2 = m1; have2 = true; m1 = x; i1 = j; }
+            else if (!have2 || x < m2) { m2 = x; have2 = true; }
+        }
+        const uint32_t par = __popc(sq) & 1u;
+        float A = __fsub_rn(__fmul_rn(a.alpha, m1), a.beta);
+        A = A < 0.0f ? 0.0f : A;
+        float B = __fsub_rn(__fmul_rn(a.alpha, m2), a.beta);
+        B = B < 0.0f ? 0.0f : B;
+        const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;         // s = prod of the others
+        const size_t so = (size_t)m[r] * 32 + lane;
+        __stcg(stt + so, __float_as_uint(A));
+        __stcg(stt + ss + so, __float_as_uint(B));
+        __stcg(stt + 2 * ss + so, sg | ((uint32_t)i1 << 16));
+        if (!frozen) {
+#pragma unroll
+            for (int j = 0; j < DC; ++j) {
+                const float mag = (j == i1) ? B : A;
+                atomicAdd(Lat + off[r][j], ((sg >> j) & 1u) ? -mag : mag);     // Z^(k)_n += L^(k)_mn
+            }
+        }
     }
-    const uint32_t par = __popc(sq) & 1u;
-    float A = __fsub_rn(__fmul_rn(a.alpha, m1), a.beta);
-    A = A < 0.0f ? 0.0f : A;
-    float B = __fsub_rn(__fmul_rn(a.alpha, m2), a.beta);
-    B = B < 0.0f ? 0.0f : B;
-    const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;             // s = prod of the others
-    __stcg(stb + so, __float_as_uint(A));
-    __stcg(stb + ss + so, __float_as_uint(B));
-    __stcg(stb + 2 * ss + so, sg | ((uint32_t)i1 << 16));
-    if (frozen) return;
-#pragma unroll
-    for (int j = 0; j < DC; ++j) {
-        const float mag = (j == i1) ? B : A;
-        atomicAdd(La + idx[j], ((sg >> j) & 1u) ? -mag : mag);             // Z^(k)_n += L^(k)_mn
+}
+
+template <int NR, bool ES>
+__device__ __forceinline__ void stream_dispatch_f(int dc, const StreamArgs &a, int lane, const int (&m)[NR],
+                                                  const RowT *rt, const float *Lpt, float *Lat, uint32_t *stt,
+                                                  bool first_iter, bool frozen, uint32_t &synd) {
+    switch (dc) {
+    case 2: stream_rows_f<2, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 3: stream_rows_f<3, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 4: stream_rows_f<4, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 5: stream_rows_f<5, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 6: stream_rows_f<6, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 7: stream_rows_f<7, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 8: stream_rows_f<8, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 9: stream_rows_f<9, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 10: stream_rows_f<10, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 11: stream_rows_f<11, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 12: stream_rows_f<12, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 13: stream_rows_f<13, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 14: stream_rows_f<14, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 15: stream_rows_f<15, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 16: stream_rows_f<16, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
     }
 }
 
 template <bool ES>
-__global__ void __launch_bounds__(256) k_stream_iter_f(const StreamArgs a, int k) {
+__device__ __forceinline__ void stream_dispatch2_f(int dc, const StreamArgs &a, int lane, const int (&m)[2],
+                                                   const RowT *rt, const float *Lpt, float *Lat, uint32_t *stt,
+                                                   bool first_iter, bool frozen, uint32_t &synd) {
+    switch (dc) {
+    case 2: stream_rows_f<2, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 3: stream_rows_f<3, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 4: stream_rows_f<4, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 5: stream_rows_f<5, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 6: stream_rows_f<6, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    case 7: stream_rows_f<7, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+    }
+}
+
+template <bool ES>
+__global__ void __launch_bounds__(256, 3) k_stream_iter_f(const StreamArgs a, int k) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nwg = gridDim.x * (blockDim.x >> 5);
-    const float *Lp = (const float *)a.Lb[(k - 1) % 3];
-    float *La = (float *)a.Lb[k % 3];
-    uint32_t *Ln = a.Lb[(k + 1) % 3];
+    const size_t plane = (size_t)tile * a.N * 32;
+    const float *Lpt = (const float *)a.Lb[(k - 1) % 3] + plane;
+    float *Lat = (float *)a.Lb[k % 3] + plane;
+    uint32_t *Lnt = a.Lb[(k + 1) % 3] + plane;
+    uint32_t *stt = a.st + (size_t)tile * 3 * a.M * 32;
     bool frozen = false;
     if (ES) {
         frozen = (a.done[tile * 32 + lane] & 1u) != 0;
         if (__all_sync(0xFFFFFFFFu, frozen)) return;
     }
     if (k < a.K) {
-        for (int n = wg; n < a.N; n += nwg) {
-            const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
-            if (!frozen) __stcg(Ln + idx, __ldcg(a.Z0 + idx));
+        if (!ES || !__any_sync(0xFFFFFFFFu, frozen)) {
+            stream_init_next(a.Z0 + plane, Lnt, a.N, wg, nwg, lane);
+        } else {
+            for (int n = wg; n < a.N; n += nwg) {
+                const size_t idx = (size_t)n * 32 + lane;
+                if (!frozen) __stcg(Lnt + idx, __ldcg(a.Z0 + plane + idx));
+            }
         }
     }
     uint32_t synd = 0;
     const bool first_iter = (k == 1);
     for (int m = wg; m < a.M; m += nwg) {
-        const int e0 = __ldg(a.row_ptr + m), dc = __ldg(a.row_ptr + m + 1) - e0;
-        switch (dc) {
-        case 2: stream_row_f<2, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 3: stream_row_f<3, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 4: stream_row_f<4, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 5: stream_row_f<5, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 6: stream_row_f<6, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 7: stream_row_f<7, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 8: stream_row_f<8, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 9: stream_row_f<9, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 10: stream_row_f<10, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 11: stream_row_f<11, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 12: stream_row_f<12, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 13: stream_row_f<13, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 14: stream_row_f<14, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 15: stream_row_f<15, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        case 16: stream_row_f<16, ES>(a, tile, lane, m, e0, Lp, La, first_iter, frozen, synd); break;
-        }
+        const RowT rt = load_rowt(a.rowtab, m, a.M);
+        int dc = rt.dc;
+        if (dc == 15) dc = __ldg(a.row_ptr + m + 1) - __ldg(a.row_ptr + m);
+        const int mm[1] = {m};
+        stream_dispatch_f<1, ES>(dc, a, lane, mm, &rt, Lpt, Lat, stt, first_iter, frozen, synd);
     }
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
 }

@@ -67,6 +67,7 @@ struct ldpc_code {
     int max_dc = 0, max_dv = 0;
     // device CSR (stream kernels)
     int32_t *d_row_ptr = nullptr, *d_col_idx = nullptr;
+    uint32_t *d_rowtab = nullptr;   // [M][8] padded column table (streaming kernels)
     // resident schedule
     bool qc = false;
     int Z = 0, mb = 0, nb = 0;
@@ -146,6 +147,7 @@ static void free_code(ldpc_code *c) {
     if (!c) return;
     cudaFree(c->d_row_ptr);
     cudaFree(c->d_col_idx);
+    cudaFree(c->d_rowtab);
     delete c->qtab;
     cudaFree(c->d_bptr);
     cudaFree(c->d_colT);
@@ -188,6 +190,18 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
         return st;
     }
     const int N = c->N, M = c->M;
+    {
+        std::vector<uint32_t> rt((size_t)M * 8, 0u);
+        for (int m = 0; m < M; ++m) {
+            const int32_t a = desc->row_ptr[m], b = desc->row_ptr[m + 1];
+            const int dc = b - a;
+            if (dc <= 8)
+                for (int32_t e = a; e < b; ++e) rt[(size_t)m * 8 + (e - a)] = (uint32_t)desc->col_idx[e];
+            rt[(size_t)m * 8] |= (uint32_t)(dc <= 8 ? dc : 15) << 28;
+        }
+        if (N >= (1 << 28)) { free_code(c); return fail(LDPC_ERR_UNSUPPORTED, "n_vars >= 2^28"); }
+        if ((st = upload(&c->d_rowtab, rt.data(), rt.size())) != LDPC_OK) { free_code(c); return st; }
+    }
     // ---------- resident schedule (only when a frame pair's double buffer fits in shared memory)
     if (c->max_dc <= kMaxDC && (size_t)2 * N * 4 + 16384 <= c->smem_optin) {
         int nqent = 0;
@@ -577,6 +591,7 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     a.beta = pl.betaf;
     a.row_ptr = c->d_row_ptr;
     a.col_idx = c->d_col_idx;
+    a.rowtab = (const uint4 *)c->d_rowtab;
     a.llr = llr;
     a.Z0 = (uint32_t *)(w + pl.off_z0);
     for (int i = 0; i < 3; ++i) a.Lb[i] = (uint32_t *)(w + pl.off_lb[i]);

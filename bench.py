@@ -36,9 +36,10 @@ L2_FLUSH_BYTES = 256 << 20
 # bytes/iter/frame = N (w_Z0 + 2 w_L) + 2 M w_state.
 W_BYTES = {1: (2, 2, 4), 2: (2, 2, 4), 3: (1, 2, 2.375), 4: (2, 2, 4), 5: (4, 4, 12)}
 # Algorithmic integer operations per edge-update of the method:
-# rebuild L_old (select magnitude, apply sign), q = Z - L_old, |q|, two-minimum
-# update (2 compares), sign product, new message (select, sign, exclusion), Z += L.
-ALG_OPS_PER_EU = 12
+# rebuild L_old = s f(A,B,n,ñ) (compare n==ñ, select, sign: 3), q = Z - L_old (1),
+# |q| and sgn q (2), two-minimum update (compare + 2 selects: 3), sign product (1),
+# new message (compare, select, sign of the others, apply: 4), Z += L (1) = 15.
+ALG_OPS_PER_EU = 15
 
 
 def describe(cfg, code):
@@ -264,7 +265,7 @@ def main():
         roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / peaks["hbm_gbs"], "traffic": None}
     roof["peak_source"] = peak_src
-    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg.idx}.json")
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg.idx}.json")   # from tools/ncu_summary.py
     if os.path.exists(prof):
         with open(prof) as f:
             roof["traffic"] = json.load(f).get("dram_bytes_per_launch")

@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
     const int nb = QC ? t.nsb : a.nbatch;
     if (tid == 0) mbar_init(&zbar, 1);
     const uint32_t tbase = tmem_alloc_cta(&tslot, a.tmem_cols);   // includes a block barrier
-    const uint32_t tw = tmem_warp_base(tbase) + (uint32_t)(grp * a.cols_per_group);
+    // TMEM lanes are per warp quadrant (warp % 4): threads 128..255 use a second column range
+    const uint32_t tw = tmem_warp_base(tbase) + (uint32_t)((tid >> 7) * a.cols_per_group);
     uint32_t *z0w = a.ws + (size_t)blockIdx.x * a.slot_words;
     const TIN *llr = (const TIN *)a.llr;
     const uint32_t zbytes = 4u * (uint32_t)a.Np;

@@ -473,7 +473,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (pl.path == PATH_RESIDENT) {
         // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group
         pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * c->nbatch;
-        const int groups = c->qc ? c->res_threads / c->group_threads : (c->res_threads + 127) / 128;
+        const int groups = (c->res_threads + 127) / 128;   // 128-thread TMEM lane slices
         uint32_t need = (uint32_t)(pl.cols_per_group * groups), cols = 32;
         while (cols < need) cols <<= 1;
         if (cols > 512) return fail(LDPC_ERR_UNSUPPORTED, "compact state needs %u TMEM columns (> 512)", need);

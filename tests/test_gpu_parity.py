@@ -271,3 +271,44 @@ def test_batch_composition_invariance():
     again = gpu_decode(code, llr, params)
     for a, b in zip(full, again):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("shape", [(3, 6, 200), (4, 9, 33), (2, 5, 129)], ids=lambda s: f"qc{s[0]}x{s[1]}Z{s[2]}")
+def test_qc_group_layouts(shape):
+    """QC codes with Z > 128 (one thread group per batch) and Z not a multiple of 32."""
+    mb, nb, Z = shape
+    w = np.array(([3, 2] * nb)[:nb], np.int32)
+    w = np.minimum(w, mb)
+    code = g.qc(mb, nb, Z, w, seed=Z)
+    s2 = g.ebn0_to_sigma2(1.5, max(code.rate, 0.3))
+    for F in (3, 64):
+        llr = g.llr(9 + F, 0, F, code.n_vars, s2, g.LLR_I16, 3, 511)
+        for es in (0, 1):
+            params = P.make_params(8, es, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+            assert_int_parity(code, llr, params, 8, es, 1, 511)
+
+
+def test_wide_rows_f32_and_unsupported_int():
+    """Row degree 12: fp32 path (<= 16) decodes within tolerance; integer paths report UNSUPPORTED."""
+    code = g.regular(120, 6, 12, seed=2, remove_4cycles=False)
+    s2 = g.ebn0_to_sigma2(3.0, code.rate)
+    llr = g.llr(4, 0, 20, code.n_vars, s2, g.LLR_F32)
+    params = P.make_params(8, 1, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    ref = oracle.decode(code, llr, "compact", "f32", 8, 1, alpha=0.75, nthreads=NT)
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    dec = decoder(code)
+    with pytest.raises(P.LdpcError) as e:
+        dec.workspace(4, P.make_params(8, 0, P.LDPC_MINSUM_OFFSET, 1, 0, 1.0, 63, P.LDPC_LLR_I16))
+    assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+
+
+def test_clamp_and_offset_variants_int():
+    """Other clamps / offsets than the configs' (Q = 63, 255; beta = 0, 3) on the cfg1 code."""
+    cfg = g.CONFIGS[1]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, 40)
+    for Q, beta in ((63, 0), (255, 3), (511, 0)):
+        z = np.clip(llr, -Q, Q)
+        params = P.make_params(12, 1, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+        assert_int_parity(code, z, params, 12, 1, beta, Q)

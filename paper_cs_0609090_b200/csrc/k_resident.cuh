@@ -38,12 +38,13 @@ struct QcTab {
     uint32_t Z4;                        // 4 * Z (bytes)
     int32_t e0[kQcMaxSB][kQcGroups];    // first entry of the base row handled by group g
     int32_t dc[kQcMaxSB][kQcGroups];    // its degree (0 = group idle in this super-batch)
+    int32_t run_end[kQcMaxSB][kQcGroups];  // first later super-batch where the group's degree changes
     uint2 ent[kQcMaxEnt];               // (4 * shift, 4 * (j * Z)) per base-matrix entry
 };
 
 struct ResArgs {
     int N, Np, M, npairs, nframes, K, Qsat, wpf;   // Np = N rounded up to 4; wpf = ceil(N/32)
-    uint32_t nbeta2, q2;
+    uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp
     const void *llr;
     uint32_t *hard_bits;
     int16_t *post;
@@ -119,7 +120,7 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
         rebuild_q<DC>(L, st, q);
     }
     uint32_t rn[DC];
-    new_state<DC>(q, a.nbeta2, a.q2, st, rn);
+    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn);
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         uint32_t *pa = (uint32_t *)(Lab + off[j]);
@@ -232,6 +233,41 @@ __device__ __forceinline__ void state_tmem_store(uint32_t tw, int b, int nb, con
     }
 }
 
+// Consecutive super-batches in which this group's rows have the same degree DC are
+// processed by one loop (one dispatch per run instead of per batch).
+template <int DC, bool ES, int FMT>
+__device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, uint32_t tw, int nb,
+                                      int rloc, uint32_t r4, const char *Lpb, char *Lab, bool first_iter,
+                                      uint32_t &synd) {
+#pragma unroll 1
+    for (; b < bend; ++b) {
+        RowState st = {0u, 0u, 0u};
+        if constexpr (DC > 0) {
+            if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
+            if (rloc < a.Z) res_row<DC, true, ES>(a, t, Lpb, Lab, t.e0[b][g], r4, 0, first_iter, st, synd);
+            state_tmem_store<FMT>(tw, b, nb, st);
+        }
+        __syncthreads();                         // batch b's accumulations complete
+    }
+    return b;
+}
+
+template <bool ES, int FMT>
+__device__ __forceinline__ int qc_run_dispatch(int dc, int b, int bend, int g, const ResArgs &a, const QcTab &t,
+                                               uint32_t tw, int nb, int rloc, uint32_t r4, const char *Lpb, char *Lab,
+                                               bool first_iter, uint32_t &synd) {
+    switch (dc) {
+    case 2: return qc_run<2, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 3: return qc_run<3, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 4: return qc_run<4, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 5: return qc_run<5, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 6: return qc_run<6, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 7: return qc_run<7, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 8: return qc_run<8, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    default: return qc_run<0, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    }
+}
+
 template <bool QC, bool ES, int FMT, typename TIN>
 __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __grid_constant__ QcTab t) {
     extern __shared__ __align__(128) uint32_t smem[];
@@ -281,25 +317,23 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
             if (k > 1) { mbar_wait(&zbar, zphase); zphase ^= 1; }   // La = Z^(0) has landed
             uint32_t synd = 0;
             const bool first_iter = (k == 1);
+            if (QC) {
+                // warp-uniform group branch: uniform table indices
 #pragma unroll 1
-            for (int b = 0; b < nb; ++b) {
-                RowState st = {0u, 0u, 0u};
-                if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-                if (QC) {
-                    // warp-uniform group branch so the table index is uniform
-                    if (grp == 0) {
-                        const int dc = t.dc[b][0];
-                        if (rloc < a.Z && dc) res_dispatch<QC, ES>(dc, a, t, Lpb, Lab, t.e0[b][0], r4, 0, first_iter, st, synd);
-                    } else {
-                        const int dc = t.dc[b][1];
-                        if (rloc < a.Z && dc) res_dispatch<QC, ES>(dc, a, t, Lpb, Lab, t.e0[b][1], r4, 0, first_iter, st, synd);
-                    }
-                } else {
+                for (int b = 0; b < nb;) {
+                    if (grp == 0) b = qc_run_dispatch<ES, FMT>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+                    else b = qc_run_dispatch<ES, FMT>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+                }
+            } else {
+#pragma unroll 1
+                for (int b = 0; b < nb; ++b) {
+                    RowState st = {0u, 0u, 0u};
+                    if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
                     const int p = a.bptr[b] + tid;
                     if (p < a.bptr[b + 1]) res_dispatch<QC, ES>(a.dcT[p], a, t, Lpb, Lab, 0, 0, p, first_iter, st, synd);
+                    state_tmem_store<FMT>(tw, b, nb, st);
+                    __syncthreads();                     // batch b's accumulations complete
                 }
-                state_tmem_store<FMT>(tw, b, nb, st);
-                __syncthreads();                     // batch b's accumulations complete
             }
             tmem_wait_st();
             if (ES) {

@@ -25,7 +25,7 @@ __device__ __forceinline__ uint32_t from_vform(uint32_t v) { return v + ((v & 0x
 
 struct StreamArgs {
     int N, M, ntiles, nframes, K, Qsat, wpf;
-    uint32_t nbeta2, q2;
+    uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp
     float alpha, beta;           // fp32 variant: |L| <= max(alpha*min - beta, 0)
     const int32_t *row_ptr, *col_idx;
     const uint4 *rowtab;         // [M][2]: up to 8 column indices per row; dc in bits 28-31 of word 0 (15 = wider row)
@@ -133,7 +133,7 @@ __device__ __forceinline__ void stream_rows_i(const StreamArgs &a, int lane, con
             rebuild_q<DC>(L[r], st[r], q);
         }
         uint32_t rn[DC];
-        new_state<DC>(q, a.nbeta2, a.q2, st[r], rn);
+        new_state<DC>(q, a.nbeta2p1, a.q2p1, st[r], rn);
         StateIO<FMT>::store(stt + lane, sstride, (size_t)m[r] * 32, st[r]);
 #pragma unroll
         for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], to_vform(rn[j] & ~keep));

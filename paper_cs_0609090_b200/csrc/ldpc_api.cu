@@ -269,6 +269,12 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
             } else {
                 for (int i = 0; i < c->mb; ++i) sb.emplace_back(i, -1);
             }
+            // order super-batches by the groups' degrees so equal-degree runs are long
+            std::stable_sort(sb.begin(), sb.end(), [&](const std::pair<int, int> &x, const std::pair<int, int> &y) {
+                auto deg = [&](int i) { return i >= 0 ? (int)cols[i].size() : 0; };
+                if (deg(x.first) != deg(y.first)) return deg(x.first) > deg(y.first);
+                return deg(x.second) > deg(y.second);
+            });
             t.nsb = (int)sb.size();
             for (int b = 0; b < t.nsb; ++b) {
                 const int rows[2] = {sb[b].first, sb[b].second};
@@ -278,6 +284,9 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                     t.dc[b][g] = i >= 0 ? (int)cols[i].size() : 0;
                 }
             }
+            for (int g = 0; g < kQcGroups; ++g)
+                for (int b = t.nsb - 1; b >= 0; --b)
+                    t.run_end[b][g] = (b + 1 < t.nsb && t.dc[b + 1][g] == t.dc[b][g]) ? t.run_end[b + 1][g] : b + 1;
             c->nbatch = t.nsb;
             c->group_threads = groups == 2 ? 128 : ((c->Z + 31) / 32) * 32;
             c->res_threads = groups * c->group_threads;
@@ -536,8 +545,8 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.K = p->max_iter;
     a.Qsat = pl.Q;
     a.wpf = (c->N + 31) / 32;
-    a.nbeta2 = pack2(-2 * pl.beta, -2 * pl.beta);
-    a.q2 = pack2(2 * pl.Q, 2 * pl.Q);
+    a.nbeta2p1 = pack2(1 - 2 * pl.beta, 1 - 2 * pl.beta);
+    a.q2p1 = pack2(2 * pl.Q + 1, 2 * pl.Q + 1);
     a.llr = llr;
     a.hard_bits = hb;
     a.post = (int16_t *)post;
@@ -585,8 +594,8 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     a.K = p->max_iter;
     a.Qsat = pl.Q;
     a.wpf = (c->N + 31) / 32;
-    a.nbeta2 = pack2(-2 * pl.beta, -2 * pl.beta);
-    a.q2 = pack2(2 * pl.Q, 2 * pl.Q);
+    a.nbeta2p1 = pack2(1 - 2 * pl.beta, 1 - 2 * pl.beta);
+    a.q2p1 = pack2(2 * pl.Q + 1, 2 * pl.Q + 1);
     a.alpha = pl.alpha;
     a.beta = pl.betaf;
     a.row_ptr = c->d_row_ptr;

@@ -11,11 +11,11 @@
 //   A, B : doubled magnitudes 2A_m, 2B_m in each 16-bit half (B >= A)
 //   W    : per-edge bits, byte-interleaved so one shift + PRMT expands them to
 //          16-bit masks.  For edge pair i (edges 2i, 2i+1):
-//            byte0 bit i  : s of edge 2i,   frame lo     byte0 bit 4+i : !idx, edge 2i,   lo
-//            byte1 bit i  : s of edge 2i+1, frame lo     byte1 bit 4+i : !idx, edge 2i+1, lo
-//            byte2 bit i  : s of edge 2i,   frame hi     byte2 bit 4+i : !idx, edge 2i,   hi
-//            byte3 bit i  : s of edge 2i+1, frame hi     byte3 bit 4+i : !idx, edge 2i+1, hi
-//          s bit = 1 means L_mn < 0; "!idx" bit = 1 means n != ñ_m.  dc <= 8.
+//            byte0 bit i  : s of edge 2i,   frame lo     byte0 bit 4+i : idx, edge 2i,   lo
+//            byte1 bit i  : s of edge 2i+1, frame lo     byte1 bit 4+i : idx, edge 2i+1, lo
+//            byte2 bit i  : s of edge 2i,   frame hi     byte2 bit 4+i : idx, edge 2i,   hi
+//            byte3 bit i  : s of edge 2i+1, frame hi     byte3 bit 4+i : idx, edge 2i+1, hi
+//          s bit = 1 means L_mn < 0; "idx" bit = 1 means n is an argmin (n = ñ_m).  dc <= 8.
 #pragma once
 #include "simd16.cuh"
 
@@ -33,15 +33,15 @@ __device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowStat
 #pragma unroll
     for (int i = 0; i < (DC + 1) / 2; ++i) {
         const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte
-        const uint32_t wo = st.W << (3 - i);       // !idx bits of pair i -> bit 7 of each byte
+        const uint32_t wo = st.W << (3 - i);       // idx bits of pair i -> bit 7 of each byte
         {
-            const uint32_t sm = prmt(ws, 0u, 0xAA88u), ni = prmt(wo, 0u, 0xAA88u);
-            const uint32_t mag = sel(ni, st.A, st.B), nmag = sel(ni, nA, nB);
+            const uint32_t sm = prmt(ws, 0u, 0xAA88u), ix = prmt(wo, 0u, 0xAA88u);
+            const uint32_t mag = sel(ix, st.B, st.A), nmag = sel(ix, nB, nA);
             q[2 * i] = vadd(L[2 * i], sel(sm, mag, nmag));      // Z - L_old: L_old = s*mag
         }
         if (2 * i + 1 < DC) {
-            const uint32_t sm = prmt(ws, 0u, 0xBB99u), ni = prmt(wo, 0u, 0xBB99u);
-            const uint32_t mag = sel(ni, st.A, st.B), nmag = sel(ni, nA, nB);
+            const uint32_t sm = prmt(ws, 0u, 0xBB99u), ix = prmt(wo, 0u, 0xBB99u);
+            const uint32_t mag = sel(ix, st.B, st.A), nmag = sel(ix, nB, nA);
             q[2 * i + 1] = vadd(L[2 * i + 1], sel(sm, mag, nmag));
         }
     }
@@ -85,9 +85,9 @@ __device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, u
 //   A = min(max(min1 - beta, 0), Q), B = min(max(min2 - beta, 0), Q)  (readings D5, D6)
 //   ñ = argmin |q| (ties: any minimiser -- unobservable, A = B then; reading D3)
 //   s_mn = prod_{n' != n} sgn(q_mn')  (sgn(0) = +1, reading D1)
-// nbeta2 = packed (-2 beta, -2 beta), q2 = packed (2Q, 2Q).
+// nbeta2p1 = packed (1 - 2 beta), q2p1 = packed (2Q + 1).
 template <int DC>
-__device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbeta2, uint32_t q2, RowState &st,
+__device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbeta2p1, uint32_t q2p1, RowState &st,
                                           uint32_t (&r)[DC]) {
     uint32_t mt[DC];
 #pragma unroll
@@ -98,30 +98,31 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbet
 #pragma unroll
     for (int j = 1; j < DC; ++j) par ^= q[j];
     const uint32_t Pm = signmask(par);                          // product of all signs < 0
-    // doubled magnitudes: 2|q| = m~ + (m~ & 1)
-    const uint32_t a2 = vadd(m1, m1 & 0x00010001u), b2 = vadd(m2, m2 & 0x00010001u);
-    const uint32_t A = vaddmin_relu(a2, nbeta2, q2), B = vaddmin_relu(b2, nbeta2, q2);
+    // A = clamp(2|q|min - 2 beta, 0, 2Q) on doubled values: with m~ in {2|q|-1, 2|q|},
+    // relu(min(m~ + 1 - 2 beta, 2Q + 1)) with the low bit cleared is exact (one VIADDMNMX + LOP3).
+    const uint32_t A = vaddmin_relu(m1, nbeta2p1, q2p1) & 0xFFFEFFFEu;
+    const uint32_t B = vaddmin_relu(m2, nbeta2p1, q2p1) & 0xFFFEFFFEu;
     const uint32_t nA = vneg(A), nB = vneg(B);
     // message for an edge whose own q is >= 0 carries the sign of the full product
     const uint32_t Apos = sel(Pm, nA, A), Aneg = sel(Pm, A, nA);
     const uint32_t Bpos = sel(Pm, nB, B), Bneg = sel(Pm, B, nB);
-    const uint32_t nm1 = vneg(m1);
-    uint32_t W = 0, sqp = 0, nip = 0;
+    const uint32_t cm1 = ~m1;                                   // -m1 - 1
+    uint32_t W = 0, sqp = 0, ixp = 0;
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        const uint32_t ni = vaddmin(mt[j], nm1, 0x00010001u) * 0xFFFFu;   // 0xFFFF: not an argmin
-        const uint32_t sq = signmask(q[j]);                               // 0xFFFF: q < 0
-        r[j] = sel(sq, sel(ni, Aneg, Bneg), sel(ni, Apos, Bpos));
+        const uint32_t ix = vaddmin(mt[j], cm1, 0u);            // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
+        const uint32_t sq = signmask(q[j]);                     // 0xFFFF: q < 0
+        r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
         if ((j & 1) == 0) {
             sqp = sq;
-            nip = ni;
+            ixp = ix;
             if (j == DC - 1) {
                 W |= prmt(sqp, 0u, 0x6240u) & (0x01010101u << (j >> 1));
-                W |= prmt(nip, 0u, 0x6240u) & (0x10101010u << (j >> 1));
+                W |= prmt(ixp, 0u, 0x6240u) & (0x10101010u << (j >> 1));
             }
         } else {
             W |= prmt(sqp, sq, 0x6240u) & (0x01010101u << (j >> 1));
-            W |= prmt(nip, ni, 0x6240u) & (0x10101010u << (j >> 1));
+            W |= prmt(ixp, ix, 0x6240u) & (0x10101010u << (j >> 1));
         }
     }
     W ^= Pm & 0x0F0F0F0Fu;                                      // s = sgn(q) * product

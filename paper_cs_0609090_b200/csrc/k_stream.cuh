@@ -470,7 +470,7 @@ __device__ __forceinline__ void stream_dispatch2_f(int dc, const StreamArgs &a, 
 }
 
 template <bool ES>
-__global__ void __launch_bounds__(256, 3) k_stream_iter_f(const StreamArgs a, int k) {
+__global__ void __launch_bounds__(256, 4) k_stream_iter_f(const StreamArgs a, int k) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nwg = gridDim.x * (blockDim.x >> 5);

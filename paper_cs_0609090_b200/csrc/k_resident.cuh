@@ -60,6 +60,7 @@ struct ResArgs {
     int group_threads;                // QC: threads per group (128 with two groups)
     uint32_t tmem_cols;               // TMEM columns allocated per CTA
     int cols_per_group;               // TMEM columns used by one group of threads
+    uint32_t zero;                    // 0, kept in a register (operand of VIADDMNMX)
 };
 
 template <typename TIN>
@@ -97,20 +98,28 @@ __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.pr
 template <int DC, bool QC, bool ES>
 __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const char *Lpb, char *Lab, int e0,
                                         uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
-    uint32_t off[DC];
+    // shared-memory byte addresses of the row's variables in both buffers:
+    // 4 * (jZ + (r + s) mod Z) + base, one VIADDMNMX for the modulo and one IADD3 per buffer
+    const uint32_t bp = (uint32_t)__cvta_generic_to_shared(Lpb), ba = (uint32_t)__cvta_generic_to_shared(Lab);
+    uint32_t op[DC], oa[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
+        uint32_t d, cb;
         if (QC) {
             const uint2 e = t.ent[e0 + j];
             const uint32_t u = r4 + e.x;
-            off[j] = min(u - t.Z4, u) + e.y;                // 4 * (jZ + (r + s) mod Z)
+            d = min(u - t.Z4, u);
+            cb = e.y;
         } else {
-            off[j] = __ldg(a.colT + (size_t)j * a.M + p);
+            d = __ldg(a.colT + (size_t)j * a.M + p);
+            cb = 0u;
         }
+        op[j] = d + cb + bp;
+        oa[j] = d + cb + ba;
     }
     uint32_t L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = *(const uint32_t *)(Lpb + off[j]);
+    for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(op[j]));
     if (ES) synd |= row_parity<DC>(L);
     uint32_t q[DC];
     if (first_iter) {
@@ -120,11 +129,12 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
         rebuild_q<DC>(L, st, q);
     }
     uint32_t rn[DC];
-    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn);
+    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.zero);
 #pragma unroll
-    for (int j = 0; j < DC; ++j) {
-        uint32_t *pa = (uint32_t *)(Lab + off[j]);
-        *pa = vadd(*pa, rn[j]);                              // Z^(k)_n += L^(k)_mn
+    for (int j = 0; j < DC; ++j) {                           // Z^(k)_n += L^(k)_mn
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(oa[j]) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(oa[j]), "r"(vadd(v, rn[j])) : "memory");
     }
 }
 

@@ -88,7 +88,7 @@ __device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, u
 // nbeta2p1 = packed (1 - 2 beta), q2p1 = packed (2Q + 1).
 template <int DC>
 __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbeta2p1, uint32_t q2p1, RowState &st,
-                                          uint32_t (&r)[DC]) {
+                                          uint32_t (&r)[DC], uint32_t zero = 0u) {
     uint32_t mt[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) mt[j] = vmax(q[j], ~q[j]);   // 2|q| - [q<0]
@@ -110,7 +110,7 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbet
     uint32_t W = 0, sqp = 0, ixp = 0;
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        const uint32_t ix = vaddmin(mt[j], cm1, 0u);            // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
+        const uint32_t ix = vaddmin(mt[j], cm1, zero);          // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
         const uint32_t sq = signmask(q[j]);                     // 0xFFFF: q < 0
         r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
         if ((j & 1) == 0) {

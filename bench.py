@@ -252,7 +252,9 @@ def main():
     resident = launches_per_step == 1
     if resident:
         clk = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-        peak_ops = 148 * 128 * 2 * clk * 1e6 / 1e12     # 16x2 SIMD int ops/s (TOP/s), DESIGN.md §5.2
+        # 16-bit integer ops: ALU pipe 64 lanes/clk/SM (VIADD/VIMNMX/LOP3/PRMT all issue
+        # there) x 2 frames per lane (16x2 SIMD) x 148 SMs x SM clock
+        peak_ops = 148 * 64 * 2 * clk * 1e6 / 1e12
         achieved = ALG_OPS_PER_EU * my_eu / (my_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
                 "frac": achieved / peak_ops, "traffic": None,

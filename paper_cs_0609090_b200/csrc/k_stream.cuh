@@ -170,7 +170,10 @@ __device__ __forceinline__ void stream_dispatch2_i(int dc, const StreamArgs &a, 
 }
 
 template <int FMT, bool ES>
-__global__ void __launch_bounds__(256, 3) k_stream_iter_i(const StreamArgs a, int k) {
+#ifndef LDPC_STREAM_NR2
+#define LDPC_STREAM_NR2 0
+#endif
+__global__ void __launch_bounds__(256, LDPC_STREAM_NR2 ? 2 : 3) k_stream_iter_i(const StreamArgs a, int k) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nwg = gridDim.x * (blockDim.x >> 5);
@@ -201,11 +204,29 @@ __global__ void __launch_bounds__(256, 3) k_stream_iter_i(const StreamArgs a, in
     uint32_t synd = 0;
     const bool first_iter = (k == 1);
     // row tables of the next row pair are prefetched while the current pair is processed
+#if LDPC_STREAM_NR2
+    for (int m0 = wg; m0 < a.M; m0 += 2 * nwg) {
+        const int m1 = m0 + nwg;
+        const RowT rt[2] = {load_rowt(a.rowtab, m0, a.M), load_rowt(a.rowtab, m1, a.M)};
+        if (rt[0].dc == rt[1].dc && rt[0].dc <= 7) {
+            const int mm[2] = {m0, m1};
+            stream_dispatch2_i<FMT, ES>(rt[0].dc, a, lane, mm, rt, Lpt, Lat, stt, first_iter, keep, synd);
+        } else {
+            const int mm0[1] = {m0};
+            stream_dispatch_i<1, FMT, ES>(rt[0].dc, a, lane, mm0, rt, Lpt, Lat, stt, first_iter, keep, synd);
+            if (rt[1].dc) {
+                const int mm1[1] = {m1};
+                stream_dispatch_i<1, FMT, ES>(rt[1].dc, a, lane, mm1, rt + 1, Lpt, Lat, stt, first_iter, keep, synd);
+            }
+        }
+    }
+#else
     for (int m = wg; m < a.M; m += nwg) {
         const RowT rt = load_rowt(a.rowtab, m, a.M);
         const int mm[1] = {m};
         stream_dispatch_i<1, FMT, ES>(rt.dc, a, lane, mm, &rt, Lpt, Lat, stt, first_iter, keep, synd);
     }
+#endif
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
 }
 

@@ -16,6 +16,7 @@
 
 #include "../../include/ldpc.h"
 #include "k_resident.cuh"
+#include "k_resident_mp.cuh"
 #include "k_stream.cuh"
 
 using namespace ldpc;
@@ -387,6 +388,7 @@ struct Plan {
     size_t slot_words = 0;
     uint32_t tmem_cols = 0;
     int cols_per_group = 0;
+    int np = 1;                  // frame pairs per CTA (multi-pair QC kernel when > 1)
     // stream
     int tile = 64, ntiles = 0;
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
@@ -482,6 +484,28 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (pl.path == PATH_RESIDENT) {
         // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group
         pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * c->nbatch;
+        // multi-pair QC kernel: NP pairs per CTA, one CTA per SM.  Opt-in (LDPC_MP=1): it
+        // measured slower than one pair per CTA at 3 CTAs/SM on cfg2/cfg3.
+        const char *mpenv = getenv("LDPC_MP");
+        if (c->qc && mpenv && mpenv[0] == '1') {
+            const int groups = (c->res_threads + 127) / 128;
+            int np = (int)std::min<size_t>(3, c->smem_optin / (c->res_smem + 64));
+            while (np > 1 && (uint32_t)(groups * np * pl.cols_per_group) > 512) --np;
+            if (np >= 2) {
+                pl.np = np;
+                uint32_t need = (uint32_t)(groups * np * pl.cols_per_group), cols = 32;
+                while (cols < need) cols <<= 1;
+                pl.tmem_cols = cols;
+                const int64_t ngroups = (npairs + np - 1) / np;
+                pl.grid = (int)std::min<int64_t>(std::max<int64_t>(ngroups, 1), (int64_t)c->sm_count);
+                pl.slot_words = ((size_t)c->N + 63) & ~(size_t)63;
+                pl.ws_bytes = align256((size_t)pl.grid * np * pl.slot_words * 4);
+                if (getenv("LDPC_DEBUG"))
+                    fprintf(stderr, "[ldpc] resident-mp: np=%d threads=%d smem=%zu tmem_cols=%u grid=%d batches=%d\n", np,
+                            c->res_threads, (size_t)np * c->res_smem, cols, pl.grid, c->nbatch);
+                return LDPC_OK;
+            }
+        }
         const int groups = (c->res_threads + 127) / 128;   // 128-thread TMEM lane slices
         uint32_t need = (uint32_t)(pl.cols_per_group * groups), cols = 32;
         while (cols < need) cols <<= 1;
@@ -533,6 +557,30 @@ cudaError_t launch_res_t(const ldpc_code *c, const Plan &pl, const ResArgs &a, i
                                    : launch_res<QC, ES, FMT, int16_t>(c, pl, a, s);
 }
 
+template <int NP, bool ES, int FMT, typename TIN>
+cudaError_t launch_mp(const ldpc_code *c, const Plan &pl, const ResArgs &a, cudaStream_t s) {
+    auto kern = k_resident_mp<NP, ES, FMT, TIN>;
+    const size_t smem = (size_t)NP * c->res_smem;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<pl.grid, c->res_threads, smem, s>>>(a, *c->qtab);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+template <int NP, bool ES, int FMT>
+cudaError_t launch_mp_t(const ldpc_code *c, const Plan &pl, const ResArgs &a, int llr_type, cudaStream_t s) {
+    return llr_type == LDPC_LLR_I8 ? launch_mp<NP, ES, FMT, int8_t>(c, pl, a, s) : launch_mp<NP, ES, FMT, int16_t>(c, pl, a, s);
+}
+
+template <int NP>
+cudaError_t launch_mp_any(const ldpc_code *c, const Plan &pl, const ResArgs &a, bool es, int llr_type, cudaStream_t s) {
+    if (es) return pl.fmt == FMT_C16 ? launch_mp_t<NP, true, FMT_C16>(c, pl, a, llr_type, s)
+                                     : launch_mp_t<NP, true, FMT_1BIT>(c, pl, a, llr_type, s);
+    return pl.fmt == FMT_C16 ? launch_mp_t<NP, false, FMT_C16>(c, pl, a, llr_type, s)
+                             : launch_mp_t<NP, false, FMT_1BIT>(c, pl, a, llr_type, s);
+}
+
 cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_params *p, int64_t F,
                          const void *llr, uint32_t *hb, void *post, uint8_t *ok, int32_t *it, void *ws,
                          cudaStream_t s) {
@@ -564,6 +612,8 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.cols_per_group = pl.cols_per_group;
     const bool es = p->early_stop != 0;
     const int t = p->llr_type;
+    if (pl.np == 3) return launch_mp_any<3>(c, pl, a, es, t, s);
+    if (pl.np == 2) return launch_mp_any<2>(c, pl, a, es, t, s);
     if (c->qc) {
         if (es) return pl.fmt == FMT_C16 ? launch_res_t<true, true, FMT_C16>(c, pl, a, t, s)
                                          : launch_res_t<true, true, FMT_1BIT>(c, pl, a, t, s);

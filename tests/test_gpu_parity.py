@@ -312,3 +312,16 @@ def test_clamp_and_offset_variants_int():
         z = np.clip(llr, -Q, Q)
         params = P.make_params(12, 1, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
         assert_int_parity(code, z, params, 12, 1, beta, Q)
+
+
+def test_multi_pair_qc_kernel(monkeypatch):
+    """The opt-in multi-pair QC kernel (LDPC_MP=1: 3 frame pairs per CTA) is bit-exact too."""
+    monkeypatch.setenv("LDPC_MP", "1")
+    for idx in (2, 3):
+        cfg = g.CONFIGS[idx]
+        code = cfg.code()
+        llr = cfg.llrs(code, 0, 301)
+        assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, cfg.early_stop, cfg.offset_raw, cfg.clamp)
+    s2 = g.ebn0_to_sigma2(2.25, g.CONFIGS[2].code().rate)
+    llr = g.llr(99, 0, 200, g.CONFIGS[2].code().n_vars, s2, g.LLR_I16, 3, 511)
+    assert_int_parity(g.CONFIGS[2].code(), llr, _cfg_params(g.CONFIGS[2]), 15, 1, 1, 511)

@@ -1,0 +1,256 @@
+// k_stream_pipe.cuh -- software-pipelined streaming kernels (long codes).
+//
+// Same data layout and per-row arithmetic as k_stream.cuh, but every warp keeps
+// PD rows in flight: the 128-byte lines a row needs (its dc posterior lines and
+// its compact-state lines for the warp's 32 lanes) are copied global -> shared
+// with cp.async (LDGSTS, 16 B per lane) PD rows ahead of the row being computed,
+// so memory-level parallelism is set by the shared-memory ring, not by
+// registers.  A CTA owns a block of RB consecutive check rows of one frame tile;
+// their column tables are staged in shared memory once.  Accumulation into
+// Z^(k) stays a coalesced global RED (fire-and-forget).
+#pragma once
+#include "k_stream.cuh"
+
+namespace ldpc {
+
+constexpr int kPipeRB = 64;        // rows per CTA
+constexpr int kPipeWarps = 8;      // warps per CTA
+constexpr int kPipeD = 4;          // rows in flight per warp
+constexpr int kPipeLines = 11;     // 8 posterior lines + up to 3 state lines per row
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Issue the copies of one row's lines into a slot: lines 0..dc-1 are posterior lines
+// (variable col[l] of this tile), lines 8..8+nst-1 the state words of row m.
+__device__ __forceinline__ void pipe_issue_row(uint32_t slot, const uint32_t *Lpt, const uint32_t *stt, size_t sstride,
+                                               const uint32_t *cols, int dc, int nst, int m, int lane) {
+    const int nl = 8 + nst;
+    const int chunk = lane & 7;
+    for (int l0 = 0; l0 < nl; l0 += 4) {
+        const int l = l0 + (lane >> 3);
+        if (l < nl) {
+            const uint32_t *src = nullptr;
+            if (l < dc) src = Lpt + (size_t)cols[l] * 32;
+            else if (l >= 8) src = stt + (size_t)(l - 8) * sstride + (size_t)m * 32;
+            if (src) cp_async16(slot + (uint32_t)(l * 128 + chunk * 16), (const char *)src + chunk * 16);
+        }
+    }
+}
+
+template <int DC, int FMT, bool ES>
+__device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *sl, const uint32_t *cols, int m,
+                                           int lane, uint32_t *Lat, uint32_t *stt, size_t sstride, bool first_iter,
+                                           uint32_t keep, uint32_t &synd) {
+    uint32_t L[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) L[j] = from_vform(sl[j * 32 + lane]);
+    if (ES) synd |= row_parity<DC>(L);
+    RowState st;
+    uint32_t q[DC];
+    if (first_iter) {
+#pragma unroll
+        for (int j = 0; j < DC; ++j) q[j] = L[j];
+    } else {
+        if (FMT == FMT_C16) {
+            st.A = sl[8 * 32 + lane];
+            st.B = sl[9 * 32 + lane];
+            st.W = sl[10 * 32 + lane];
+        } else {
+            const uint32_t X = sl[8 * 32 + lane];
+            st.A = prmt(X, 0u, 0x4240u);
+            st.B = prmt(X, 0u, 0x4341u);
+            st.W = sl[9 * 32 + lane];
+        }
+        rebuild_q<DC>(L, st, q);
+    }
+    uint32_t rn[DC];
+    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn);
+    StateIO<FMT>::store(stt + lane, sstride, (size_t)m * 32, st);
+#pragma unroll
+    for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, to_vform(rn[j] & ~keep));
+}
+
+template <int DC, bool ES>
+__device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *sl, const uint32_t *cols, int m,
+                                           int lane, float *Lat, uint32_t *stt, size_t ss, bool first_iter,
+                                           bool frozen, uint32_t &synd) {
+    float L[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) L[j] = __uint_as_float(sl[j * 32 + lane]);
+    if (ES) {
+        uint32_t p = 0;
+#pragma unroll
+        for (int j = 0; j < DC; ++j) p ^= L[j] <= 0.0f ? 1u : 0u;
+        synd |= p;
+    }
+    float q[DC];
+    if (first_iter) {
+#pragma unroll
+        for (int j = 0; j < DC; ++j) q[j] = L[j];
+    } else {
+        const float A0 = __uint_as_float(sl[8 * 32 + lane]), B0 = __uint_as_float(sl[9 * 32 + lane]);
+        const uint32_t W0 = sl[10 * 32 + lane];
+        const int idx0 = (int)(W0 >> 16);
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            const float mag = (j == idx0) ? B0 : A0;                 // f(A,B,n,ñ)
+            const float lold = ((W0 >> j) & 1u) ? -mag : mag;        // s_mn f(...)
+            q[j] = __fsub_rn(L[j], lold);                            // Z_n' - L_mn'  (D11)
+        }
+    }
+    float m1 = fabsf(q[0]), m2 = 0.0f;
+    int i1 = 0;
+    bool have2 = false;
+    uint32_t sq = q[0] < 0.0f ? 1u : 0u;
+#pragma unroll
+    for (int j = 1; j < DC; ++j) {
+        const float x = fabsf(q[j]);
+        sq |= (q[j] < 0.0f ? 1u : 0u) << j;
+        if (x < m1) { m2 = m1; have2 = true; m1 = x; i1 = j; }
+        else if (!have2 || x < m2) { m2 = x; have2 = true; }
+    }
+    const uint32_t par = __popc(sq) & 1u;
+    float A = __fsub_rn(__fmul_rn(a.alpha, m1), a.beta);
+    A = A < 0.0f ? 0.0f : A;
+    float B = __fsub_rn(__fmul_rn(a.alpha, m2), a.beta);
+    B = B < 0.0f ? 0.0f : B;
+    const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;
+    const size_t so = (size_t)m * 32 + lane;
+    __stcg(stt + so, __float_as_uint(A));
+    __stcg(stt + ss + so, __float_as_uint(B));
+    __stcg(stt + 2 * ss + so, sg | ((uint32_t)i1 << 16));
+    if (!frozen) {
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            const float mag = (j == i1) ? B : A;
+            atomicAdd(Lat + (size_t)cols[j] * 32 + lane, ((sg >> j) & 1u) ? -mag : mag);
+        }
+    }
+}
+
+// PAIR = true: int16 pairs (V-form accumulators); false: fp32.
+template <bool PAIR, int FMT, bool ES>
+__global__ void __launch_bounds__(kPipeWarps * 32, 3) k_stream_pipe(const StreamArgs a, int k) {
+    extern __shared__ __align__(128) uint32_t psm[];
+    uint32_t *coltab = psm;                                       // [RB][8]
+    uint8_t *dctab = (uint8_t *)(psm + kPipeRB * 8);              // [RB]
+    uint32_t *ring = psm + kPipeRB * 8 + kPipeRB / 4;             // [warps][D][lines][32]
+    const int tile = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int mb0 = blockIdx.x * kPipeRB;
+    const int nrows = min(kPipeRB, a.M - mb0);
+    const size_t plane = (size_t)tile * a.N * 32;
+    const uint32_t *Lpt = a.Lb[(k - 1) % 3] + plane;
+    uint32_t *Lat = a.Lb[k % 3] + plane;
+    uint32_t *Lnt = a.Lb[(k + 1) % 3] + plane;
+    const int nst = PAIR ? StateIO<FMT>::kWords : 3;
+    uint32_t *stt = a.st + (size_t)tile * nst * a.M * 32;
+    const size_t sstride = (size_t)a.M * 32;
+    // compact row tables of the block -> shared (one 32 B entry per row)
+    for (int i = threadIdx.x; i < nrows * 2; i += blockDim.x) {
+        const uint4 v = __ldg(a.rowtab + 2 * (size_t)mb0 + i);
+        uint4 w = v;
+        if ((i & 1) == 0) {
+            w.x = v.x & 0x0FFFFFFFu;
+            int dc = (int)(v.x >> 28);
+            if (dc == 15) dc = __ldg(a.row_ptr + mb0 + i / 2 + 1) - __ldg(a.row_ptr + mb0 + i / 2);
+            dctab[i / 2] = (uint8_t)dc;
+        }
+        ((uint4 *)coltab)[i] = w;
+    }
+    uint32_t keep = 0;
+    bool frozen = false;
+    if (ES) {
+        const uint32_t d = a.done[tile * 32 + lane];
+        if (PAIR) keep = ((d & 1) ? 0x0000FFFFu : 0u) | ((d & 2) ? 0xFFFF0000u : 0u);
+        else frozen = (d & 1u) != 0;
+    }
+    // accumulator of the next iteration (it held Z^(k-2))
+    if (k < a.K) {
+        const int wg = blockIdx.x * kPipeWarps + warp, nwg = gridDim.x * kPipeWarps;
+        if (!ES || !__any_sync(0xFFFFFFFFu, keep != 0 || frozen)) {
+            stream_init_next(a.Z0 + plane, Lnt, a.N, wg, nwg, lane);
+        } else {
+            for (int n = wg; n < a.N; n += nwg) {
+                const size_t idx = (size_t)n * 32 + lane;
+                if (PAIR) {
+                    uint32_t v = __ldcg(a.Z0 + plane + idx);
+                    if (keep) v = to_vform(sel(keep, from_vform(__ldcg(Lnt + idx)), from_vform(v)));
+                    __stcg(Lnt + idx, v);
+                } else if (!frozen) {
+                    __stcg(Lnt + idx, __ldcg(a.Z0 + plane + idx));
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const bool first_iter = (k == 1);
+    const int nst_copy = first_iter ? 0 : nst;
+    uint32_t *wring = ring + (size_t)warp * kPipeD * kPipeLines * 32;
+    const uint32_t wring_s = (uint32_t)__cvta_generic_to_shared(wring);
+    // rows of this warp: warp, warp + W, ...
+    int nmy = 0;
+    for (int r = warp; r < nrows; r += kPipeWarps) ++nmy;
+    // prologue
+#pragma unroll
+    for (int i = 0; i < kPipeD; ++i) {
+        if (i < nmy) {
+            const int r = warp + i * kPipeWarps;
+            pipe_issue_row(wring_s + (uint32_t)(i * kPipeLines * 128), Lpt, stt, sstride, coltab + r * 8, dctab[r],
+                           nst_copy, mb0 + r, lane);
+        }
+        cp_async_commit();
+    }
+    uint32_t synd = 0;
+    for (int i = 0; i < nmy; ++i) {
+        cp_async_wait<kPipeD - 1>();
+        __syncwarp();
+        const int r = warp + i * kPipeWarps;
+        const int m = mb0 + r;
+        const int slot = i % kPipeD;
+        const uint32_t *sl = wring + slot * kPipeLines * 32;
+        const uint32_t *cols = coltab + r * 8;
+        const int dc = dctab[r];
+        if (PAIR) {
+            switch (dc) {
+            case 2: pipe_row_i<2, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 3: pipe_row_i<3, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 4: pipe_row_i<4, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 5: pipe_row_i<5, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 6: pipe_row_i<6, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 7: pipe_row_i<7, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 8: pipe_row_i<8, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            }
+        } else {
+            switch (dc) {
+            case 2: pipe_row_f<2, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
+            case 3: pipe_row_f<3, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
+            case 4: pipe_row_f<4, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
+            case 5: pipe_row_f<5, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
+            case 6: pipe_row_f<6, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
+            case 7: pipe_row_f<7, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
+            case 8: pipe_row_f<8, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
+            }
+        }
+        __syncwarp();                                          // slot consumed before it is refilled
+        const int inext = i + kPipeD;
+        if (inext < nmy) {
+            const int rn = warp + inext * kPipeWarps;
+            pipe_issue_row(wring_s + (uint32_t)(slot * kPipeLines * 128), Lpt, stt, sstride, coltab + rn * 8,
+                           dctab[rn], nst_copy, mb0 + rn, lane);
+        }
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
+    if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
+}
+
+inline size_t pipe_smem_bytes() {
+    return (size_t)kPipeRB * 8 * 4 + kPipeRB + (size_t)kPipeWarps * kPipeD * kPipeLines * 128 + 64;
+}
+
+}  // namespace ldpc

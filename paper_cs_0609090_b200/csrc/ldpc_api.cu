@@ -18,6 +18,7 @@
 #include "k_resident.cuh"
 #include "k_resident_mp.cuh"
 #include "k_stream.cuh"
+#include "k_stream_pipe.cuh"
 
 using namespace ldpc;
 
@@ -681,7 +682,32 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     }
     if (e != cudaSuccess) return e;
     const unsigned fgrid = (unsigned)((pl.ntiles * 32 + 255) / 256);
-    for (int k = 1; k <= p->max_iter; ++k) {
+    // software-pipelined iteration kernel (cp.async row prefetch) unless LDPC_PIPE=0
+    const char *pipe_env = getenv("LDPC_PIPE");
+    const bool use_pipe = c->max_dc <= 8 && !(pipe_env && pipe_env[0] == '0');
+    const dim3 gp((unsigned)((c->M + kPipeRB - 1) / kPipeRB), (unsigned)pl.ntiles);
+    const size_t psmem = pipe_smem_bytes();
+    for (int k = 1; k <= p->max_iter && use_pipe; ++k) {
+        if (pair) {
+            if (pl.fmt == FMT_C16) {
+                if (es) e = launch([&] { k_stream_pipe<true, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
+                else e = launch([&] { k_stream_pipe<true, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
+            } else {
+                if (es) e = launch([&] { k_stream_pipe<true, FMT_1BIT, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
+                else e = launch([&] { k_stream_pipe<true, FMT_1BIT, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
+            }
+        } else {
+            if (es) e = launch([&] { k_stream_pipe<false, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
+            else e = launch([&] { k_stream_pipe<false, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
+        }
+        if (e != cudaSuccess) return e;
+        if (es) {
+            if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); });
+            else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); });
+            if (e != cudaSuccess) return e;
+        }
+    }
+    for (int k = 1; k <= p->max_iter && !use_pipe; ++k) {
         if (pair) {
             if (pl.fmt == FMT_C16) {
                 if (es) e = launch([&] { k_stream_iter_i<FMT_C16, true><<<gr, 256, 0, s>>>(a, k); });

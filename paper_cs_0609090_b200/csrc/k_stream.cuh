@@ -23,6 +23,48 @@ namespace ldpc {
 __device__ __forceinline__ uint32_t to_vform(uint32_t p) { return p - ((p & 0x8000u) << 1); }
 __device__ __forceinline__ uint32_t from_vform(uint32_t v) { return v + ((v & 0x8000u) << 1); }
 
+// fp32 check row (one frame per lane), branch-free.  Reading D11: one RN rounding
+// per operation (__fsub_rn/__fmul_rn, no FMA).  Two minima with multiplicity:
+// m2 = min(m2, max(m1, x)), m1 = min(m1, x), argmin on strict '<' (lowest position).
+template <int DC>
+__device__ __forceinline__ void f32_row(const float (&L)[DC], bool first_iter, float A0, float B0, uint32_t W0,
+                                        float alpha, float beta, float &A, float &B, uint32_t &Wn, float (&r)[DC]) {
+    float q[DC];
+    if (first_iter) {
+#pragma unroll
+        for (int j = 0; j < DC; ++j) q[j] = L[j];                    // L^(0)_mn = 0
+    } else {
+        const int idx0 = (int)(W0 >> 16);
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {
+            const float mag = (j == idx0) ? B0 : A0;                 // f(A,B,n,ñ)
+            const float lold = ((W0 >> j) & 1u) ? -mag : mag;        // s_mn f(...)
+            q[j] = __fsub_rn(L[j], lold);                            // Z_n' - L_mn'  (D8)
+        }
+    }
+    float m1 = fabsf(q[0]), m2 = __int_as_float(0x7f800000);
+    int i1 = 0;
+    uint32_t sq = q[0] < 0.0f ? 1u : 0u;
+#pragma unroll
+    for (int j = 1; j < DC; ++j) {
+        const float x = fabsf(q[j]);
+        i1 = x < m1 ? j : i1;
+        m2 = fminf(m2, fmaxf(m1, x));
+        m1 = fminf(m1, x);
+        sq |= (q[j] < 0.0f ? 1u : 0u) << j;
+    }
+    const uint32_t par = __popc(sq) & 1u;
+    A = fmaxf(__fsub_rn(__fmul_rn(alpha, m1), beta), 0.0f);
+    B = fmaxf(__fsub_rn(__fmul_rn(alpha, m2), beta), 0.0f);
+    const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;       // s = prod of the others' signs
+    Wn = sg | ((uint32_t)i1 << 16);
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        const float mag = (j == i1) ? B : A;
+        r[j] = ((sg >> j) & 1u) ? -mag : mag;
+    }
+}
+
 struct StreamArgs {
     int N, M, ntiles, nframes, K, Qsat, wpf;
     uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp

@@ -88,48 +88,23 @@ __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *
         for (int j = 0; j < DC; ++j) p ^= L[j] <= 0.0f ? 1u : 0u;
         synd |= p;
     }
-    float q[DC];
-    if (first_iter) {
-#pragma unroll
-        for (int j = 0; j < DC; ++j) q[j] = L[j];
-    } else {
-        const float A0 = __uint_as_float(sl[8 * 32 + lane]), B0 = __uint_as_float(sl[9 * 32 + lane]);
-        const uint32_t W0 = sl[10 * 32 + lane];
-        const int idx0 = (int)(W0 >> 16);
-#pragma unroll
-        for (int j = 0; j < DC; ++j) {
-            const float mag = (j == idx0) ? B0 : A0;                 // f(A,B,n,ñ)
-            const float lold = ((W0 >> j) & 1u) ? -mag : mag;        // s_mn f(...)
-            q[j] = __fsub_rn(L[j], lold);                            // Z_n' - L_mn'  (D11)
-        }
+    float A0 = 0.f, B0 = 0.f;
+    uint32_t W0 = 0;
+    if (!first_iter) {
+        A0 = __uint_as_float(sl[8 * 32 + lane]);
+        B0 = __uint_as_float(sl[9 * 32 + lane]);
+        W0 = sl[10 * 32 + lane];
     }
-    float m1 = fabsf(q[0]), m2 = 0.0f;
-    int i1 = 0;
-    bool have2 = false;
-    uint32_t sq = q[0] < 0.0f ? 1u : 0u;
-#pragma unroll
-    for (int j = 1; j < DC; ++j) {
-        const float x = fabsf(q[j]);
-        sq |= (q[j] < 0.0f ? 1u : 0u) << j;
-        if (x < m1) { m2 = m1; have2 = true; m1 = x; i1 = j; }
-        else if (!have2 || x < m2) { m2 = x; have2 = true; }
-    }
-    const uint32_t par = __popc(sq) & 1u;
-    float A = __fsub_rn(__fmul_rn(a.alpha, m1), a.beta);
-    A = A < 0.0f ? 0.0f : A;
-    float B = __fsub_rn(__fmul_rn(a.alpha, m2), a.beta);
-    B = B < 0.0f ? 0.0f : B;
-    const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;
+    float A, B, r[DC];
+    uint32_t Wn;
+    f32_row<DC>(L, first_iter, A0, B0, W0, a.alpha, a.beta, A, B, Wn, r);
     const size_t so = (size_t)m * 32 + lane;
     __stcg(stt + so, __float_as_uint(A));
     __stcg(stt + ss + so, __float_as_uint(B));
-    __stcg(stt + 2 * ss + so, sg | ((uint32_t)i1 << 16));
+    __stcg(stt + 2 * ss + so, Wn);
     if (!frozen) {
 #pragma unroll
-        for (int j = 0; j < DC; ++j) {
-            const float mag = (j == i1) ? B : A;
-            atomicAdd(Lat + (size_t)cols[j] * 32 + lane, ((sg >> j) & 1u) ? -mag : mag);
-        }
+        for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, r[j]);   // Z^(k)_n += L^(k)_mn
     }
 }
 

@@ -29,16 +29,23 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // (variable col[l] of this tile), lines 8..8+nst-1 the state words of row m.
 __device__ __forceinline__ void pipe_issue_row(uint32_t slot, const uint32_t *Lpt, const uint32_t *stt, size_t sstride,
                                                const uint32_t *cols, int dc, int nst, int m, int lane) {
-    const int nl = 8 + nst;
-    const int chunk = lane & 7;
-    for (int l0 = 0; l0 < nl; l0 += 4) {
-        const int l = l0 + (lane >> 3);
-        if (l < nl) {
-            const uint32_t *src = nullptr;
-            if (l < dc) src = Lpt + (size_t)cols[l] * 32;
-            else if (l >= 8) src = stt + (size_t)(l - 8) * sstride + (size_t)m * 32;
-            if (src) cp_async16(slot + (uint32_t)(l * 128 + chunk * 16), (const char *)src + chunk * 16);
+    // lane handles 16-byte chunk (lane & 7) of lines (lane >> 3) + {0, 4, 8}; branch-free
+    // source selection, predicated copies (lines 0..dc-1 posterior, 8.. state).
+    const int chunk = lane & 7, l0 = lane >> 3;
+    const char *sbase = (const char *)(stt + (size_t)m * 32) + chunk * 16;
+#pragma unroll
+    for (int step = 0; step < 3; ++step) {
+        const int l = l0 + 4 * step;
+        const char *src;
+        bool on;
+        if (step < 2) {                                  // lines 0..7: posterior lines
+            on = l < dc;
+            src = (const char *)(Lpt + (size_t)cols[l] * 32) + chunk * 16;
+        } else {                                         // lines 8..10: state words
+            on = l - 8 < nst;
+            src = sbase + (size_t)(l - 8) * sstride * 4;
         }
+        if (on) cp_async16(slot + (uint32_t)(l * 128 + chunk * 16), src);
     }
 }
 

@@ -12,7 +12,7 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/bench_
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_cfg2.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "launches rc=$?"
 for c in 2 4 5; do
-  K=k_resident; [ $c -ge 4 ] && K=k_stream_iter
+  K=k_resident; [ $c -ge 4 ] && K=k_stream_pipe
   timeout 300 python tools/prof_decode.py --config $c --reps 2 > $OUT/prof_plain_cfg$c.log 2>&1 && \
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K -s 1 -c 1 -o $OUT/prof_cfg$c \
     python tools/prof_decode.py --config $c --reps 2 > $OUT/ncu_cfg$c.log 2>&1; echo "ncu cfg$c rc=$?"

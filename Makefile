@@ -6,13 +6,18 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 LIB := paper_cs_0609090_b200/libldpc.so
-SRCS := paper_cs_0609090_b200/csrc/ldpc_api.cu
-HDRS := $(wildcard paper_cs_0609090_b200/csrc/*.cuh) include/ldpc.h
+CSRC := paper_cs_0609090_b200/csrc
+SRCS := $(wildcard $(CSRC)/*.cu)
+OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
+HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/ldpc.h
 
 all: $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so
 
-$(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -lcudart 2> build/ptxas.log || (cat build/ptxas.log; false)
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
 oracle/liboracle.so: oracle/oracle.c oracle/engine.inc
 	gcc -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -o $@ oracle/oracle.c -lpthread
@@ -21,7 +26,7 @@ ldpcgen/libldpcgen.so: ldpcgen/ldpcgen.c
 	gcc -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -o $@ ldpcgen/ldpcgen.c -lm -lpthread
 
 clean:
-	rm -f $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so
+	rm -f build/*.o $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so
 
 .PHONY: all clean
 $(shell mkdir -p build)

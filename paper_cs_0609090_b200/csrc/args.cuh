@@ -1,0 +1,74 @@
+// args.cuh -- kernel argument blocks shared by the host planner (ldpc_api.cu) and the
+// kernel translation units (res_launch.cu, stream_launch.cu).  Plain data only.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "simd16.cuh"
+
+namespace ldpc {
+
+constexpr int kMaxDC = 8;
+constexpr int kQcMaxSB = 128;
+constexpr int kQcGroups = 2;
+constexpr int kQcMaxEnt = 1536;
+
+// QC circulant table, passed by value (kernel parameter = constant bank).
+struct QcTab {
+    int nsb;                            // super-batches per iteration
+    uint32_t Z4;                        // 4 * Z (bytes)
+    int32_t e0[kQcMaxSB][kQcGroups];    // first entry of the base row handled by group g
+    int32_t dc[kQcMaxSB][kQcGroups];    // its degree (0 = group idle in this super-batch)
+    int32_t run_end[kQcMaxSB][kQcGroups];  // first later super-batch where the group's degree changes
+    uint2 ent[kQcMaxEnt];               // (4 * shift, 4 * (j * Z)) per base-matrix entry
+};
+
+struct ResArgs {
+    int N, Np, M, npairs, nframes, K, Qsat, wpf;   // Np = N rounded up to 4; wpf = ceil(N/32)
+    uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp
+    const void *llr;
+    uint32_t *hard_bits;
+    int16_t *post;
+    uint8_t *ok;
+    int32_t *iters;
+    uint32_t *ws;
+    size_t slot_words;
+    int nbatch;                       // CSR: colour batches (QC: unused, see QcTab::nsb)
+    const int32_t *bptr;              // CSR: batch b = schedule positions [bptr[b], bptr[b+1])
+    const uint32_t *colT;             // CSR: [kMaxDC][M] byte offsets 4*n of each edge
+    const uint8_t *dcT;               // CSR: degree per schedule position
+    int Z;                            // QC circulant size
+    int group_threads;                // QC: threads per group (128 with two groups)
+    uint32_t tmem_cols;               // TMEM columns allocated per CTA
+    int cols_per_group;               // TMEM columns used by one group of threads
+    RegK rk;                          // register constants (simd16.cuh)
+};
+
+struct StreamArgs {
+    RegK rk;                     // register constants (simd16.cuh)
+    int N, M, ntiles, nframes, K, Qsat, wpf;
+    uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp
+    float alpha, beta;           // fp32 variant: |L| <= max(alpha*min - beta, 0)
+    const int32_t *row_ptr, *col_idx;
+    const uint4 *rowtab;         // [M][2]: up to 8 column indices per row; dc in bits 28-31 of word 0 (15 = wider row)
+    const void *llr;
+    uint32_t *Z0;                // [tile][N][32]
+    uint32_t *Lb[3];             // rotating posterior buffers [tile][N][32]
+    uint32_t *st;                // [tile][words][M][32]
+    uint32_t *synd;              // [tile][32]: syndrome-fail bits found during the current launch
+    uint32_t *done;              // [tile][32]: frames frozen (early stop)
+    int32_t *it_ws;              // [tile*TILE] iterations used per frame
+    uint8_t *ok_ws;              // [tile*TILE] syndrome ok per frame (frozen frames)
+    uint32_t *hard_bits;
+    void *post;
+    uint8_t *ok;
+    int32_t *iters;
+};
+
+// persistent state formats (workspace words per row-pair)
+// FMT_C16 : 3 words (A, B, W); magnitudes up to 2Q = 1022.
+// FMT_1BIT: 2 words (X = bytes [A_lo, B_lo, A_hi, B_hi], W); magnitudes up to 2Q = 254.
+enum { FMT_C16 = 0, FMT_1BIT = 1 };
+
+}  // namespace ldpc

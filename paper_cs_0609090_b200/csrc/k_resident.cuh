@@ -22,46 +22,11 @@
 // codes: the host builds batches by greedy row colouring and per-edge byte
 // offsets come from a [DC][M] table.
 #pragma once
+#include "args.cuh"
 #include "rowcore.cuh"
 #include "tmem.cuh"
 
 namespace ldpc {
-
-constexpr int kMaxDC = 8;
-constexpr int kQcMaxSB = 128;
-constexpr int kQcGroups = 2;
-constexpr int kQcMaxEnt = 1536;
-
-// QC circulant table, passed by value (kernel parameter = constant bank).
-struct QcTab {
-    int nsb;                            // super-batches per iteration
-    uint32_t Z4;                        // 4 * Z (bytes)
-    int32_t e0[kQcMaxSB][kQcGroups];    // first entry of the base row handled by group g
-    int32_t dc[kQcMaxSB][kQcGroups];    // its degree (0 = group idle in this super-batch)
-    int32_t run_end[kQcMaxSB][kQcGroups];  // first later super-batch where the group's degree changes
-    uint2 ent[kQcMaxEnt];               // (4 * shift, 4 * (j * Z)) per base-matrix entry
-};
-
-struct ResArgs {
-    int N, Np, M, npairs, nframes, K, Qsat, wpf;   // Np = N rounded up to 4; wpf = ceil(N/32)
-    uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp
-    const void *llr;
-    uint32_t *hard_bits;
-    int16_t *post;
-    uint8_t *ok;
-    int32_t *iters;
-    uint32_t *ws;
-    size_t slot_words;
-    int nbatch;                       // CSR: colour batches (QC: unused, see QcTab::nsb)
-    const int32_t *bptr;              // CSR: batch b = schedule positions [bptr[b], bptr[b+1])
-    const uint32_t *colT;             // CSR: [kMaxDC][M] byte offsets 4*n of each edge
-    const uint8_t *dcT;               // CSR: degree per schedule position
-    int Z;                            // QC circulant size
-    int group_threads;                // QC: threads per group (128 with two groups)
-    uint32_t tmem_cols;               // TMEM columns allocated per CTA
-    int cols_per_group;               // TMEM columns used by one group of threads
-    uint32_t zero;                    // 0, kept in a register (operand of VIADDMNMX)
-};
 
 template <typename TIN>
 __device__ __forceinline__ int load_llr_sat(const TIN *p, int Q) {
@@ -120,16 +85,16 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
     uint32_t L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(op[j]));
-    if (ES) synd |= row_parity<DC>(L);
+    if (ES) synd |= row_parity<DC>(L, a.rk);
     uint32_t q[DC];
     if (first_iter) {
 #pragma unroll
         for (int j = 0; j < DC; ++j) q[j] = L[j];            // L^(0)_mn = 0
     } else {
-        rebuild_q<DC>(L, st, q);
+        rebuild_q<DC>(L, st, q, a.rk);
     }
     uint32_t rn[DC];
-    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.zero);
+    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.rk);
 #pragma unroll
     for (int j = 0; j < DC; ++j) {                           // Z^(k)_n += L^(k)_mn
         uint32_t v;
@@ -169,7 +134,7 @@ __device__ __forceinline__ uint32_t res_parity(const ResArgs &a, const QcTab &t,
         }
         L[j] = *(const uint32_t *)(Lpb + off);
     }
-    return row_parity<DC>(L);
+    return row_parity<DC>(L, a.rk);
 }
 
 template <bool QC>

@@ -16,6 +16,7 @@
 // integer RED adds both 16-bit lanes exactly; gathers convert back to the
 // packed per-half form.  fp32 path: one frame per lane, RED.F32.
 #pragma once
+#include "args.cuh"
 #include "rowcore.cuh"
 
 namespace ldpc {
@@ -64,26 +65,6 @@ __device__ __forceinline__ void f32_row(const float (&L)[DC], bool first_iter, f
         r[j] = ((sg >> j) & 1u) ? -mag : mag;
     }
 }
-
-struct StreamArgs {
-    int N, M, ntiles, nframes, K, Qsat, wpf;
-    uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp
-    float alpha, beta;           // fp32 variant: |L| <= max(alpha*min - beta, 0)
-    const int32_t *row_ptr, *col_idx;
-    const uint4 *rowtab;         // [M][2]: up to 8 column indices per row; dc in bits 28-31 of word 0 (15 = wider row)
-    const void *llr;
-    uint32_t *Z0;                // [tile][N][32]
-    uint32_t *Lb[3];             // rotating posterior buffers [tile][N][32]
-    uint32_t *st;                // [tile][words][M][32]
-    uint32_t *synd;              // [tile][32]: syndrome-fail bits found during the current launch
-    uint32_t *done;              // [tile][32]: frames frozen (early stop)
-    int32_t *it_ws;              // [tile*TILE] iterations used per frame
-    uint8_t *ok_ws;              // [tile*TILE] syndrome ok per frame (frozen frames)
-    uint32_t *hard_bits;
-    void *post;
-    uint8_t *ok;
-    int32_t *iters;
-};
 
 // -------------------------------------------------------------- integer path
 // ingest: user [F][N] -> Z0 (V form, doubled, saturated) and Lb[0] (packed form
@@ -166,16 +147,16 @@ __device__ __forceinline__ void stream_rows_i(const StreamArgs &a, int lane, con
         for (int j = 0; j < DC; ++j) L[r][j] = from_vform(__ldcg(Lpt + off[r][j]));
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-        if (ES) synd |= row_parity<DC>(L[r]);
+        if (ES) synd |= row_parity<DC>(L[r], a.rk);
         uint32_t q[DC];
         if (first_iter) {
 #pragma unroll
             for (int j = 0; j < DC; ++j) q[j] = L[r][j];
         } else {
-            rebuild_q<DC>(L[r], st[r], q);
+            rebuild_q<DC>(L[r], st[r], q, a.rk);
         }
         uint32_t rn[DC];
-        new_state<DC>(q, a.nbeta2p1, a.q2p1, st[r], rn);
+        new_state<DC>(q, a.nbeta2p1, a.q2p1, st[r], rn, a.rk);
         StateIO<FMT>::store(stt + lane, sstride, (size_t)m[r] * 32, st[r]);
 #pragma unroll
         for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], to_vform(rn[j] & ~keep));
@@ -567,35 +548,6 @@ __global__ void __launch_bounds__(256, 4) k_stream_iter_f(const StreamArgs a, in
         stream_dispatch_f<1, ES>(dc, a, lane, mm, &rt, Lpt, Lat, stt, first_iter, frozen, synd);
     }
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
-}
-
-// -------------------------------------------------------------- error counters
-__global__ void k_count_errors(int64_t nframes, int wpf, const uint32_t *hb, const uint8_t *ok, const int32_t *it,
-                               unsigned long long *cnt) {
-    unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nframes; f += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long be = 0;
-        for (int w = 0; w < wpf; ++w) be += __popc(hb[f * wpf + w]);
-        c0 += be;
-        c1 += be ? 1 : 0;
-        c2 += (be && ok[f]) ? 1 : 0;
-        c3 += ok[f] ? 0 : 1;
-        c4 += it ? (unsigned long long)it[f] : 0ull;
-    }
-    for (int o = 16; o; o >>= 1) {
-        c0 += __shfl_xor_sync(0xFFFFFFFFu, c0, o);
-        c1 += __shfl_xor_sync(0xFFFFFFFFu, c1, o);
-        c2 += __shfl_xor_sync(0xFFFFFFFFu, c2, o);
-        c3 += __shfl_xor_sync(0xFFFFFFFFu, c3, o);
-        c4 += __shfl_xor_sync(0xFFFFFFFFu, c4, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (c0) atomicAdd(cnt + 0, c0);
-        if (c1) atomicAdd(cnt + 1, c1);
-        if (c2) atomicAdd(cnt + 2, c2);
-        if (c3) atomicAdd(cnt + 3, c3);
-        if (c4) atomicAdd(cnt + 4, c4);
-    }
 }
 
 }  // namespace ldpc

@@ -56,7 +56,7 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
     uint32_t L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) L[j] = from_vform(sl[j * 32 + lane]);
-    if (ES) synd |= row_parity<DC>(L);
+    if (ES) synd |= row_parity<DC>(L, a.rk);
     RowState st;
     uint32_t q[DC];
     if (first_iter) {
@@ -73,10 +73,10 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
             st.B = prmt(X, 0u, 0x4341u);
             st.W = sl[9 * 32 + lane];
         }
-        rebuild_q<DC>(L, st, q);
+        rebuild_q<DC>(L, st, q, a.rk);
     }
     uint32_t rn[DC];
-    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn);
+    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.rk);
     StateIO<FMT>::store(stt + lane, sstride, (size_t)m * 32, st);
 #pragma unroll
     for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, to_vform(rn[j] & ~keep));

@@ -1,0 +1,29 @@
+// launch.h -- host entry points of the kernel translation units (res_launch.cu,
+// stream_launch.cu), called by the planner in ldpc_api.cu.  Split so the kernel
+// instantiations compile in parallel.
+#pragma once
+#include "args.cuh"
+
+namespace ldpc {
+
+// Resident kernel (k_resident.cuh).  i8 selects int8 channel LLRs (else int16).
+cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, size_t dyn_smem, size_t smem_per_sm, int threads,
+                          int *blocks);
+cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, int grid, int threads, size_t dyn_smem, const ResArgs &a,
+                       const QcTab &t, cudaStream_t s);
+
+// Streaming kernels (k_stream.cuh, k_stream_pipe.cuh): every launch of one decode.
+struct StreamRun {
+    bool pair;            // integer path (two frames per 16x2 lane) vs fp32
+    bool i8;              // int8 channel LLRs (integer path)
+    int fmt;              // FMT_C16 / FMT_1BIT
+    bool es;              // per-frame early stop
+    int max_iter, max_dc, ntiles;
+    size_t flags_bytes;   // bytes from a.synd to the end of the per-tile flag words (zeroed first)
+};
+cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, int32_t *launches);
+
+cudaError_t count_errors_launch(int64_t nframes, int wpf, const uint32_t *hb, const uint8_t *ok, const int32_t *it,
+                                unsigned long long *cnt, cudaStream_t s);
+
+}  // namespace ldpc

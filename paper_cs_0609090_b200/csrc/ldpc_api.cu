@@ -15,10 +15,8 @@
 #include <vector>
 
 #include "../../include/ldpc.h"
-#include "k_resident.cuh"
-#include "k_resident_mp.cuh"
-#include "k_stream.cuh"
-#include "k_stream_pipe.cuh"
+#include "launch.h"
+#include "simd16.cuh"
 
 using namespace ldpc;
 
@@ -389,50 +387,15 @@ struct Plan {
     size_t slot_words = 0;
     uint32_t tmem_cols = 0;
     int cols_per_group = 0;
-    int np = 1;                  // frame pairs per CTA (multi-pair QC kernel when > 1)
     // stream
     int tile = 64, ntiles = 0;
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
     size_t ws_bytes = 0;
 };
 
-template <bool QC, bool ES, int FMT, typename TIN>
-cudaError_t res_occupancy(const ldpc_code *c, int *blocks) {
-    // The occupancy API reports 1 block/SM for kernels that allocate TMEM; compute the
-    // limit from the kernel's registers, shared memory and threads instead (TMEM is
-    // accounted for by the caller).
-    auto kern = k_resident<QC, ES, FMT, TIN>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem);
-    if (e != cudaSuccess) return e;
-    cudaFuncAttributes fa;
-    if ((e = cudaFuncGetAttributes(&fa, kern)) != cudaSuccess) return e;
-    const size_t per_block_smem = c->res_smem + fa.sharedSizeBytes + 1024;   // + driver reserve
-    int by_smem = (int)(c->smem_per_sm / per_block_smem);
-    int regs = ((fa.numRegs + 7) / 8) * 8 * c->res_threads;
-    int by_regs = regs > 0 ? 65536 / regs : 32;
-    int by_threads = 2048 / c->res_threads;
-    *blocks = std::max(0, std::min(std::min(by_smem, by_regs), std::min(by_threads, 32)));
-    return cudaSuccess;
-}
-
-template <bool QC, bool ES, int FMT>
-cudaError_t res_occupancy_t(const ldpc_code *c, int llr_type, int *blocks) {
-    return llr_type == LDPC_LLR_I8 ? res_occupancy<QC, ES, FMT, int8_t>(c, blocks)
-                                   : res_occupancy<QC, ES, FMT, int16_t>(c, blocks);
-}
-
 cudaError_t res_occupancy_any(const ldpc_code *c, const ldpc_decode_params *p, int fmt, int *blocks) {
-    const bool es = p->early_stop != 0;
-    if (c->qc) {
-        if (es) return fmt == FMT_C16 ? res_occupancy_t<true, true, FMT_C16>(c, p->llr_type, blocks)
-                                      : res_occupancy_t<true, true, FMT_1BIT>(c, p->llr_type, blocks);
-        return fmt == FMT_C16 ? res_occupancy_t<true, false, FMT_C16>(c, p->llr_type, blocks)
-                              : res_occupancy_t<true, false, FMT_1BIT>(c, p->llr_type, blocks);
-    }
-    if (es) return fmt == FMT_C16 ? res_occupancy_t<false, true, FMT_C16>(c, p->llr_type, blocks)
-                                  : res_occupancy_t<false, true, FMT_1BIT>(c, p->llr_type, blocks);
-    return fmt == FMT_C16 ? res_occupancy_t<false, false, FMT_C16>(c, p->llr_type, blocks)
-                          : res_occupancy_t<false, false, FMT_1BIT>(c, p->llr_type, blocks);
+    return res_occupancy(c->qc, p->early_stop != 0, fmt, p->llr_type == LDPC_LLR_I8, c->res_smem, c->smem_per_sm,
+                         c->res_threads, blocks);
 }
 
 ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p, Plan &pl) {
@@ -485,28 +448,6 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (pl.path == PATH_RESIDENT) {
         // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group
         pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * c->nbatch;
-        // multi-pair QC kernel: NP pairs per CTA, one CTA per SM.  Opt-in (LDPC_MP=1): it
-        // measured slower than one pair per CTA at 3 CTAs/SM on cfg2/cfg3.
-        const char *mpenv = getenv("LDPC_MP");
-        if (c->qc && mpenv && mpenv[0] == '1') {
-            const int groups = (c->res_threads + 127) / 128;
-            int np = (int)std::min<size_t>(3, c->smem_optin / (c->res_smem + 64));
-            while (np > 1 && (uint32_t)(groups * np * pl.cols_per_group) > 512) --np;
-            if (np >= 2) {
-                pl.np = np;
-                uint32_t need = (uint32_t)(groups * np * pl.cols_per_group), cols = 32;
-                while (cols < need) cols <<= 1;
-                pl.tmem_cols = cols;
-                const int64_t ngroups = (npairs + np - 1) / np;
-                pl.grid = (int)std::min<int64_t>(std::max<int64_t>(ngroups, 1), (int64_t)c->sm_count);
-                pl.slot_words = ((size_t)c->N + 63) & ~(size_t)63;
-                pl.ws_bytes = align256((size_t)pl.grid * np * pl.slot_words * 4);
-                if (getenv("LDPC_DEBUG"))
-                    fprintf(stderr, "[ldpc] resident-mp: np=%d threads=%d smem=%zu tmem_cols=%u grid=%d batches=%d\n", np,
-                            c->res_threads, (size_t)np * c->res_smem, cols, pl.grid, c->nbatch);
-                return LDPC_OK;
-            }
-        }
         const int groups = (c->res_threads + 127) / 128;   // 128-thread TMEM lane slices
         uint32_t need = (uint32_t)(pl.cols_per_group * groups), cols = 32;
         while (cols < need) cols <<= 1;
@@ -541,47 +482,6 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     return LDPC_OK;
 }
 
-template <bool QC, bool ES, int FMT, typename TIN>
-cudaError_t launch_res(const ldpc_code *c, const Plan &pl, const ResArgs &a, cudaStream_t s) {
-    auto kern = k_resident<QC, ES, FMT, TIN>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->res_smem);
-    if (e != cudaSuccess) return e;
-    static const QcTab empty_tab{};
-    kern<<<pl.grid, c->res_threads, c->res_smem, s>>>(a, c->qtab ? *c->qtab : empty_tab);
-    ++g_launches;
-    return cudaGetLastError();
-}
-
-template <bool QC, bool ES, int FMT>
-cudaError_t launch_res_t(const ldpc_code *c, const Plan &pl, const ResArgs &a, int llr_type, cudaStream_t s) {
-    return llr_type == LDPC_LLR_I8 ? launch_res<QC, ES, FMT, int8_t>(c, pl, a, s)
-                                   : launch_res<QC, ES, FMT, int16_t>(c, pl, a, s);
-}
-
-template <int NP, bool ES, int FMT, typename TIN>
-cudaError_t launch_mp(const ldpc_code *c, const Plan &pl, const ResArgs &a, cudaStream_t s) {
-    auto kern = k_resident_mp<NP, ES, FMT, TIN>;
-    const size_t smem = (size_t)NP * c->res_smem;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<pl.grid, c->res_threads, smem, s>>>(a, *c->qtab);
-    ++g_launches;
-    return cudaGetLastError();
-}
-
-template <int NP, bool ES, int FMT>
-cudaError_t launch_mp_t(const ldpc_code *c, const Plan &pl, const ResArgs &a, int llr_type, cudaStream_t s) {
-    return llr_type == LDPC_LLR_I8 ? launch_mp<NP, ES, FMT, int8_t>(c, pl, a, s) : launch_mp<NP, ES, FMT, int16_t>(c, pl, a, s);
-}
-
-template <int NP>
-cudaError_t launch_mp_any(const ldpc_code *c, const Plan &pl, const ResArgs &a, bool es, int llr_type, cudaStream_t s) {
-    if (es) return pl.fmt == FMT_C16 ? launch_mp_t<NP, true, FMT_C16>(c, pl, a, llr_type, s)
-                                     : launch_mp_t<NP, true, FMT_1BIT>(c, pl, a, llr_type, s);
-    return pl.fmt == FMT_C16 ? launch_mp_t<NP, false, FMT_C16>(c, pl, a, llr_type, s)
-                             : launch_mp_t<NP, false, FMT_1BIT>(c, pl, a, llr_type, s);
-}
-
 cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_params *p, int64_t F,
                          const void *llr, uint32_t *hb, void *post, uint8_t *ok, int32_t *it, void *ws,
                          cudaStream_t s) {
@@ -611,27 +511,12 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.group_threads = c->group_threads;
     a.tmem_cols = pl.tmem_cols;
     a.cols_per_group = pl.cols_per_group;
-    const bool es = p->early_stop != 0;
-    const int t = p->llr_type;
-    if (pl.np == 3) return launch_mp_any<3>(c, pl, a, es, t, s);
-    if (pl.np == 2) return launch_mp_any<2>(c, pl, a, es, t, s);
-    if (c->qc) {
-        if (es) return pl.fmt == FMT_C16 ? launch_res_t<true, true, FMT_C16>(c, pl, a, t, s)
-                                         : launch_res_t<true, true, FMT_1BIT>(c, pl, a, t, s);
-        return pl.fmt == FMT_C16 ? launch_res_t<true, false, FMT_C16>(c, pl, a, t, s)
-                                 : launch_res_t<true, false, FMT_1BIT>(c, pl, a, t, s);
-    }
-    if (es) return pl.fmt == FMT_C16 ? launch_res_t<false, true, FMT_C16>(c, pl, a, t, s)
-                                     : launch_res_t<false, true, FMT_1BIT>(c, pl, a, t, s);
-    return pl.fmt == FMT_C16 ? launch_res_t<false, false, FMT_C16>(c, pl, a, t, s)
-                             : launch_res_t<false, false, FMT_1BIT>(c, pl, a, t, s);
-}
-
-template <typename F>
-cudaError_t launch(F f) {
-    f();
+    a.rk = make_regk();
+    static const QcTab empty_tab{};
+    cudaError_t e = res_launch(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.grid, c->res_threads,
+                               c->res_smem, a, c->qtab ? *c->qtab : empty_tab, s);
     ++g_launches;
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_params *p, int64_t F, const void *llr,
@@ -648,6 +533,7 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     a.nbeta2p1 = pack2(1 - 2 * pl.beta, 1 - 2 * pl.beta);
     a.q2p1 = pack2(2 * pl.Q + 1, 2 * pl.Q + 1);
     a.alpha = pl.alpha;
+    a.rk = make_regk();
     a.beta = pl.betaf;
     a.row_ptr = c->d_row_ptr;
     a.col_idx = c->d_col_idx;
@@ -664,79 +550,18 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     a.post = post;
     a.ok = ok;
     a.iters = it;
-    cudaError_t e;
-    // synd, done (contiguous) and per-frame flags
-    if ((e = cudaMemsetAsync(a.synd, 0, pl.off_it - pl.off_synd, s)) != cudaSuccess) return e;
-    const bool es = p->early_stop != 0;
-    const bool pair = pl.path == PATH_STREAM_I;
-    const int nwarps_per_block = 8;
-    dim3 gi((unsigned)std::min<int64_t>(((int64_t)c->N + 7) / 8, 1024), (unsigned)pl.ntiles);
-    // ~8 rows per warp per launch
-    const int rows_per_block = nwarps_per_block * 8;
-    dim3 gr((unsigned)std::max(1, (c->M + rows_per_block - 1) / rows_per_block), (unsigned)pl.ntiles);
-    if (pair) {
-        if (p->llr_type == LDPC_LLR_I8) e = launch([&] { k_stream_ingest_i<int8_t><<<gi, 256, 0, s>>>(a); });
-        else e = launch([&] { k_stream_ingest_i<int16_t><<<gi, 256, 0, s>>>(a); });
-    } else {
-        e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); });
-    }
-    if (e != cudaSuccess) return e;
-    const unsigned fgrid = (unsigned)((pl.ntiles * 32 + 255) / 256);
-    // software-pipelined iteration kernel (cp.async row prefetch) unless LDPC_PIPE=0
-    const char *pipe_env = getenv("LDPC_PIPE");
-    const bool use_pipe = c->max_dc <= 8 && !(pipe_env && pipe_env[0] == '0');
-    const dim3 gp((unsigned)((c->M + kPipeRB - 1) / kPipeRB), (unsigned)pl.ntiles);
-    const size_t psmem = pipe_smem_bytes();
-    for (int k = 1; k <= p->max_iter && use_pipe; ++k) {
-        if (pair) {
-            if (pl.fmt == FMT_C16) {
-                if (es) e = launch([&] { k_stream_pipe<true, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
-                else e = launch([&] { k_stream_pipe<true, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
-            } else {
-                if (es) e = launch([&] { k_stream_pipe<true, FMT_1BIT, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
-                else e = launch([&] { k_stream_pipe<true, FMT_1BIT, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
-            }
-        } else {
-            if (es) e = launch([&] { k_stream_pipe<false, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
-            else e = launch([&] { k_stream_pipe<false, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); });
-        }
-        if (e != cudaSuccess) return e;
-        if (es) {
-            if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); });
-            else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); });
-            if (e != cudaSuccess) return e;
-        }
-    }
-    for (int k = 1; k <= p->max_iter && !use_pipe; ++k) {
-        if (pair) {
-            if (pl.fmt == FMT_C16) {
-                if (es) e = launch([&] { k_stream_iter_i<FMT_C16, true><<<gr, 256, 0, s>>>(a, k); });
-                else e = launch([&] { k_stream_iter_i<FMT_C16, false><<<gr, 256, 0, s>>>(a, k); });
-            } else {
-                if (es) e = launch([&] { k_stream_iter_i<FMT_1BIT, true><<<gr, 256, 0, s>>>(a, k); });
-                else e = launch([&] { k_stream_iter_i<FMT_1BIT, false><<<gr, 256, 0, s>>>(a, k); });
-            }
-        } else {
-            if (es) e = launch([&] { k_stream_iter_f<true><<<gr, 256, 0, s>>>(a, k); });
-            else e = launch([&] { k_stream_iter_f<false><<<gr, 256, 0, s>>>(a, k); });
-        }
-        if (e != cudaSuccess) return e;
-        if (es) {
-            if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); });
-            else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); });
-            if (e != cudaSuccess) return e;
-        }
-    }
-    const int kb = p->max_iter % 3;
-    if (pair) e = launch([&] { k_stream_syndrome<true><<<gr, 256, 0, s>>>(a, kb); });
-    else e = launch([&] { k_stream_syndrome<false><<<gr, 256, 0, s>>>(a, kb); });
-    if (e != cudaSuccess) return e;
-    if (pair) e = launch([&] { k_stream_finalize_flags<true><<<fgrid, 256, 0, s>>>(a); });
-    else e = launch([&] { k_stream_finalize_flags<false><<<fgrid, 256, 0, s>>>(a); });
-    if (e != cudaSuccess) return e;
-    dim3 go((unsigned)a.wpf, (unsigned)pl.ntiles);
-    if (pair) e = launch([&] { k_stream_output<true><<<go, 256, 0, s>>>(a); });
-    else e = launch([&] { k_stream_output<false><<<go, 256, 0, s>>>(a); });
+    StreamRun r{};
+    r.pair = pl.path == PATH_STREAM_I;
+    r.i8 = p->llr_type == LDPC_LLR_I8;
+    r.fmt = pl.fmt;
+    r.es = p->early_stop != 0;
+    r.max_iter = p->max_iter;
+    r.max_dc = c->max_dc;
+    r.ntiles = pl.ntiles;
+    r.flags_bytes = pl.off_it - pl.off_synd;
+    int32_t n = 0;
+    cudaError_t e = stream_run(a, r, s, &n);
+    g_launches += n;
     return e;
 }
 
@@ -897,10 +722,8 @@ extern "C" ldpc_status ldpc_count_errors(const ldpc_code *code, int64_t n_frames
     if (n_frames == 0) return LDPC_OK;
     DeviceGuard guard(code->device);
     const int wpf = (code->N + 31) / 32;
-    const unsigned blocks = (unsigned)std::min<int64_t>((n_frames + 255) / 256, 4096);
-    k_count_errors<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_frames, wpf, hard_bits, syndrome_ok, iterations_used,
-                                                             (unsigned long long *)counters);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = count_errors_launch(n_frames, wpf, hard_bits, syndrome_ok, iterations_used,
+                                        (unsigned long long *)counters, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "count kernel: %s", cudaGetErrorString(e));
     return LDPC_OK;
 }

@@ -1,0 +1,75 @@
+// res_launch.cu -- instantiations and launches of the decode-resident kernel.
+#include <algorithm>
+
+#include "k_resident.cuh"
+#include "launch.h"
+
+namespace ldpc {
+namespace {
+
+template <bool QC, bool ES, int FMT, typename TIN>
+cudaError_t occ(size_t dyn_smem, size_t smem_per_sm, int threads, int *blocks) {
+    // The occupancy API reports 1 block/SM for kernels that allocate TMEM; compute the
+    // limit from the kernel's registers, shared memory and threads instead (TMEM is
+    // accounted for by the caller).
+    auto kern = k_resident<QC, ES, FMT, TIN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, kern)) != cudaSuccess) return e;
+    const size_t per_block_smem = dyn_smem + fa.sharedSizeBytes + 1024;   // + driver reserve
+    const int by_smem = (int)(smem_per_sm / per_block_smem);
+    const int regs = ((fa.numRegs + 7) / 8) * 8 * threads;
+    const int by_regs = regs > 0 ? 65536 / regs : 32;
+    const int by_threads = 2048 / threads;
+    *blocks = std::max(0, std::min(std::min(by_smem, by_regs), std::min(by_threads, 32)));
+    return cudaSuccess;
+}
+
+template <bool QC, bool ES, int FMT, typename TIN>
+cudaError_t launch(int grid, int threads, size_t dyn_smem, const ResArgs &a, const QcTab &t, cudaStream_t s) {
+    auto kern = k_resident<QC, ES, FMT, TIN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, threads, dyn_smem, s>>>(a, t);
+    return cudaGetLastError();
+}
+
+// dispatch over the template parameters; F is called with a pointer-to-instantiation tag
+template <template <bool, bool, int, typename> class K, typename... Args>
+cudaError_t dispatch(bool qc, bool es, int fmt, bool i8, Args... args) {
+#define LDPC_RES_CASE(Q, E, F)                                                              \
+    if (qc == Q && es == E && fmt == F)                                                     \
+        return i8 ? K<Q, E, F, int8_t>::run(args...) : K<Q, E, F, int16_t>::run(args...);
+    LDPC_RES_CASE(true, true, FMT_C16) LDPC_RES_CASE(true, true, FMT_1BIT)
+    LDPC_RES_CASE(true, false, FMT_C16) LDPC_RES_CASE(true, false, FMT_1BIT)
+    LDPC_RES_CASE(false, true, FMT_C16) LDPC_RES_CASE(false, true, FMT_1BIT)
+    LDPC_RES_CASE(false, false, FMT_C16) LDPC_RES_CASE(false, false, FMT_1BIT)
+#undef LDPC_RES_CASE
+    return cudaErrorInvalidValue;
+}
+
+template <bool QC, bool ES, int FMT, typename TIN>
+struct Occ {
+    static cudaError_t run(size_t d, size_t sps, int th, int *b) { return occ<QC, ES, FMT, TIN>(d, sps, th, b); }
+};
+template <bool QC, bool ES, int FMT, typename TIN>
+struct Launch {
+    static cudaError_t run(int g, int th, size_t d, const ResArgs *a, const QcTab *t, cudaStream_t s) {
+        return launch<QC, ES, FMT, TIN>(g, th, d, *a, *t, s);
+    }
+};
+
+}  // namespace
+
+cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, size_t dyn_smem, size_t smem_per_sm, int threads,
+                          int *blocks) {
+    return dispatch<Occ>(qc, es, fmt, i8, dyn_smem, smem_per_sm, threads, blocks);
+}
+
+cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, int grid, int threads, size_t dyn_smem, const ResArgs &a,
+                       const QcTab &t, cudaStream_t s) {
+    return dispatch<Launch>(qc, es, fmt, i8, grid, threads, dyn_smem, &a, &t, s);
+}
+
+}  // namespace ldpc

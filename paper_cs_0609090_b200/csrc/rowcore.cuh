@@ -17,6 +17,7 @@
 //            byte3 bit i  : s of edge 2i+1, frame hi     byte3 bit 4+i : idx, edge 2i+1, hi
 //          s bit = 1 means L_mn < 0; "idx" bit = 1 means n is an argmin (n = ñ_m).  dc <= 8.
 #pragma once
+#include "args.cuh"
 #include "simd16.cuh"
 
 namespace ldpc {
@@ -28,8 +29,9 @@ struct RowState {
 // Rebuild L^(k-1)_mn = s f(A, B, n, ñ) and form
 // q_mn = Z^(k-1)_n - L^(k-1)_mn (index reading D8) for all edges.
 template <int DC>
-__device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowState &st, uint32_t (&q)[DC]) {
-    const uint32_t nA = vneg(st.A), nB = vneg(st.B);
+__device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowState &st, uint32_t (&q)[DC],
+                                          const RegK &k) {
+    const uint32_t nA = vneg(st.A, k), nB = vneg(st.B, k);
 #pragma unroll
     for (int i = 0; i < (DC + 1) / 2; ++i) {
         const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte
@@ -88,10 +90,10 @@ __device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, u
 // nbeta2p1 = packed (1 - 2 beta), q2p1 = packed (2Q + 1).
 template <int DC>
 __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbeta2p1, uint32_t q2p1, RowState &st,
-                                          uint32_t (&r)[DC], uint32_t zero = 0u) {
+                                          uint32_t (&r)[DC], const RegK &k) {
     uint32_t mt[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) mt[j] = vmax(q[j], ~q[j]);   // 2|q| - [q<0]
+    for (int j = 0; j < DC; ++j) mt[j] = vmax(q[j], fnot(q[j], k));   // 2|q| - [q<0]
     uint32_t m1, m2;
     two_min<DC>(mt, m1, m2);
     uint32_t par = q[0];
@@ -102,15 +104,15 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbet
     // relu(min(m~ + 1 - 2 beta, 2Q + 1)) with the low bit cleared is exact (one VIADDMNMX + LOP3).
     const uint32_t A = vaddmin_relu(m1, nbeta2p1, q2p1) & 0xFFFEFFFEu;
     const uint32_t B = vaddmin_relu(m2, nbeta2p1, q2p1) & 0xFFFEFFFEu;
-    const uint32_t nA = vneg(A), nB = vneg(B);
+    const uint32_t nA = vneg(A, k), nB = vneg(B, k);
     // message for an edge whose own q is >= 0 carries the sign of the full product
     const uint32_t Apos = sel(Pm, nA, A), Aneg = sel(Pm, A, nA);
     const uint32_t Bpos = sel(Pm, nB, B), Bneg = sel(Pm, B, nB);
-    const uint32_t cm1 = ~m1;                                   // -m1 - 1
+    const uint32_t cm1 = fnot(m1, k);                           // -m1 - 1
     uint32_t W = 0, sqp = 0, ixp = 0;
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        const uint32_t ix = vaddmin(mt[j], cm1, zero);          // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
+        const uint32_t ix = vaddmin(mt[j], cm1, k.zero);          // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
         const uint32_t sq = signmask(q[j]);                     // 0xFFFF: q < 0
         r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
         if ((j & 1) == 0) {
@@ -133,18 +135,17 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbet
 
 // Hard-decision parity of the row for the syndrome (x̂ = 1 iff Z <= 0, P:168-172;
 // H x̂ = 0 test): bit 15 / bit 31 set iff the row's parity is odd.
+// Per half, sign(Lhat - 1) = [L <= 0].  The subtraction is one 32-bit IMAD of
+// -0x00010001: the low half can borrow from the high half (when it is 0), which
+// makes the high half Lhat_hi - 2 instead of Lhat_hi - 1 -- the same sign, because
+// doubled values are even.
 template <int DC>
-__device__ __forceinline__ uint32_t row_parity(const uint32_t (&L)[DC]) {
+__device__ __forceinline__ uint32_t row_parity(const uint32_t (&L)[DC], const RegK &k) {
     uint32_t p = 0;
 #pragma unroll
-    for (int j = 0; j < DC; ++j) p ^= vadd(L[j], 0xFFFFFFFFu);   // sign of (Lhat - 1) = [L <= 0]
+    for (int j = 0; j < DC; ++j) p ^= fadd32(L[j], 0xFFFEFFFFu, k);
     return p & 0x80008000u;
 }
-
-// ---------------- persistent state formats (workspace words per row-pair)
-// FMT_C16 : 3 words (A, B, W); magnitudes up to 2Q = 1022.
-// FMT_1BIT: 2 words (X = bytes [A_lo, B_lo, A_hi, B_hi], W); magnitudes up to 2Q = 254.
-enum { FMT_C16 = 0, FMT_1BIT = 1 };
 
 template <int FMT>
 struct StateIO {

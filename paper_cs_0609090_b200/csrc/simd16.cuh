@@ -13,8 +13,30 @@ namespace ldpc {
 __device__ __forceinline__ uint32_t vadd(uint32_t a, uint32_t b) { return __vadd2(a, b); }
 __device__ __forceinline__ uint32_t vmin(uint32_t a, uint32_t b) { return __vmins2(a, b); }
 __device__ __forceinline__ uint32_t vmax(uint32_t a, uint32_t b) { return __vmaxs2(a, b); }
-// -a per half (LOP3 + VIADD)
-__device__ __forceinline__ uint32_t vneg(uint32_t a) { return __vadd2(~a, 0x00010001u); }
+// Constants the kernels keep in REGISTERS (loaded from the kernel parameters, so ptxas
+// cannot see their values): they let bitwise-NOT and some additions run as IMAD on
+// the FMA pipe instead of LOP3 / IADD3 on the ALU pipe, which is the binding pipe of
+// the integer row core (ncu: ALU 69% vs FMA 15% busy).
+struct RegK {
+    uint32_t zero;   // 0
+    uint32_t m1;     // 0xFFFFFFFF
+    uint32_t one;    // 1
+};
+__host__ __device__ inline RegK make_regk() { return RegK{0u, 0xFFFFFFFFu, 1u}; }
+// ~a = a * (-1) + (-1): exact bitwise NOT as one IMAD (FMA pipe)
+__device__ __forceinline__ uint32_t fnot(uint32_t a, const RegK &k) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %2;" : "=r"(d) : "r"(a), "r"(k.m1));
+    return d;
+}
+// a + c (32-bit, wrapping) as one IMAD a * 1 + c (FMA pipe)
+__device__ __forceinline__ uint32_t fadd32(uint32_t a, uint32_t c, const RegK &k) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(k.one), "r"(c));
+    return d;
+}
+// -a per half (IMAD NOT + VIADD)
+__device__ __forceinline__ uint32_t vneg(uint32_t a, const RegK &k) { return __vadd2(fnot(a, k), 0x00010001u); }
 // min(a + b, c) per half, then max(., 0)   (VIADDMNMX.S16x2.RELU)
 __device__ __forceinline__ uint32_t vaddmin_relu(uint32_t a, uint32_t b, uint32_t c) {
     return __viaddmin_s16x2_relu(a, b, c);

@@ -1,0 +1,134 @@
+// stream_launch.cu -- launches of the streaming kernels (long codes) and the error counter.
+#include <algorithm>
+#include <cstdlib>
+
+#include "k_stream_pipe.cuh"
+#include "launch.h"
+
+namespace ldpc {
+
+// -------------------------------------------------------------- error counters
+__global__ void k_count_errors(int64_t nframes, int wpf, const uint32_t *hb, const uint8_t *ok, const int32_t *it,
+                               unsigned long long *cnt) {
+    unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nframes; f += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long be = 0;
+        for (int w = 0; w < wpf; ++w) be += __popc(hb[f * wpf + w]);
+        c0 += be;
+        c1 += be ? 1 : 0;
+        c2 += (be && ok[f]) ? 1 : 0;
+        c3 += ok[f] ? 0 : 1;
+        c4 += it ? (unsigned long long)it[f] : 0ull;
+    }
+    for (int o = 16; o; o >>= 1) {
+        c0 += __shfl_xor_sync(0xFFFFFFFFu, c0, o);
+        c1 += __shfl_xor_sync(0xFFFFFFFFu, c1, o);
+        c2 += __shfl_xor_sync(0xFFFFFFFFu, c2, o);
+        c3 += __shfl_xor_sync(0xFFFFFFFFu, c3, o);
+        c4 += __shfl_xor_sync(0xFFFFFFFFu, c4, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (c0) atomicAdd(cnt + 0, c0);
+        if (c1) atomicAdd(cnt + 1, c1);
+        if (c2) atomicAdd(cnt + 2, c2);
+        if (c3) atomicAdd(cnt + 3, c3);
+        if (c4) atomicAdd(cnt + 4, c4);
+    }
+}
+
+
+namespace {
+template <typename F>
+cudaError_t launch(F f, int32_t *n) {
+    f();
+    ++*n;
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t count_errors_launch(int64_t nframes, int wpf, const uint32_t *hb, const uint8_t *ok, const int32_t *it,
+                                unsigned long long *cnt, cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<int64_t>((nframes + 255) / 256, 4096);
+    k_count_errors<<<blocks, 256, 0, s>>>(nframes, wpf, hb, ok, it, cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, int32_t *nl) {
+    cudaError_t e;
+    // synd, done (contiguous) and per-frame flags
+    if ((e = cudaMemsetAsync(a.synd, 0, r.flags_bytes, s)) != cudaSuccess) return e;
+    const bool es = r.es;
+    const bool pair = r.pair;
+    const int nwarps_per_block = 8;
+    dim3 gi((unsigned)std::min<int64_t>(((int64_t)a.N + 7) / 8, 1024), (unsigned)r.ntiles);
+    // ~8 rows per warp per launch
+    const int rows_per_block = nwarps_per_block * 8;
+    dim3 gr((unsigned)std::max(1, (a.M + rows_per_block - 1) / rows_per_block), (unsigned)r.ntiles);
+    if (pair) {
+        if (r.i8) e = launch([&] { k_stream_ingest_i<int8_t><<<gi, 256, 0, s>>>(a); }, nl);
+        else e = launch([&] { k_stream_ingest_i<int16_t><<<gi, 256, 0, s>>>(a); }, nl);
+    } else {
+        e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); }, nl);
+    }
+    if (e != cudaSuccess) return e;
+    const unsigned fgrid = (unsigned)((r.ntiles * 32 + 255) / 256);
+    // software-pipelined iteration kernel (cp.async row prefetch) unless LDPC_PIPE=0
+    const char *pipe_env = getenv("LDPC_PIPE");
+    const bool use_pipe = r.max_dc <= 8 && !(pipe_env && pipe_env[0] == '0');
+    const dim3 gp((unsigned)((a.M + kPipeRB - 1) / kPipeRB), (unsigned)r.ntiles);
+    const size_t psmem = pipe_smem_bytes();
+    for (int k = 1; k <= r.max_iter && use_pipe; ++k) {
+        if (pair) {
+            if (r.fmt == FMT_C16) {
+                if (es) e = launch([&] { k_stream_pipe<true, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
+                else e = launch([&] { k_stream_pipe<true, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
+            } else {
+                if (es) e = launch([&] { k_stream_pipe<true, FMT_1BIT, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
+                else e = launch([&] { k_stream_pipe<true, FMT_1BIT, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
+            }
+        } else {
+            if (es) e = launch([&] { k_stream_pipe<false, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
+            else e = launch([&] { k_stream_pipe<false, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
+        }
+        if (e != cudaSuccess) return e;
+        if (es) {
+            if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); }, nl);
+            else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); }, nl);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    for (int k = 1; k <= r.max_iter && !use_pipe; ++k) {
+        if (pair) {
+            if (r.fmt == FMT_C16) {
+                if (es) e = launch([&] { k_stream_iter_i<FMT_C16, true><<<gr, 256, 0, s>>>(a, k); }, nl);
+                else e = launch([&] { k_stream_iter_i<FMT_C16, false><<<gr, 256, 0, s>>>(a, k); }, nl);
+            } else {
+                if (es) e = launch([&] { k_stream_iter_i<FMT_1BIT, true><<<gr, 256, 0, s>>>(a, k); }, nl);
+                else e = launch([&] { k_stream_iter_i<FMT_1BIT, false><<<gr, 256, 0, s>>>(a, k); }, nl);
+            }
+        } else {
+            if (es) e = launch([&] { k_stream_iter_f<true><<<gr, 256, 0, s>>>(a, k); }, nl);
+            else e = launch([&] { k_stream_iter_f<false><<<gr, 256, 0, s>>>(a, k); }, nl);
+        }
+        if (e != cudaSuccess) return e;
+        if (es) {
+            if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); }, nl);
+            else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); }, nl);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    const int kb = r.max_iter % 3;
+    if (pair) e = launch([&] { k_stream_syndrome<true><<<gr, 256, 0, s>>>(a, kb); }, nl);
+    else e = launch([&] { k_stream_syndrome<false><<<gr, 256, 0, s>>>(a, kb); }, nl);
+    if (e != cudaSuccess) return e;
+    if (pair) e = launch([&] { k_stream_finalize_flags<true><<<fgrid, 256, 0, s>>>(a); }, nl);
+    else e = launch([&] { k_stream_finalize_flags<false><<<fgrid, 256, 0, s>>>(a); }, nl);
+    if (e != cudaSuccess) return e;
+    dim3 go((unsigned)a.wpf, (unsigned)r.ntiles);
+    if (pair) e = launch([&] { k_stream_output<true><<<go, 256, 0, s>>>(a); }, nl);
+    else e = launch([&] { k_stream_output<false><<<go, 256, 0, s>>>(a); }, nl);
+    return e;
+}
+
+
+}  // namespace ldpc

@@ -314,9 +314,9 @@ def test_clamp_and_offset_variants_int():
         assert_int_parity(code, z, params, 12, 1, beta, Q)
 
 
-def test_multi_pair_qc_kernel(monkeypatch):
-    """The opt-in multi-pair QC kernel (LDPC_MP=1: 3 frame pairs per CTA) is bit-exact too."""
-    monkeypatch.setenv("LDPC_MP", "1")
+def test_qc_odd_batch_and_mixed_convergence():
+    """QC resident kernel: odd frame count (a half-empty last pair) on cfg2/cfg3, and a
+    2.25 dB batch where frames stop at different iterations."""
     for idx in (2, 3):
         cfg = g.CONFIGS[idx]
         code = cfg.code()

@@ -19,6 +19,7 @@ struct StreamRun {
     int fmt;              // FMT_C16 / FMT_1BIT
     bool es;              // per-frame early stop
     int max_iter, max_dc, ntiles;
+    int chunk_tiles;      // tiles decoded together through all iterations (0 = all)
     size_t flags_bytes;   // bytes from a.synd to the end of the per-tile flag words (zeroed first)
 };
 cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, int32_t *launches);

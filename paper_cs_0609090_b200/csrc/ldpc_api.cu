@@ -559,6 +559,11 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     r.max_dc = c->max_dc;
     r.ntiles = pl.ntiles;
     r.flags_bytes = pl.off_it - pl.off_synd;
+    // L2 chunking (opt-in, LDPC_CHUNK_TILES = tiles per chunk): measured SLOWER on cfg4/cfg5
+    // at every chunk size (the streaming kernels are issue/latency-bound,
+    // not HBM-bound, and chunks add launch tails), so all tiles run together by default.
+    r.chunk_tiles = 0;
+    if (const char *ce = getenv("LDPC_CHUNK_TILES")) r.chunk_tiles = atoi(ce);
     int32_t n = 0;
     cudaError_t e = stream_run(a, r, s, &n);
     g_launches += n;

@@ -75,46 +75,71 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
     // software-pipelined iteration kernel (cp.async row prefetch) unless LDPC_PIPE=0
     const char *pipe_env = getenv("LDPC_PIPE");
     const bool use_pipe = r.max_dc <= 8 && !(pipe_env && pipe_env[0] == '0');
-    const dim3 gp((unsigned)((a.M + kPipeRB - 1) / kPipeRB), (unsigned)r.ntiles);
     const size_t psmem = pipe_smem_bytes();
-    for (int k = 1; k <= r.max_iter && use_pipe; ++k) {
-        if (pair) {
-            if (r.fmt == FMT_C16) {
-                if (es) e = launch([&] { k_stream_pipe<true, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
-                else e = launch([&] { k_stream_pipe<true, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
+    // Frame tiles are decoded in CHUNKS whose per-iteration working set (Z^(0), the three
+    // posterior planes and the compact state of the chunk's tiles) fits in L2: all
+    // iterations of a chunk run before the next chunk starts, so after the first
+    // iteration the streaming kernels hit L2 instead of HBM.  Every kernel of the
+    // iteration loop indexes per tile, so a chunk is the same arguments with the
+    // tile-major pointers advanced.
+    const int chunk = r.chunk_tiles > 0 ? std::min(r.chunk_tiles, r.ntiles) : r.ntiles;
+    const int tw = pair ? 64 : 32;
+    const int nst = pair ? (r.fmt == FMT_C16 ? 3 : 2) : 3;
+    for (int t0 = 0; t0 < r.ntiles; t0 += chunk) {
+        const int nt = std::min(chunk, r.ntiles - t0);
+        StreamArgs c = a;
+        const size_t plane = (size_t)t0 * a.N * 32;
+        c.Z0 = a.Z0 + plane;
+        for (int i = 0; i < 3; ++i) c.Lb[i] = a.Lb[i] + plane;
+        c.st = a.st + (size_t)t0 * nst * a.M * 32;
+        c.synd = a.synd + (size_t)t0 * 32;
+        c.done = a.done + (size_t)t0 * 32;
+        c.it_ws = a.it_ws + (size_t)t0 * tw;
+        c.ok_ws = a.ok_ws + (size_t)t0 * tw;
+        c.nframes = a.nframes - t0 * tw;
+        c.ntiles = nt;
+        const unsigned fgrid = (unsigned)((nt * 32 + 255) / 256);
+        const dim3 gp((unsigned)((a.M + kPipeRB - 1) / kPipeRB), (unsigned)nt);
+        const dim3 gr((unsigned)std::max(1, (a.M + rows_per_block - 1) / rows_per_block), (unsigned)nt);
+        for (int k = 1; k <= r.max_iter && use_pipe; ++k) {
+            if (pair) {
+                if (r.fmt == FMT_C16) {
+                    if (es) e = launch([&] { k_stream_pipe<true, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
+                    else e = launch([&] { k_stream_pipe<true, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
+                } else {
+                    if (es) e = launch([&] { k_stream_pipe<true, FMT_1BIT, true><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
+                    else e = launch([&] { k_stream_pipe<true, FMT_1BIT, false><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
+                }
             } else {
-                if (es) e = launch([&] { k_stream_pipe<true, FMT_1BIT, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
-                else e = launch([&] { k_stream_pipe<true, FMT_1BIT, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
+                if (es) e = launch([&] { k_stream_pipe<false, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
+                else e = launch([&] { k_stream_pipe<false, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
             }
-        } else {
-            if (es) e = launch([&] { k_stream_pipe<false, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
-            else e = launch([&] { k_stream_pipe<false, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(a, k); }, nl);
-        }
-        if (e != cudaSuccess) return e;
-        if (es) {
-            if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); }, nl);
-            else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); }, nl);
             if (e != cudaSuccess) return e;
+            if (es) {
+                if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(c, k); }, nl);
+                else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(c, k); }, nl);
+                if (e != cudaSuccess) return e;
+            }
         }
-    }
-    for (int k = 1; k <= r.max_iter && !use_pipe; ++k) {
-        if (pair) {
-            if (r.fmt == FMT_C16) {
-                if (es) e = launch([&] { k_stream_iter_i<FMT_C16, true><<<gr, 256, 0, s>>>(a, k); }, nl);
-                else e = launch([&] { k_stream_iter_i<FMT_C16, false><<<gr, 256, 0, s>>>(a, k); }, nl);
+        for (int k = 1; k <= r.max_iter && !use_pipe; ++k) {
+            if (pair) {
+                if (r.fmt == FMT_C16) {
+                    if (es) e = launch([&] { k_stream_iter_i<FMT_C16, true><<<gr, 256, 0, s>>>(c, k); }, nl);
+                    else e = launch([&] { k_stream_iter_i<FMT_C16, false><<<gr, 256, 0, s>>>(c, k); }, nl);
+                } else {
+                    if (es) e = launch([&] { k_stream_iter_i<FMT_1BIT, true><<<gr, 256, 0, s>>>(c, k); }, nl);
+                    else e = launch([&] { k_stream_iter_i<FMT_1BIT, false><<<gr, 256, 0, s>>>(c, k); }, nl);
+                }
             } else {
-                if (es) e = launch([&] { k_stream_iter_i<FMT_1BIT, true><<<gr, 256, 0, s>>>(a, k); }, nl);
-                else e = launch([&] { k_stream_iter_i<FMT_1BIT, false><<<gr, 256, 0, s>>>(a, k); }, nl);
+                if (es) e = launch([&] { k_stream_iter_f<true><<<gr, 256, 0, s>>>(c, k); }, nl);
+                else e = launch([&] { k_stream_iter_f<false><<<gr, 256, 0, s>>>(c, k); }, nl);
             }
-        } else {
-            if (es) e = launch([&] { k_stream_iter_f<true><<<gr, 256, 0, s>>>(a, k); }, nl);
-            else e = launch([&] { k_stream_iter_f<false><<<gr, 256, 0, s>>>(a, k); }, nl);
-        }
-        if (e != cudaSuccess) return e;
-        if (es) {
-            if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); }, nl);
-            else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); }, nl);
             if (e != cudaSuccess) return e;
+            if (es) {
+                if (pair) e = launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(c, k); }, nl);
+                else e = launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(c, k); }, nl);
+                if (e != cudaSuccess) return e;
+            }
         }
     }
     const int kb = r.max_iter % 3;

@@ -325,3 +325,26 @@ def test_qc_odd_batch_and_mixed_convergence():
     s2 = g.ebn0_to_sigma2(2.25, g.CONFIGS[2].code().rate)
     llr = g.llr(99, 0, 200, g.CONFIGS[2].code().n_vars, s2, g.LLR_I16, 3, 511)
     assert_int_parity(g.CONFIGS[2].code(), llr, _cfg_params(g.CONFIGS[2]), 15, 1, 1, 511)
+
+
+@pytest.mark.parametrize("chunk", ["1", "2"])
+def test_stream_l2_chunks(chunk, monkeypatch):
+    """Streaming kernels decoding the frame tiles in chunks (LDPC_CHUNK_TILES, opt-in):
+    int16 with early stop on a QC code (mixed stopping iterations), 1-bit, and fp32 --
+    several tiles plus a ragged last tile, identical to the oracle."""
+    monkeypatch.setenv("LDPC_FORCE_STREAM", "1")
+    monkeypatch.setenv("LDPC_CHUNK_TILES", chunk)
+    code = g.qc(6, 12, 37, np.array([3, 4] * 6, np.int32), seed=8)
+    s2 = g.ebn0_to_sigma2(2.5, code.rate)
+    llr = g.llr(41, 0, 230, code.n_vars, s2, g.LLR_I16, 3, 511)
+    params = P.make_params(12, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 0, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+    assert_int_parity(code, llr, params, 12, 1, 1, 511)
+    llr = g.llr(43, 0, 230, code.n_vars, s2, g.LLR_I8, 2, 127)
+    params = P.make_params(12, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 127, P.LDPC_LLR_I8, P.LDPC_MSG_1BIT)
+    assert_int_parity(code, llr, params, 12, 0, 1, 127)
+    llr = g.llr(42, 0, 100, code.n_vars, s2, g.LLR_F32)
+    params = P.make_params(10, 1, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    ref = oracle.decode(code, llr, "compact", "f32", 10, 1, alpha=0.75, nthreads=NT)
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    np.testing.assert_array_equal(it, ref.iters)

@@ -91,6 +91,17 @@ enum { LDPC_MINSUM_OFFSET = 0,       /* |L| <= max(|L| - beta, 0); offset 0 = pl
  *   ONEBIT : "1-bit messages": the only per-edge persistent datum is the
  *            sign bit; magnitudes are stored as bytes (integer LLRs, Q <= 127). */
 enum { LDPC_MSG_COMPACT = 0, LDPC_MSG_1BIT = 1 };
+/* Decoding schedule.
+ *   SINGLESCAN: the paper's method -- flooding single-scan min-sum over the compact
+ *               state (Eq.(3)); the default.
+ *   TWOSCAN   : the two-scan min-sum of §3 the paper compares against
+ *               (P:29-30): per-edge messages L_mn and Z_mn in device memory, a
+ *               horizontal (check) and a vertical (variable) scan per iteration, both
+ *               addressings.  Same outputs as SINGLESCAN (bit-exact for
+ *               integer LLRs); requires msg_format COMPACT, row degree <= 8 and
+ *               column degree <= 16 (else LDPC_ERR_UNSUPPORTED).  A baseline, not a
+ *               fast path: it always uses the streaming (HBM) layout. */
+enum { LDPC_SCHED_SINGLESCAN = 0, LDPC_SCHED_TWOSCAN = 1 };
 
 typedef struct {
     int32_t max_iter;      /* >= 1: the iteration cap of P:174-175 */
@@ -108,7 +119,7 @@ typedef struct {
                               Q <= 127 (ONEBIT), else LDPC_ERR_UNSUPPORTED.  Ignored for F32. */
     int32_t llr_type;      /* LDPC_LLR_I16 | LDPC_LLR_I8 | LDPC_LLR_F32 */
     int32_t msg_format;    /* LDPC_MSG_COMPACT | LDPC_MSG_1BIT (1BIT requires integer LLRs) */
-    int32_t reserved;      /* must be 0 */
+    int32_t schedule;      /* LDPC_SCHED_SINGLESCAN (0, default) | LDPC_SCHED_TWOSCAN */
 } ldpc_decode_params;
 
 /* Device workspace bytes needed by ldpc_decode_batch for n_frames frames. */

@@ -22,6 +22,7 @@ LDPC_OK, LDPC_ERR_INVALID_ARG, LDPC_ERR_INVALID_CODE, LDPC_ERR_UNSUPPORTED, LDPC
 LDPC_LLR_I16, LDPC_LLR_I8, LDPC_LLR_F32 = 0, 1, 2
 LDPC_MINSUM_OFFSET, LDPC_MINSUM_NORMALIZED = 0, 1
 LDPC_MSG_COMPACT, LDPC_MSG_1BIT = 0, 1
+LDPC_SCHED_SINGLESCAN, LDPC_SCHED_TWOSCAN = 0, 1
 
 # every symbol include/ldpc.h declares
 EXPORTS = [
@@ -42,7 +43,7 @@ class ldpc_decode_params(ctypes.Structure):
     _fields_ = [("max_iter", ctypes.c_int32), ("early_stop", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("offset_raw", ctypes.c_int32), ("offset_f", ctypes.c_float), ("alpha", ctypes.c_float),
                 ("clamp_raw", ctypes.c_int32), ("llr_type", ctypes.c_int32), ("msg_format", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("schedule", ctypes.c_int32)]
 
 
 class LdpcError(RuntimeError):
@@ -150,9 +151,11 @@ def ldpc_code_query(handle: int):
 
 
 def make_params(max_iter=10, early_stop=0, variant=LDPC_MINSUM_OFFSET, offset_raw=0, offset_f=0.0, alpha=1.0,
-                clamp_raw=0, llr_type=LDPC_LLR_I16, msg_format=LDPC_MSG_COMPACT) -> ldpc_decode_params:
+                clamp_raw=0, llr_type=LDPC_LLR_I16, msg_format=LDPC_MSG_COMPACT,
+                schedule=None) -> ldpc_decode_params:
+    sched = LDPC_SCHED_SINGLESCAN if schedule is None else int(schedule)
     return ldpc_decode_params(int(max_iter), int(early_stop), int(variant), int(offset_raw), float(offset_f),
-                              float(alpha), int(clamp_raw), int(llr_type), int(msg_format), 0)
+                              float(alpha), int(clamp_raw), int(llr_type), int(msg_format), sched)
 
 
 def ldpc_decode_workspace_size(handle: int, n_frames: int, params: ldpc_decode_params) -> int:
@@ -289,12 +292,15 @@ class Decoder:
         return counters
 
 
-def params_for_config(cfg) -> ldpc_decode_params:
-    """Decode parameters of one of ldpcgen.CONFIGS (BASELINE.json configs)."""
+def params_for_config(cfg, schedule=LDPC_SCHED_SINGLESCAN) -> ldpc_decode_params:
+    """Decode parameters of one of ldpcgen.CONFIGS (BASELINE.json configs).
+    schedule=LDPC_SCHED_TWOSCAN gives the paper's two-scan baseline on the same workload
+    (full per-edge messages, so the message format is COMPACT)."""
     import ldpcgen
     llr_type = {ldpcgen.LLR_I16: LDPC_LLR_I16, ldpcgen.LLR_I8: LDPC_LLR_I8, ldpcgen.LLR_F32: LDPC_LLR_F32}[cfg.llr_kind]
     if cfg.variant == "normalized":
         return make_params(cfg.max_iter, cfg.early_stop, LDPC_MINSUM_NORMALIZED, 0, 0.0, cfg.alpha, 0, llr_type,
-                           LDPC_MSG_COMPACT)
+                           LDPC_MSG_COMPACT, schedule)
+    fmt = LDPC_MSG_1BIT if cfg.msg_format == "1bit" and schedule == LDPC_SCHED_SINGLESCAN else LDPC_MSG_COMPACT
     return make_params(cfg.max_iter, cfg.early_stop, LDPC_MINSUM_OFFSET, cfg.offset_raw, 0.0, 1.0, cfg.clamp,
-                       llr_type, LDPC_MSG_1BIT if cfg.msg_format == "1bit" else LDPC_MSG_COMPACT)
+                       llr_type, fmt, schedule)

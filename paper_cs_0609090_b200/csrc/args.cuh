@@ -66,6 +66,16 @@ struct StreamArgs {
     int32_t *iters;
 };
 
+// two-scan baseline (k_twoscan.cuh): column addressing and the per-edge message planes
+struct TwoScanArgs {
+    const int32_t *vptr;    // [N+1] column pointers
+    const int32_t *vedge;   // [E] edge ids of column n, ascending row
+    const int32_t *ecol;    // [E] column of edge e (CSR col_idx)
+    uint32_t *msg;          // [tile][E][32] L_mn
+    uint32_t *zv;           // [tile][E][32] Z_mn
+    int64_t E;
+};
+
 // persistent state formats (workspace words per row-pair)
 // FMT_C16 : 3 words (A, B, W); magnitudes up to 2Q = 1022.
 // FMT_1BIT: 2 words (X = bytes [A_lo, B_lo, A_hi, B_hi], W); magnitudes up to 2Q = 254.

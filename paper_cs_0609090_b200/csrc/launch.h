@@ -24,6 +24,11 @@ struct StreamRun {
 };
 cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, int32_t *launches);
 
+// Two-scan min-sum baseline (k_twoscan.cuh), same workspace conventions plus the
+// per-edge message planes in `t`.
+cudaError_t twoscan_run(const StreamArgs &a, const TwoScanArgs &t, const StreamRun &r, cudaStream_t s,
+                        int32_t *launches);
+
 cudaError_t count_errors_launch(int64_t nframes, int wpf, const uint32_t *hb, const uint8_t *ok, const int32_t *it,
                                 unsigned long long *cnt, cudaStream_t s);
 

@@ -68,6 +68,8 @@ struct ldpc_code {
     // device CSR (stream kernels)
     int32_t *d_row_ptr = nullptr, *d_col_idx = nullptr;
     uint32_t *d_rowtab = nullptr;   // [M][8] padded column table (streaming kernels)
+    // variable->check addressing, used only by the two-scan baseline
+    int32_t *d_vptr = nullptr, *d_vedge = nullptr;
     // resident schedule
     bool qc = false;
     int Z = 0, mb = 0, nb = 0;
@@ -148,6 +150,8 @@ static void free_code(ldpc_code *c) {
     cudaFree(c->d_row_ptr);
     cudaFree(c->d_col_idx);
     cudaFree(c->d_rowtab);
+    cudaFree(c->d_vptr);
+    cudaFree(c->d_vedge);
     delete c->qtab;
     cudaFree(c->d_bptr);
     cudaFree(c->d_colT);
@@ -190,6 +194,22 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
         return st;
     }
     const int N = c->N, M = c->M;
+    {
+        // column-major edge lists M(n) (ascending row) for the two-scan variable pass
+        std::vector<int32_t> vptr((size_t)N + 1, 0), vedge((size_t)c->E), fill((size_t)N, 0);
+        for (int64_t e = 0; e < c->E; ++e) vptr[(size_t)desc->col_idx[e] + 1]++;
+        for (int n = 0; n < N; ++n) vptr[(size_t)n + 1] += vptr[n];
+        for (int m = 0; m < M; ++m)
+            for (int32_t e = desc->row_ptr[m]; e < desc->row_ptr[m + 1]; ++e) {
+                const int n = desc->col_idx[e];
+                vedge[(size_t)vptr[n] + fill[n]++] = e;
+            }
+        if ((st = upload(&c->d_vptr, vptr.data(), vptr.size())) != LDPC_OK ||
+            (st = upload(&c->d_vedge, vedge.data(), vedge.size())) != LDPC_OK) {
+            free_code(c);
+            return st;
+        }
+    }
     {
         std::vector<uint32_t> rt((size_t)M * 8, 0u);
         for (int m = 0; m < M; ++m) {
@@ -380,6 +400,7 @@ enum Path { PATH_RESIDENT = 0, PATH_STREAM_I = 1, PATH_STREAM_F = 2 };
 
 struct Plan {
     Path path;
+    int sched = LDPC_SCHED_SINGLESCAN;
     int Q = 0, beta = 0, fmt = FMT_C16;
     float alpha = 1.f, betaf = 0.f;
     // resident
@@ -390,6 +411,7 @@ struct Plan {
     // stream
     int tile = 64, ntiles = 0;
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
+    size_t off_msg = 0, off_zv = 0;   // two-scan: per-edge L_mn and Z_mn planes
     size_t ws_bytes = 0;
 };
 
@@ -405,7 +427,15 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (F > (int64_t)1 << 31) return fail(LDPC_ERR_UNSUPPORTED, "n_frames > 2^31");
     if (p->max_iter < 1) return fail(LDPC_ERR_INVALID_ARG, "max_iter must be >= 1");
     if (p->early_stop != 0 && p->early_stop != 1) return fail(LDPC_ERR_INVALID_ARG, "early_stop must be 0 or 1");
-    if (p->reserved != 0) return fail(LDPC_ERR_INVALID_ARG, "reserved must be 0");
+    if (p->schedule != LDPC_SCHED_SINGLESCAN && p->schedule != LDPC_SCHED_TWOSCAN)
+        return fail(LDPC_ERR_INVALID_ARG, "bad schedule %d", p->schedule);
+    pl.sched = p->schedule;
+    if (pl.sched == LDPC_SCHED_TWOSCAN) {
+        if (p->msg_format != LDPC_MSG_COMPACT)
+            return fail(LDPC_ERR_UNSUPPORTED, "two-scan stores full per-edge messages: msg_format must be COMPACT");
+        if (c->max_dc > 8) return fail(LDPC_ERR_UNSUPPORTED, "two-scan supports row degree <= 8 (max %d)", c->max_dc);
+        if (c->max_dv > 16) return fail(LDPC_ERR_UNSUPPORTED, "two-scan supports column degree <= 16 (max %d)", c->max_dv);
+    }
     if (p->msg_format != LDPC_MSG_COMPACT && p->msg_format != LDPC_MSG_1BIT)
         return fail(LDPC_ERR_INVALID_ARG, "bad msg_format %d", p->msg_format);
     if (p->variant != LDPC_MINSUM_OFFSET && p->variant != LDPC_MINSUM_NORMALIZED)
@@ -439,7 +469,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         pl.beta = p->offset_raw;
         // LDPC_FORCE_STREAM=1 (test hook) routes integer decodes through the streaming kernels
         const char *force = getenv("LDPC_FORCE_STREAM");
-        pl.path = (c->res_ok && !(force && force[0] == '1')) ? PATH_RESIDENT : PATH_STREAM_I;
+        pl.path = (c->res_ok && !(force && force[0] == '1') && pl.sched == LDPC_SCHED_SINGLESCAN) ? PATH_RESIDENT
+                                                                                                   : PATH_STREAM_I;
         pl.tile = 64;
     } else {
         return fail(LDPC_ERR_INVALID_ARG, "bad llr_type %d", p->llr_type);
@@ -472,7 +503,13 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         size_t off = 0;
         pl.off_z0 = off; off += align256(plane);
         for (int i = 0; i < 3; ++i) { pl.off_lb[i] = off; off += align256(plane); }
-        pl.off_st = off; off += align256((size_t)pl.ntiles * sw * c->M * 32 * 4);
+        if (pl.sched == LDPC_SCHED_TWOSCAN) {
+            const size_t eplane = (size_t)pl.ntiles * (size_t)c->E * 32 * 4;
+            pl.off_msg = off; off += align256(eplane);
+            pl.off_zv = off; off += align256(eplane);
+        } else {
+            pl.off_st = off; off += align256((size_t)pl.ntiles * sw * c->M * 32 * 4);
+        }
         pl.off_synd = off; off += align256((size_t)pl.ntiles * 32 * 4);
         pl.off_done = off; off += align256((size_t)pl.ntiles * 32 * 4);
         pl.off_it = off; off += align256((size_t)pl.ntiles * pl.tile * 4);
@@ -565,7 +602,19 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     r.chunk_tiles = 0;
     if (const char *ce = getenv("LDPC_CHUNK_TILES")) r.chunk_tiles = atoi(ce);
     int32_t n = 0;
-    cudaError_t e = stream_run(a, r, s, &n);
+    cudaError_t e;
+    if (pl.sched == LDPC_SCHED_TWOSCAN) {
+        TwoScanArgs t{};
+        t.vptr = c->d_vptr;
+        t.vedge = c->d_vedge;
+        t.ecol = c->d_col_idx;
+        t.msg = (uint32_t *)(w + pl.off_msg);
+        t.zv = (uint32_t *)(w + pl.off_zv);
+        t.E = c->E;
+        e = twoscan_run(a, t, r, s, &n);
+    } else {
+        e = stream_run(a, r, s, &n);
+    }
     g_launches += n;
     return e;
 }

@@ -3,6 +3,7 @@
 #include <cstdlib>
 
 #include "k_stream_pipe.cuh"
+#include "k_twoscan.cuh"
 #include "launch.h"
 
 namespace ldpc {
@@ -155,5 +156,66 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
     return e;
 }
 
+
+// Two-scan min-sum (k_twoscan.cuh): ingest, Z_mn init, then per iteration the
+// horizontal and vertical scans; early stop checks H x^ = 0 on Z^(k) after each
+// iteration (and on Z^(0) first, reading D10) with the shared syndrome/freeze kernels.
+cudaError_t twoscan_run(const StreamArgs &a, const TwoScanArgs &t, const StreamRun &r, cudaStream_t s, int32_t *nl) {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(a.synd, 0, r.flags_bytes, s)) != cudaSuccess) return e;
+    const bool pair = r.pair, es = r.es;
+    dim3 gi((unsigned)std::min<int64_t>(((int64_t)a.N + 7) / 8, 1024), (unsigned)r.ntiles);
+    if (pair) {
+        if (r.i8) e = launch([&] { k_stream_ingest_i<int8_t><<<gi, 256, 0, s>>>(a); }, nl);
+        else e = launch([&] { k_stream_ingest_i<int16_t><<<gi, 256, 0, s>>>(a); }, nl);
+    } else {
+        e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); }, nl);
+    }
+    if (e != cudaSuccess) return e;
+    const dim3 ge((unsigned)std::min<int64_t>((t.E + 7) / 8, 4096), (unsigned)r.ntiles);
+    const dim3 gm((unsigned)std::max(1, std::min((a.M + 7) / 8, 4096)), (unsigned)r.ntiles);
+    const dim3 gn((unsigned)std::max(1, std::min((a.N + 7) / 8, 4096)), (unsigned)r.ntiles);
+    const dim3 gr((unsigned)std::max(1, (a.M + 63) / 64), (unsigned)r.ntiles);
+    const unsigned fgrid = (unsigned)((r.ntiles * 32 + 255) / 256);
+    auto syndrome = [&](int bufidx) {
+        return pair ? launch([&] { k_stream_syndrome<true><<<gr, 256, 0, s>>>(a, bufidx); }, nl)
+                    : launch([&] { k_stream_syndrome<false><<<gr, 256, 0, s>>>(a, bufidx); }, nl);
+    };
+    auto freeze = [&](int k) {
+        return pair ? launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); }, nl)
+                    : launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); }, nl);
+    };
+    e = pair ? launch([&] { k_ts_init<true><<<ge, 256, 0, s>>>(a, t); }, nl)
+             : launch([&] { k_ts_init<false><<<ge, 256, 0, s>>>(a, t); }, nl);
+    if (e != cudaSuccess) return e;
+    if (es) {
+        // k = 0: Z^(0) is in Lb[0]; frames passing freeze with iterations_used = 0
+        if ((e = syndrome(0)) != cudaSuccess || (e = freeze(1)) != cudaSuccess) return e;
+    }
+    for (int k = 1; k <= r.max_iter; ++k) {
+        e = pair ? launch([&] { k_ts_check<true><<<gm, 256, 0, s>>>(a, t); }, nl)
+                 : launch([&] { k_ts_check<false><<<gm, 256, 0, s>>>(a, t); }, nl);
+        if (e != cudaSuccess) return e;
+        if (pair) {
+            if (es) e = launch([&] { k_ts_var<true, true><<<gn, 256, 0, s>>>(a, t, k); }, nl);
+            else e = launch([&] { k_ts_var<true, false><<<gn, 256, 0, s>>>(a, t, k); }, nl);
+        } else {
+            if (es) e = launch([&] { k_ts_var<false, true><<<gn, 256, 0, s>>>(a, t, k); }, nl);
+            else e = launch([&] { k_ts_var<false, false><<<gn, 256, 0, s>>>(a, t, k); }, nl);
+        }
+        if (e != cudaSuccess) return e;
+        if (es && k < r.max_iter) {
+            if ((e = syndrome(k % 3)) != cudaSuccess || (e = freeze(k + 1)) != cudaSuccess) return e;
+        }
+    }
+    // final syndrome of Z^(K); frames not frozen get iterations_used = K
+    if ((e = syndrome(r.max_iter % 3)) != cudaSuccess) return e;
+    e = pair ? launch([&] { k_stream_finalize_flags<true><<<fgrid, 256, 0, s>>>(a); }, nl)
+             : launch([&] { k_stream_finalize_flags<false><<<fgrid, 256, 0, s>>>(a); }, nl);
+    if (e != cudaSuccess) return e;
+    dim3 go((unsigned)a.wpf, (unsigned)r.ntiles);
+    return pair ? launch([&] { k_stream_output<true><<<go, 256, 0, s>>>(a); }, nl)
+                : launch([&] { k_stream_output<false><<<go, 256, 0, s>>>(a); }, nl);
+}
 
 }  // namespace ldpc

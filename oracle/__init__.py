@@ -12,6 +12,9 @@ Engines (PAPER.md section / lines):
   TWOSCAN        §3 with the two-minima check rule
   SINGLESCAN     §4 single-scan, per-edge L storage
   COMPACT        §5 memory-efficient single-scan -- the GPU's parity target
+  LAYERED_FULL   Eq.(3) with ONE in-place posterior array, rows in ascending m (layered /
+                 Gauss-Seidel reading D25); per-edge L, Eq.(1) literally
+  LAYERED        the same schedule over the §5 compact state -- the GPU layered target
 Numeric modes: "int" (int32 raw LSBs; offset beta + clamp Q), "f64", "f32".
 """
 from __future__ import annotations
@@ -28,8 +31,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-TWOSCAN_NAIVE, TWOSCAN, SINGLESCAN, COMPACT = 0, 1, 2, 3
-ENGINES = {"twoscan_naive": TWOSCAN_NAIVE, "twoscan": TWOSCAN, "singlescan": SINGLESCAN, "compact": COMPACT}
+TWOSCAN_NAIVE, TWOSCAN, SINGLESCAN, COMPACT, LAYERED_FULL, LAYERED = 0, 1, 2, 3, 4, 5
+ENGINES = {"twoscan_naive": TWOSCAN_NAIVE, "twoscan": TWOSCAN, "singlescan": SINGLESCAN, "compact": COMPACT,
+           "layered_full": LAYERED_FULL, "layered": LAYERED}
 
 
 class Params(ctypes.Structure):

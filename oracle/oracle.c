@@ -14,6 +14,10 @@
  *   ENG_SINGLESCAN     §4 Eq.(3) block with per-edge L_mn storage.
  *   ENG_COMPACT        §5 memory-efficient single-scan (variants P:338-353):
  *                      the CUDA path's direct parity target.
+ *   ENG_LAYERED_FULL   the Eq.(3) block with a single in-place posterior array (the
+ *                      layered / Gauss-Seidel reading, DESIGN D25),
+ *                      per-edge L_mn and Eq.(1) evaluated literally.
+ *   ENG_LAYERED        the same schedule over the §5 compact state (GPU layered target).
  * Numeric types: int32 (fixed point, offset + clamp), double, float.
  * Readings of silent/ambiguous passages are listed in DESIGN.md §3 (D1-D23).
  * Parity pins: tests/test_oracle_*.py (none of this file is "parity unpinned").
@@ -24,7 +28,8 @@
 #include <pthread.h>
 #include <unistd.h>
 
-enum { ENG_TWOSCAN_NAIVE = 0, ENG_TWOSCAN = 1, ENG_SINGLESCAN = 2, ENG_COMPACT = 3 };
+enum { ENG_TWOSCAN_NAIVE = 0, ENG_TWOSCAN = 1, ENG_SINGLESCAN = 2, ENG_COMPACT = 3,
+       ENG_LAYERED_FULL = 4, ENG_LAYERED = 5 };
 
 typedef struct {
     int32_t max_iter;     /* K >= 1 */

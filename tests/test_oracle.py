@@ -320,3 +320,78 @@ def test_exhaustive_ml_tiny_code_high_snr():
     assert agree >= 0.98, agree
     conv = r.ok == 1
     assert np.all(((r.bits[conv].astype(np.int64) @ H.T) % 2) == 0)
+
+
+# ------------------------------------------------- layered schedule (§8(f2))
+@pytest.mark.parametrize("case", _load("layered_toy.json")["cases"], ids=lambda c: c["cite"])
+@pytest.mark.parametrize("engine", ["layered_full", "layered"])
+def test_layered_toy_trajectories(case, engine):
+    """Hand-evaluated in-place trajectories (tests/golden/layered_toy.json, reading D25)."""
+    code = g.from_dense(_load("layered_toy.json")["code"])
+    r = oracle.decode(code, np.array([case["z0"]]), engine=engine, mode=case["mode"], max_iter=2,
+                      beta=case["beta"], trace=True)
+    np.testing.assert_allclose(r.trace_post[0], case["post"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("code", _codes_small(), ids=lambda c: c.name)
+@pytest.mark.parametrize("beta,clamp", [(0, 511), (1, 31)])
+def test_layered_compact_equals_full_messages(code, beta, clamp):
+    """The compact state recovers every previous message exactly, so the
+    layered schedule over the compact state is bit-identical to layered with stored
+    per-edge L_mn and the literal Eq.(1) rule, per iteration, with and without early stop."""
+    sigma2 = g.ebn0_to_sigma2(1.5, max(code.rate, 0.3))
+    z0 = g.llr(78, 0, 30, code.n_vars, sigma2, g.LLR_I16, 3, 511).astype(np.int32)
+    for es in (0, 1):
+        a = oracle.decode(code, z0, "layered_full", "int", 20, es, beta, clamp, trace=True)
+        b = oracle.decode(code, z0, "layered", "int", 20, es, beta, clamp, trace=True)
+        for x, y in [(a.trace_post, b.trace_post), (a.trace_msg, b.trace_msg), (a.post, b.post), (a.bits, b.bits),
+                     (a.ok, b.ok), (a.iters, b.iters)]:
+            assert np.array_equal(x, y)
+
+
+def test_layered_equals_flooding_when_rows_share_no_variable():
+    """With every column in one row there is nothing for a later row to see: the
+    layered and flooding schedules coincide exactly."""
+    rng = np.random.default_rng(7)
+    perm = rng.permutation(60)
+    H = np.zeros((12, 60), np.uint8)
+    for m in range(12):
+        H[m, perm[5 * m:5 * m + 5]] = 1
+    code = g.from_dense(H, name="disjoint")
+    z0 = rng.integers(-60, 61, (20, 60)).astype(np.int32)
+    a = oracle.decode(code, z0, "layered", "int", 6, 0, 1, 127, trace=True)
+    b = oracle.decode(code, z0, "compact", "int", 6, 0, 1, 127, trace=True)
+    assert np.array_equal(a.trace_post, b.trace_post)
+
+
+def test_layered_tree_posteriors_are_exact_max_marginals():
+    """On a cycle-free Tanner graph the layered schedule, like flooding, reaches the
+    exact max-marginals (plain min-sum) once enough iterations have run."""
+    rng = np.random.default_rng(321)
+    for t in range(300):
+        code = _random_tree_code(rng, n_checks=int(rng.integers(2, 6)))
+        C = _codewords(code.dense())
+        z0 = rng.integers(-20, 21, (1, code.n_vars))
+        r = oracle.decode(code, z0, "layered", "int", 12, 0, 0, 0)
+        mc = ((1 - 2 * C.astype(np.int64)) * z0).sum(axis=1)
+        want = np.array([(mc[C[:, n] == 0].max() - mc[C[:, n] == 1].max()) // 2 for n in range(code.n_vars)])
+        assert np.array_equal(r.post[0], want), t
+
+
+def test_layered_row_order_matters_and_stopping():
+    """Layered is NOT the flooding schedule on a loopy code -- it differs after
+    the first row that sees an earlier update -- yet noiseless frames still stop at k=0
+    and converged hard decisions agree with flooding at high SNR."""
+    code = g.regular(96, 3, 6, seed=5)
+    z0 = g.llr(5, 0, 8, code.n_vars, g.ebn0_to_sigma2(1.5, code.rate), g.LLR_I16, 3, 511).astype(np.int32)
+    a = oracle.decode(code, z0, "layered", "int", 3, 0, 1, 511)
+    b = oracle.decode(code, z0, "compact", "int", 3, 0, 1, 511)
+    assert not np.array_equal(a.post, b.post)
+    r = oracle.decode(code, np.full((3, code.n_vars), 12, np.int32), "layered", "int", 10, 1, 1, 511)
+    assert np.all(r.iters == 0) and np.all(r.ok == 1)
+    z0 = g.llr(6, 0, 40, code.n_vars, g.ebn0_to_sigma2(5.0, code.rate), g.LLR_I16, 3, 511).astype(np.int32)
+    a = oracle.decode(code, z0, "layered", "int", 30, 1, 1, 511)
+    b = oracle.decode(code, z0, "compact", "int", 30, 1, 1, 511)
+    both = (a.ok == 1) & (b.ok == 1)
+    assert both.sum() >= 38 and np.array_equal(a.bits[both], b.bits[both])
+    assert a.iters[both].mean() <= b.iters[both].mean()

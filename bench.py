@@ -176,6 +176,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-twoscan", action="store_true", help="skip timing the GPU two-scan baseline")
+    ap.add_argument("--no-layered", action="store_true", help="skip timing the layered schedule")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -300,34 +301,43 @@ def main():
                "d2h_bytes_per_step": int(hbh.numel() * 4 + okh.numel() + ith.numel() * 4),
                "ms_per_step": float(te.item()) / len(e_ms)}
 
-    # ---- the paper's comparison on the GPU: the two-scan schedule
-    # decoding the same frames, timed the same way (events on this stream, L2 flushed)
-    twoscan = None
-    if not args.no_twoscan:
-        tparams = P.params_for_config(cfg, P.LDPC_SCHED_TWOSCAN)
-        tout = dec.alloc_outputs(F, tparams.llr_type, posteriors=True)
-        dec.decode(llr, tparams, tout)
+    # ---- the other schedules on the same frames, timed the same way (events on this
+    # stream, L2 flushed): the paper's comparison against two-scan (SURVEY
+    # §8(f1)) and the layered schedule (§8(f2), resident-kernel codes only)
+    def time_schedule(sched):
+        sp = P.params_for_config(cfg, sched)
+        try:
+            dec.workspace(F, sp)
+        except P.LdpcError as ex:
+            return {"unsupported": str(ex)}
+        so = dec.alloc_outputs(F, sp.llr_type, posteriors=True)
+        dec.decode(llr, sp, so)
         torch.cuda.synchronize(dev)
         t_ms = []
         for i in range(max(2, min(args.steps, 5))):
             flush.fill_(i & 0xFF)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            dec.decode(llr, tparams, tout)
+            dec.decode(llr, sp, so)
             b.record(stream)
             b.synchronize()
             t_ms.append(a.elapsed_time(b))
         tt = torch.tensor([sum(t_ms)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ts_val = info_bits_per_step * len(t_ms) / (float(tt.item()) * 1e-3) / 1e9
-        same = bool(torch.equal(tout.iterations, out.iterations) and torch.equal(tout.hard_bits, out.hard_bits))
-        twoscan = {"value": ts_val, "unit": UNIT, "ms_per_step": float(tt.item()) / len(t_ms),
-                   "edge_updates_per_s": eu_per_step * len(t_ms) / (float(tt.item()) * 1e-3),
-                   "singlescan_over_twoscan": value / ts_val if ts_val else None,
-                   "same_hard_bits_and_iterations": same,
-                   "paper_claim": "single-scan more than twice as fast as two-scan min-sum (PAPER.md P:29-30)"}
-        del tout
+        v = info_bits_per_step * len(t_ms) / (float(tt.item()) * 1e-3) / 1e9
+        its = float(so.iterations.double().mean().item())
+        return {"value": v, "unit": UNIT, "ms_per_step": float(tt.item()) / len(t_ms),
+                "edge_updates_per_s": its * F * world * code.n_edges * len(t_ms) / (float(tt.item()) * 1e-3),
+                "mean_iterations": its, "frames_converged": int(so.syndrome_ok.sum().item()),
+                "singlescan_over_this": value / v if v else None}
+
+    twoscan = layered = None
+    if not args.no_twoscan:
+        twoscan = time_schedule(P.LDPC_SCHED_TWOSCAN)
+        twoscan["paper_claim"] = "single-scan more than twice as fast as two-scan min-sum (PAPER.md P:29-30)"
+    if not args.no_layered:
+        layered = time_schedule(P.LDPC_SCHED_LAYERED)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -352,7 +362,7 @@ def main():
                            "code_sha256": code.sha256()[:16]},
                 "errors": {"bit_errors": c[0], "frame_errors": c[1], "undetected": c[2], "not_converged": c[3],
                            "mean_iterations": sum_iters / (F * world)},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_twoscan": twoscan,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_twoscan": twoscan, "gpu_layered": layered,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -100,8 +100,18 @@ enum { LDPC_MSG_COMPACT = 0, LDPC_MSG_1BIT = 1 };
  *               addressings.  Same outputs as SINGLESCAN (bit-exact for
  *               integer LLRs); requires msg_format COMPACT, row degree <= 8 and
  *               column degree <= 16 (else LDPC_ERR_UNSUPPORTED).  A baseline, not a
- *               fast path: it always uses the streaming (HBM) layout. */
-enum { LDPC_SCHED_SINGLESCAN = 0, LDPC_SCHED_TWOSCAN = 1 };
+ *               fast path: it always uses the streaming (HBM) layout.
+ *   LAYERED   : the Eq.(3) block with ONE in-place posterior array (the paper stores
+ *               "Z_n, which are of N items"): rows are processed in ascending
+ *               m and row m replaces its old message in the current posterior,
+ *               Z_n <- (Z_n - L^(k-1)_mn) + L^(k)_mn, so it sees the updates of the rows
+ *               before it (layered / Gauss-Seidel schedule, reading D25).  Not
+ *               equivalent to two-scan; usually converges in fewer iterations.  The row
+ *               order of H defines the schedule (QC codes: base row by base row).
+ *               Requires the resident kernel (a frame pair's N posteriors in shared
+ *               memory, e.g. N <= ~27000) and at most 256 consecutive variable-disjoint
+ *               rows per batch, else LDPC_ERR_UNSUPPORTED. */
+enum { LDPC_SCHED_SINGLESCAN = 0, LDPC_SCHED_TWOSCAN = 1, LDPC_SCHED_LAYERED = 2 };
 
 typedef struct {
     int32_t max_iter;      /* >= 1: the iteration cap of P:174-175 */
@@ -119,7 +129,7 @@ typedef struct {
                               Q <= 127 (ONEBIT), else LDPC_ERR_UNSUPPORTED.  Ignored for F32. */
     int32_t llr_type;      /* LDPC_LLR_I16 | LDPC_LLR_I8 | LDPC_LLR_F32 */
     int32_t msg_format;    /* LDPC_MSG_COMPACT | LDPC_MSG_1BIT (1BIT requires integer LLRs) */
-    int32_t schedule;      /* LDPC_SCHED_SINGLESCAN (0, default) | LDPC_SCHED_TWOSCAN */
+    int32_t schedule;      /* LDPC_SCHED_SINGLESCAN (0, default) | _TWOSCAN | _LAYERED */
 } ldpc_decode_params;
 
 /* Device workspace bytes needed by ldpc_decode_batch for n_frames frames. */

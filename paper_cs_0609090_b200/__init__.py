@@ -22,7 +22,7 @@ LDPC_OK, LDPC_ERR_INVALID_ARG, LDPC_ERR_INVALID_CODE, LDPC_ERR_UNSUPPORTED, LDPC
 LDPC_LLR_I16, LDPC_LLR_I8, LDPC_LLR_F32 = 0, 1, 2
 LDPC_MINSUM_OFFSET, LDPC_MINSUM_NORMALIZED = 0, 1
 LDPC_MSG_COMPACT, LDPC_MSG_1BIT = 0, 1
-LDPC_SCHED_SINGLESCAN, LDPC_SCHED_TWOSCAN = 0, 1
+LDPC_SCHED_SINGLESCAN, LDPC_SCHED_TWOSCAN, LDPC_SCHED_LAYERED = 0, 1, 2
 
 # every symbol include/ldpc.h declares
 EXPORTS = [

@@ -60,7 +60,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 // ------------------------------------------------------------ one check row
-template <int DC, bool QC, bool ES>
+// LAY = false: flooding (Z^(k-1) read from Lpb, Z^(k) accumulated in Lab).
+// LAY = true : layered / in-place (reading D25): one array, Z_n <- (Z_n - L_old) + L_new.
+template <int DC, bool QC, bool ES, bool LAY>
 __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const char *Lpb, char *Lab, int e0,
                                         uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
     // shared-memory byte addresses of the row's variables in both buffers:
@@ -95,26 +97,32 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
     }
     uint32_t rn[DC];
     new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.rk);
+    if (LAY) {
 #pragma unroll
-    for (int j = 0; j < DC; ++j) {                           // Z^(k)_n += L^(k)_mn
-        uint32_t v;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(oa[j]) : "memory");
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(oa[j]), "r"(vadd(v, rn[j])) : "memory");
+        for (int j = 0; j < DC; ++j)                          // Z_n = (Z_n - L^(k-1)_mn) + L^(k)_mn
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(op[j]), "r"(vadd(q[j], rn[j])) : "memory");
+    } else {
+#pragma unroll
+        for (int j = 0; j < DC; ++j) {                       // Z^(k)_n += L^(k)_mn
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(oa[j]) : "memory");
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(oa[j]), "r"(vadd(v, rn[j])) : "memory");
+        }
     }
 }
 
-template <bool QC, bool ES>
+template <bool QC, bool ES, bool LAY>
 __device__ __forceinline__ void res_dispatch(int dc, const ResArgs &a, const QcTab &t, const char *Lpb, char *Lab,
                                              int e0, uint32_t r4, int p, bool first_iter, RowState &st,
                                              uint32_t &synd) {
     switch (dc) {
-    case 2: res_row<2, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 3: res_row<3, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 4: res_row<4, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 5: res_row<5, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 6: res_row<6, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 7: res_row<7, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 8: res_row<8, QC, ES>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 2: res_row<2, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 3: res_row<3, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 4: res_row<4, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 5: res_row<5, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 6: res_row<6, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 7: res_row<7, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 8: res_row<8, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
     }
 }
 
@@ -210,7 +218,7 @@ __device__ __forceinline__ void state_tmem_store(uint32_t tw, int b, int nb, con
 
 // Consecutive super-batches in which this group's rows have the same degree DC are
 // processed by one loop (one dispatch per run instead of per batch).
-template <int DC, bool ES, int FMT>
+template <int DC, bool ES, int FMT, bool LAY>
 __device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, uint32_t tw, int nb,
                                       int rloc, uint32_t r4, const char *Lpb, char *Lab, bool first_iter,
                                       uint32_t &synd) {
@@ -219,7 +227,7 @@ __device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, 
         RowState st = {0u, 0u, 0u};
         if constexpr (DC > 0) {
             if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-            if (rloc < a.Z) res_row<DC, true, ES>(a, t, Lpb, Lab, t.e0[b][g], r4, 0, first_iter, st, synd);
+            if (rloc < a.Z) res_row<DC, true, ES, LAY>(a, t, Lpb, Lab, t.e0[b][g], r4, 0, first_iter, st, synd);
             state_tmem_store<FMT>(tw, b, nb, st);
         }
         __syncthreads();                         // batch b's accumulations complete
@@ -227,34 +235,58 @@ __device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, 
     return b;
 }
 
-template <bool ES, int FMT>
+template <bool ES, int FMT, bool LAY>
 __device__ __forceinline__ int qc_run_dispatch(int dc, int b, int bend, int g, const ResArgs &a, const QcTab &t,
                                                uint32_t tw, int nb, int rloc, uint32_t r4, const char *Lpb, char *Lab,
                                                bool first_iter, uint32_t &synd) {
     switch (dc) {
-    case 2: return qc_run<2, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 3: return qc_run<3, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 4: return qc_run<4, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 5: return qc_run<5, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 6: return qc_run<6, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 7: return qc_run<7, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 8: return qc_run<8, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    default: return qc_run<0, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 2: return qc_run<2, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 3: return qc_run<3, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 4: return qc_run<4, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 5: return qc_run<5, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 6: return qc_run<6, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 7: return qc_run<7, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 8: return qc_run<8, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    default: return qc_run<0, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
     }
 }
 
-template <bool QC, bool ES, int FMT, typename TIN>
+// Parity of every row of this thread against the posterior array Lpb (bit 15 / 31 set
+// iff some row of the lo / hi frame is unsatisfied): H x̂ = 0 test of P:174.
+template <bool QC>
+__device__ __forceinline__ uint32_t parity_pass(const ResArgs &a, const QcTab &t, const char *Lpb, int nb, int grp,
+                                                int rloc, uint32_t r4, int tid) {
+    uint32_t synd = 0;
+    for (int b = 0; b < nb; ++b) {
+        if (QC) {
+            const int dc = t.dc[b][grp];
+            if (rloc < a.Z && dc) synd |= res_parity_dispatch<QC>(dc, a, t, Lpb, t.e0[b][grp], r4, 0);
+        } else {
+            const int p = a.bptr[b] + tid;
+            if (p < a.bptr[b + 1]) synd |= res_parity_dispatch<QC>(a.dcT[p], a, t, Lpb, 0, 0, p);
+        }
+    }
+    return synd;
+}
+
+// LAY = false: flooding schedule (the paper's Eq.(3) with Z^(k-1) / Z^(k) double
+// buffer, reading D7).  LAY = true: layered schedule (one in-place posterior array,
+// rows in ascending m, reading D25): the batches then hold consecutive variable-
+// disjoint rows (QC: consecutive base rows), so processing a batch in parallel is the
+// same as processing its rows one after the other.
+template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
 __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __grid_constant__ QcTab t) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint32_t tslot;
     __shared__ __align__(8) uint64_t zbar;
-    uint32_t *buf0 = smem, *buf1 = smem + a.Np;
+    uint32_t *buf0 = smem, *buf1 = LAY ? smem : smem + a.Np;
+    uint32_t *sst = smem + a.Np;                 // layered, non-QC: compact state [3][M] (see below)
     const int tid = threadIdx.x, nth = blockDim.x;
     const int grp = QC ? (a.group_threads == 128 ? (tid >> 7) : 0) : tid >> 7;
     const int rloc = QC ? tid - grp * a.group_threads : tid;
     const uint32_t r4 = 4u * (uint32_t)rloc;
     const int nb = QC ? t.nsb : a.nbatch;
-    if (tid == 0) mbar_init(&zbar, 1);
+    if (!LAY && tid == 0) mbar_init(&zbar, 1);
     const uint32_t tbase = tmem_alloc_cta(&tslot, a.tmem_cols);   // includes a block barrier
     // TMEM lanes are per warp quadrant (warp % 4): threads 128..255 use a second column range
     const uint32_t tw = tmem_warp_base(tbase) + (uint32_t)((tid >> 7) * a.cols_per_group);
@@ -268,7 +300,7 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
         const bool hi_valid = f1 < a.nframes;
         __syncthreads();                             // previous pair's outputs read the buffers
         // ingest: saturate to +-Q, double, pack the pair; Z^(0) -> slot, Z^(0) buffer and
-        // the first accumulator
+        // the first accumulator (layered: the one posterior array)
         for (int n = tid; n < a.Np; n += nth) {
             uint32_t v = 0;
             if (n < a.N) {
@@ -276,42 +308,70 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
                 const int zh = hi_valid ? load_llr_sat(llr + (size_t)f1 * a.N + n, a.Qsat) : 0;
                 v = pack2(2 * zl, 2 * zh);
             }
-            __stcg(z0w + n, v);
+            if (!LAY) {
+                __stcg(z0w + n, v);
+                buf1[n] = v;
+            }
             buf0[n] = v;
-            buf1[n] = v;
         }
-        fence_proxy_async_all();                     // z0w (generic writes) is later read by TMA
+        if (!LAY) fence_proxy_async_all();           // z0w (generic writes) is later read by TMA
         __syncthreads();
         int done = hi_valid ? 0 : 2;
         bool finished = false;
         int k = 1;
         for (; k <= a.K; ++k) {
-            // buffers by iteration parity: Z^(k-1) in Lp, Z^(k) accumulates in La
+            // buffers by iteration parity: Z^(k-1) in Lp, Z^(k) accumulates in La (layered: same array)
             const char *Lpb = (const char *)(((k & 1) ? buf0 : buf1));
             char *Lab = (char *)(((k & 1) ? buf1 : buf0));
-            if (k > 1) { mbar_wait(&zbar, zphase); zphase ^= 1; }   // La = Z^(0) has landed
+            if (!LAY && k > 1) { mbar_wait(&zbar, zphase); zphase ^= 1; }   // La = Z^(0) has landed
             uint32_t synd = 0;
             const bool first_iter = (k == 1);
+            if (LAY && ES) {
+                // syndrome of the posterior after iteration k-1, before this iteration
+                // changes it in place
+                synd = parity_pass<QC>(a, t, Lpb, nb, grp, rloc, r4, tid);
+                const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
+                const int fail_hi = __syncthreads_or((synd & 0x80000000u) != 0);
+                const int newly = ((fail_lo ? 0 : 1) | (fail_hi ? 0 : 2)) & ~done;
+                if (newly) {
+                    res_write_outputs(a, (const uint32_t *)Lpb, f0, newly, k - 1, 0, 0);
+                    done |= newly;
+                    __syncthreads();                 // outputs read the array before it changes
+                }
+                if (done == 3) { finished = true; break; }
+            }
+            constexpr bool RES = ES && !LAY;         // flooding: syndrome fused into the gather
             if (QC) {
                 // warp-uniform group branch: uniform table indices
 #pragma unroll 1
                 for (int b = 0; b < nb;) {
-                    if (grp == 0) b = qc_run_dispatch<ES, FMT>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-                    else b = qc_run_dispatch<ES, FMT>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+                    if (grp == 0) b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+                    else b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
                 }
             } else {
 #pragma unroll 1
                 for (int b = 0; b < nb; ++b) {
                     RowState st = {0u, 0u, 0u};
-                    if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
                     const int p = a.bptr[b] + tid;
-                    if (p < a.bptr[b + 1]) res_dispatch<QC, ES>(a.dcT[p], a, t, Lpb, Lab, 0, 0, p, first_iter, st, synd);
-                    state_tmem_store<FMT>(tw, b, nb, st);
+                    const bool valid = p < a.bptr[b + 1];
+                    if (LAY) {
+                        // layered general codes: batches can be single rows (e.g. a staircase),
+                        // so the state lives in shared memory indexed by row, [3][M] words
+                        if (!first_iter && valid) { st.A = sst[p]; st.B = sst[a.M + p]; st.W = sst[2 * a.M + p]; }
+                    } else if (!first_iter) {
+                        state_tmem_load<FMT>(tw, b, nb, st);
+                    }
+                    if (valid) res_dispatch<QC, RES, LAY>(a.dcT[p], a, t, Lpb, Lab, 0, 0, p, first_iter, st, synd);
+                    if (LAY) {
+                        if (valid) { sst[p] = st.A; sst[a.M + p] = st.B; sst[2 * a.M + p] = st.W; }
+                    } else {
+                        state_tmem_store<FMT>(tw, b, nb, st);
+                    }
                     __syncthreads();                     // batch b's accumulations complete
                 }
             }
             tmem_wait_st();
-            if (ES) {
+            if (RES) {
                 // syndrome of Z^(k-1), gathered during this scan (1-iteration lag)
                 const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
                 const int fail_hi = __syncthreads_or((synd & 0x80000000u) != 0);
@@ -323,7 +383,7 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
                 }
                 if (done == 3) { finished = true; break; }
             }
-            if (k < a.K) {
+            if (!LAY && k < a.K) {
                 // restart the next accumulator (the buffer just read) from Z^(0) by TMA
                 fence_proxy_async_smem();
                 __syncthreads();
@@ -333,16 +393,7 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
         if (!finished) {
             // final syndrome of Z^(K)
             const char *Lpb = (const char *)(((a.K + 1) & 1) ? buf0 : buf1);
-            uint32_t synd = 0;
-            for (int b = 0; b < nb; ++b) {
-                if (QC) {
-                    const int dc = t.dc[b][grp];
-                    if (rloc < a.Z && dc) synd |= res_parity_dispatch<QC>(dc, a, t, Lpb, t.e0[b][grp], r4, 0);
-                } else {
-                    const int p = a.bptr[b] + tid;
-                    if (p < a.bptr[b + 1]) synd |= res_parity_dispatch<QC>(a.dcT[p], a, t, Lpb, 0, 0, p);
-                }
-            }
+            const uint32_t synd = parity_pass<QC>(a, t, Lpb, nb, grp, rloc, r4, tid);
             const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
             const int fail_hi = __syncthreads_or((synd & 0x80000000u) != 0);
             const int which = 3 & ~done;

@@ -6,11 +6,12 @@
 
 namespace ldpc {
 
-// Resident kernel (k_resident.cuh).  i8 selects int8 channel LLRs (else int16).
-cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, size_t dyn_smem, size_t smem_per_sm, int threads,
-                          int *blocks);
-cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, int grid, int threads, size_t dyn_smem, const ResArgs &a,
-                       const QcTab &t, cudaStream_t s);
+// Resident kernel (k_resident.cuh).  i8 selects int8 channel LLRs (else int16); lay the
+// layered (in-place) schedule instead of flooding.
+cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, bool lay, size_t dyn_smem, size_t smem_per_sm,
+                          int threads, int *blocks);
+cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, bool lay, int grid, int threads, size_t dyn_smem,
+                       const ResArgs &a, const QcTab &t, cudaStream_t s);
 
 // Streaming kernels (k_stream.cuh, k_stream_pipe.cuh): every launch of one decode.
 struct StreamRun {

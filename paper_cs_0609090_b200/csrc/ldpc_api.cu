@@ -80,6 +80,12 @@ struct ldpc_code {
     int32_t *d_bptr = nullptr;
     uint32_t *d_colT = nullptr;
     uint8_t *d_dcT = nullptr;
+    // layered schedule (reading D25): batches of CONSECUTIVE variable-disjoint rows
+    int nbatch_lay = 0, res_threads_lay = 0;
+    QcTab *qtab_lay = nullptr;
+    int32_t *d_bptr_lay = nullptr;
+    uint32_t *d_colT_lay = nullptr;
+    uint8_t *d_dcT_lay = nullptr;
     cudaStream_t aux[2] = {nullptr, nullptr};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
@@ -156,6 +162,10 @@ static void free_code(ldpc_code *c) {
     cudaFree(c->d_bptr);
     cudaFree(c->d_colT);
     cudaFree(c->d_dcT);
+    delete c->qtab_lay;
+    cudaFree(c->d_bptr_lay);
+    cudaFree(c->d_colT_lay);
+    cudaFree(c->d_dcT_lay);
     for (auto &s : c->aux)
         if (s) cudaStreamDestroy(s);
     for (auto &e : c->ev)
@@ -310,6 +320,36 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
             c->nbatch = t.nsb;
             c->group_threads = groups == 2 ? 128 : ((c->Z + 31) / 32) * 32;
             c->res_threads = groups * c->group_threads;
+            // layered: base rows in their natural order; consecutive base rows i, i+1 with
+            // disjoint column blocks share a super-batch (same result as i then i+1)
+            {
+                c->qtab_lay = new QcTab(t);
+                QcTab &u = *c->qtab_lay;
+                auto disjoint = [&](int x, int y) {
+                    for (int a : cols[x])
+                        for (int b : cols[y])
+                            if (a == b) return false;
+                    return true;
+                };
+                int nsb = 0;
+                for (int i = 0; i < c->mb;) {
+                    const int j = (groups == 2 && i + 1 < c->mb && disjoint(i, i + 1)) ? i + 1 : -1;
+                    const int rows[2] = {i, j};
+                    for (int g = 0; g < kQcGroups; ++g) {
+                        const int r = rows[g];
+                        u.e0[nsb][g] = r >= 0 ? rstart[r] : 0;
+                        u.dc[nsb][g] = r >= 0 ? (int)cols[r].size() : 0;
+                    }
+                    ++nsb;
+                    i += j >= 0 ? 2 : 1;
+                }
+                u.nsb = nsb;
+                for (int g = 0; g < kQcGroups; ++g)
+                    for (int b = u.nsb - 1; b >= 0; --b)
+                        u.run_end[b][g] = (b + 1 < u.nsb && u.dc[b + 1][g] == u.dc[b][g]) ? u.run_end[b + 1][g] : b + 1;
+                c->nbatch_lay = nsb;
+                c->res_threads_lay = c->res_threads;
+            }
         } else {
             // greedy colouring: rows of one colour share no variable
             std::vector<std::vector<int>> classes;
@@ -358,6 +398,39 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                 free_code(c);
                 return st;
             }
+            // layered: maximal runs of consecutive, pairwise variable-disjoint rows in
+            // ascending m (<= 256 rows), so a batch in parallel == its rows in order
+            {
+                std::vector<int32_t> lptr(1, 0);
+                std::vector<uint32_t> lcol((size_t)kMaxDC * M, 0u);
+                std::vector<uint8_t> ldc(M);
+                std::vector<int> stamp(N, -1);
+                int maxl = 0, cur = 0;
+                for (int m = 0; m < M; ++m) {
+                    bool clash = cur >= 256;
+                    for (int32_t e = desc->row_ptr[m]; e < desc->row_ptr[m + 1] && !clash; ++e)
+                        if (stamp[desc->col_idx[e]] == (int)lptr.size() - 1) clash = true;
+                    if (clash) {
+                        lptr.push_back(m);
+                        cur = 0;
+                    }
+                    for (int32_t e = desc->row_ptr[m]; e < desc->row_ptr[m + 1]; ++e) {
+                        stamp[desc->col_idx[e]] = (int)lptr.size() - 1;
+                        lcol[(size_t)(e - desc->row_ptr[m]) * M + m] = 4u * (uint32_t)desc->col_idx[e];
+                    }
+                    ldc[m] = (uint8_t)(desc->row_ptr[m + 1] - desc->row_ptr[m]);
+                    maxl = std::max(maxl, ++cur);
+                }
+                lptr.push_back(M);
+                c->nbatch_lay = (int)lptr.size() - 1;
+                c->res_threads_lay = ((maxl + 31) / 32) * 32;
+                if ((st = upload(&c->d_bptr_lay, lptr.data(), lptr.size())) != LDPC_OK ||
+                    (st = upload(&c->d_colT_lay, lcol.data(), lcol.size())) != LDPC_OK ||
+                    (st = upload(&c->d_dcT_lay, ldc.data(), ldc.size())) != LDPC_OK) {
+                    free_code(c);
+                    return st;
+                }
+            }
         }
         c->res_smem = (size_t)2 * (((size_t)N + 3) & ~(size_t)3) * 4;
         c->res_ok = c->res_smem <= c->smem_optin && c->res_threads <= 256;
@@ -404,6 +477,9 @@ struct Plan {
     int Q = 0, beta = 0, fmt = FMT_C16;
     float alpha = 1.f, betaf = 0.f;
     // resident
+    bool lay = false;            // layered schedule (LDPC_SCHED_LAYERED)
+    int threads = 0, nbatch = 0;
+    size_t smem = 0;
     int grid = 0;
     size_t slot_words = 0;
     uint32_t tmem_cols = 0;
@@ -415,9 +491,9 @@ struct Plan {
     size_t ws_bytes = 0;
 };
 
-cudaError_t res_occupancy_any(const ldpc_code *c, const ldpc_decode_params *p, int fmt, int *blocks) {
-    return res_occupancy(c->qc, p->early_stop != 0, fmt, p->llr_type == LDPC_LLR_I8, c->res_smem, c->smem_per_sm,
-                         c->res_threads, blocks);
+cudaError_t res_occupancy_any(const ldpc_code *c, const ldpc_decode_params *p, const struct Plan &pl, int *blocks) {
+    return res_occupancy(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.lay, pl.smem,
+                         c->smem_per_sm, pl.threads, blocks);
 }
 
 ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p, Plan &pl) {
@@ -427,7 +503,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (F > (int64_t)1 << 31) return fail(LDPC_ERR_UNSUPPORTED, "n_frames > 2^31");
     if (p->max_iter < 1) return fail(LDPC_ERR_INVALID_ARG, "max_iter must be >= 1");
     if (p->early_stop != 0 && p->early_stop != 1) return fail(LDPC_ERR_INVALID_ARG, "early_stop must be 0 or 1");
-    if (p->schedule != LDPC_SCHED_SINGLESCAN && p->schedule != LDPC_SCHED_TWOSCAN)
+    if (p->schedule != LDPC_SCHED_SINGLESCAN && p->schedule != LDPC_SCHED_TWOSCAN &&
+        p->schedule != LDPC_SCHED_LAYERED)
         return fail(LDPC_ERR_INVALID_ARG, "bad schedule %d", p->schedule);
     pl.sched = p->schedule;
     if (pl.sched == LDPC_SCHED_TWOSCAN) {
@@ -471,21 +548,41 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         const char *force = getenv("LDPC_FORCE_STREAM");
         pl.path = (c->res_ok && !(force && force[0] == '1') && pl.sched == LDPC_SCHED_SINGLESCAN) ? PATH_RESIDENT
                                                                                                    : PATH_STREAM_I;
+        if (pl.sched == LDPC_SCHED_LAYERED) {
+            if (!c->res_ok)
+                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule needs a code whose posteriors fit in shared memory "
+                                                  "(the resident kernel); N=%d is too long", c->N);
+            if (c->res_threads_lay > 256)
+                return fail(LDPC_ERR_UNSUPPORTED, "layered batches wider than 256 rows");
+            pl.path = PATH_RESIDENT;
+            pl.lay = true;
+        }
         pl.tile = 64;
     } else {
         return fail(LDPC_ERR_INVALID_ARG, "bad llr_type %d", p->llr_type);
     }
     const int64_t npairs = (F + 1) / 2;
     if (pl.path == PATH_RESIDENT) {
-        // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group
-        pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * c->nbatch;
-        const int groups = (c->res_threads + 127) / 128;   // 128-thread TMEM lane slices
+        pl.threads = pl.lay ? c->res_threads_lay : c->res_threads;
+        pl.nbatch = pl.lay ? c->nbatch_lay : c->nbatch;
+        pl.smem = pl.lay ? c->res_smem / 2 : c->res_smem;   // layered: one posterior array
+        // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group; layered
+        // general codes keep the state in shared memory instead ([3][M] words, by row)
+        pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * pl.nbatch;
+        if (pl.lay && !c->qc) {
+            pl.cols_per_group = 0;
+            pl.smem += (size_t)3 * c->M * 4;
+            if (pl.smem > c->smem_optin)
+                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule: posteriors + state (%zu B) exceed shared memory",
+                            pl.smem);
+        }
+        const int groups = (pl.threads + 127) / 128;   // 128-thread TMEM lane slices
         uint32_t need = (uint32_t)(pl.cols_per_group * groups), cols = 32;
         while (cols < need) cols <<= 1;
         if (cols > 512) return fail(LDPC_ERR_UNSUPPORTED, "compact state needs %u TMEM columns (> 512)", need);
         pl.tmem_cols = cols;
         int blocks = 0;
-        cudaError_t e = res_occupancy_any(c, p, pl.fmt, &blocks);
+        cudaError_t e = res_occupancy_any(c, p, pl, &blocks);
         if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "occupancy query: %s", cudaGetErrorString(e));
         if (getenv("LDPC_DEBUG")) fprintf(stderr, "[ldpc] occupancy API: %d blocks/SM\n", blocks);
         blocks = std::min(blocks, (int)(512 / cols));     // TMEM capacity per SM
@@ -494,7 +591,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         pl.slot_words = ((size_t)c->N + 63) & ~(size_t)63;
         if (getenv("LDPC_DEBUG"))
             fprintf(stderr, "[ldpc] resident: threads=%d smem=%zu tmem_cols=%u need=%u occ_blocks=%d grid=%d batches=%d\n",
-                    c->res_threads, c->res_smem, cols, need, blocks, pl.grid, c->nbatch);
+                    pl.threads, pl.smem, cols, need, blocks, pl.grid, pl.nbatch);
         pl.ws_bytes = align256((size_t)pl.grid * pl.slot_words * 4);
     } else {
         pl.ntiles = (int)((F + pl.tile - 1) / pl.tile);
@@ -540,18 +637,19 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.iters = it;
     a.ws = (uint32_t *)ws;
     a.slot_words = pl.slot_words;
-    a.nbatch = c->nbatch;
-    a.bptr = c->d_bptr;
-    a.colT = c->d_colT;
-    a.dcT = c->d_dcT;
+    a.nbatch = pl.nbatch;
+    a.bptr = pl.lay ? c->d_bptr_lay : c->d_bptr;
+    a.colT = pl.lay ? c->d_colT_lay : c->d_colT;
+    a.dcT = pl.lay ? c->d_dcT_lay : c->d_dcT;
     a.Z = c->Z;
     a.group_threads = c->group_threads;
     a.tmem_cols = pl.tmem_cols;
     a.cols_per_group = pl.cols_per_group;
     a.rk = make_regk();
     static const QcTab empty_tab{};
-    cudaError_t e = res_launch(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.grid, c->res_threads,
-                               c->res_smem, a, c->qtab ? *c->qtab : empty_tab, s);
+    const QcTab *qt = pl.lay ? c->qtab_lay : c->qtab;
+    cudaError_t e = res_launch(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.lay, pl.grid,
+                               pl.threads, pl.smem, a, qt ? *qt : empty_tab, s);
     ++g_launches;
     return e;
 }

@@ -7,12 +7,12 @@
 namespace ldpc {
 namespace {
 
-template <bool QC, bool ES, int FMT, typename TIN>
+template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
 cudaError_t occ(size_t dyn_smem, size_t smem_per_sm, int threads, int *blocks) {
     // The occupancy API reports 1 block/SM for kernels that allocate TMEM; compute the
     // limit from the kernel's registers, shared memory and threads instead (TMEM is
     // accounted for by the caller).
-    auto kern = k_resident<QC, ES, FMT, TIN>;
+    auto kern = k_resident<QC, ES, FMT, TIN, LAY>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
     if (e != cudaSuccess) return e;
     cudaFuncAttributes fa;
@@ -26,9 +26,9 @@ cudaError_t occ(size_t dyn_smem, size_t smem_per_sm, int threads, int *blocks) {
     return cudaSuccess;
 }
 
-template <bool QC, bool ES, int FMT, typename TIN>
+template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
 cudaError_t launch(int grid, int threads, size_t dyn_smem, const ResArgs &a, const QcTab &t, cudaStream_t s) {
-    auto kern = k_resident<QC, ES, FMT, TIN>;
+    auto kern = k_resident<QC, ES, FMT, TIN, LAY>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, threads, dyn_smem, s>>>(a, t);
@@ -36,11 +36,13 @@ cudaError_t launch(int grid, int threads, size_t dyn_smem, const ResArgs &a, con
 }
 
 // dispatch over the template parameters; F is called with a pointer-to-instantiation tag
-template <template <bool, bool, int, typename> class K, typename... Args>
-cudaError_t dispatch(bool qc, bool es, int fmt, bool i8, Args... args) {
-#define LDPC_RES_CASE(Q, E, F)                                                              \
-    if (qc == Q && es == E && fmt == F)                                                     \
-        return i8 ? K<Q, E, F, int8_t>::run(args...) : K<Q, E, F, int16_t>::run(args...);
+template <template <bool, bool, int, typename, bool> class K, typename... Args>
+cudaError_t dispatch(bool qc, bool es, int fmt, bool i8, bool lay, Args... args) {
+#define LDPC_RES_CASE(Q, E, F)                                                                          \
+    if (qc == Q && es == E && fmt == F) {                                                               \
+        if (lay) return i8 ? K<Q, E, F, int8_t, true>::run(args...) : K<Q, E, F, int16_t, true>::run(args...); \
+        return i8 ? K<Q, E, F, int8_t, false>::run(args...) : K<Q, E, F, int16_t, false>::run(args...);       \
+    }
     LDPC_RES_CASE(true, true, FMT_C16) LDPC_RES_CASE(true, true, FMT_1BIT)
     LDPC_RES_CASE(true, false, FMT_C16) LDPC_RES_CASE(true, false, FMT_1BIT)
     LDPC_RES_CASE(false, true, FMT_C16) LDPC_RES_CASE(false, true, FMT_1BIT)
@@ -49,27 +51,27 @@ cudaError_t dispatch(bool qc, bool es, int fmt, bool i8, Args... args) {
     return cudaErrorInvalidValue;
 }
 
-template <bool QC, bool ES, int FMT, typename TIN>
+template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
 struct Occ {
-    static cudaError_t run(size_t d, size_t sps, int th, int *b) { return occ<QC, ES, FMT, TIN>(d, sps, th, b); }
+    static cudaError_t run(size_t d, size_t sps, int th, int *b) { return occ<QC, ES, FMT, TIN, LAY>(d, sps, th, b); }
 };
-template <bool QC, bool ES, int FMT, typename TIN>
+template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
 struct Launch {
     static cudaError_t run(int g, int th, size_t d, const ResArgs *a, const QcTab *t, cudaStream_t s) {
-        return launch<QC, ES, FMT, TIN>(g, th, d, *a, *t, s);
+        return launch<QC, ES, FMT, TIN, LAY>(g, th, d, *a, *t, s);
     }
 };
 
 }  // namespace
 
-cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, size_t dyn_smem, size_t smem_per_sm, int threads,
-                          int *blocks) {
-    return dispatch<Occ>(qc, es, fmt, i8, dyn_smem, smem_per_sm, threads, blocks);
+cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, bool lay, size_t dyn_smem, size_t smem_per_sm,
+                          int threads, int *blocks) {
+    return dispatch<Occ>(qc, es, fmt, i8, lay, dyn_smem, smem_per_sm, threads, blocks);
 }
 
-cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, int grid, int threads, size_t dyn_smem, const ResArgs &a,
-                       const QcTab &t, cudaStream_t s) {
-    return dispatch<Launch>(qc, es, fmt, i8, grid, threads, dyn_smem, &a, &t, s);
+cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, bool lay, int grid, int threads, size_t dyn_smem,
+                       const ResArgs &a, const QcTab &t, cudaStream_t s) {
+    return dispatch<Launch>(qc, es, fmt, i8, lay, grid, threads, dyn_smem, &a, &t, s);
 }
 
 }  // namespace ldpc

@@ -43,6 +43,7 @@ struct ResArgs {
     uint32_t tmem_cols;               // TMEM columns allocated per CTA
     int cols_per_group;               // TMEM columns used by one group of threads
     RegK rk;                          // register constants (simd16.cuh)
+    uint32_t cpar;                    // row_parity constant (-(0x00010001), biased: -(0x40014001))
 };
 
 struct StreamArgs {

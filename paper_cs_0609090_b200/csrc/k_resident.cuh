@@ -142,7 +142,7 @@ __device__ __forceinline__ uint32_t res_parity(const ResArgs &a, const QcTab &t,
         }
         L[j] = *(const uint32_t *)(Lpb + off);
     }
-    return row_parity<DC>(L, a.rk);
+    return row_parity<DC>(L, a.rk, a.cpar);
 }
 
 template <bool QC>
@@ -161,24 +161,24 @@ __device__ __forceinline__ uint32_t res_parity_dispatch(int dc, const ResArgs &a
 }
 
 // Write outputs of the frames selected by `which` (bit0 = lo frame, bit1 = hi frame)
-// from the doubled posterior buffer Lsrc.
+// from the doubled posterior buffer Lsrc (each 16-bit lane holds 2 Z_n + bias).
 __device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc, int f0, int which, int iters,
-                                  int fail_lo, int fail_hi) {
+                                  int fail_lo, int fail_hi, int bias = 0) {
     const int f1 = f0 + 1;
     const int tid = threadIdx.x, nth = blockDim.x;
     if (a.post) {
         for (int n = tid; n < a.N; n += nth) {
             const uint32_t v = Lsrc[n];
-            if (which & 1) a.post[(size_t)f0 * a.N + n] = (int16_t)(lo16(v) >> 1);
-            if (which & 2) a.post[(size_t)f1 * a.N + n] = (int16_t)(hi16(v) >> 1);
+            if (which & 1) a.post[(size_t)f0 * a.N + n] = (int16_t)((lo16(v) - bias) >> 1);
+            if (which & 2) a.post[(size_t)f1 * a.N + n] = (int16_t)((hi16(v) - bias) >> 1);
         }
     }
     const int lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
     for (int w = warp; w < a.wpf; w += nw) {
         const int n = w * 32 + lane;
-        const uint32_t v = n < a.N ? Lsrc[n] : 0x00020002u;
-        const uint32_t blo = __ballot_sync(0xFFFFFFFFu, lo16(v) <= 0);
-        const uint32_t bhi = __ballot_sync(0xFFFFFFFFu, hi16(v) <= 0);
+        const uint32_t v = n < a.N ? Lsrc[n] : pack2(bias + 2, bias + 2);
+        const uint32_t blo = __ballot_sync(0xFFFFFFFFu, lo16(v) - bias <= 0);
+        const uint32_t bhi = __ballot_sync(0xFFFFFFFFu, hi16(v) - bias <= 0);
         if (lane == 0) {
             if (which & 1) a.hard_bits[(size_t)f0 * a.wpf + w] = blo;
             if (which & 2) a.hard_bits[(size_t)f1 * a.wpf + w] = bhi;

@@ -1,0 +1,234 @@
+// k_resident_atom.cuh -- barrier-free decode-resident single-scan min-sum kernel
+// (flooding schedule, integer LLRs).  Same residency as k_resident.cuh -- one CTA per
+// frame pair, posterior double buffer in shared memory, compact state in TMEM, Z^(0)
+// restarted by a TMA bulk copy -- but the accumulation Z^(k)_n += L^(k)_mn is
+// a shared-memory atomic add (RED.ADD on 32-bit words), so rows need no conflict-free
+// batching and there is no barrier inside an iteration: every thread runs through its
+// own rows back to back.
+//
+// Exactness of a 32-bit add on two 16-bit lanes: every posterior word holds
+// 2 Z_n + 0x4000 in each lane (BIAS).  |2 Z_n| <= 2 Q (dv + 1) < 0x4000 (checked by the
+// planner), and so does every partial sum in any order, so both lanes stay in
+// [0, 0x8000): non-negative lanes never carry or borrow across the lane boundary.  The
+// message is added in "V form" (hi * 65536 + lo as a signed 32-bit integer), which is
+// exactly the lane-wise add.  Gathers read the biased words directly; the bias is
+// folded into the rebuilt previous message (rowcore.cuh rebuild_q<BIASED>) and the
+// syndrome constant, so q_mn comes out unbiased with no extra work per edge.
+//
+// Row ownership: QC codes -- thread r of group g owns circulant row r of the base rows
+// listed for group g (QcTab slots b; the two groups get base-row lists of equal total
+// degree); other codes -- thread t owns rows t, t + T, t + 2T, ...  The TMEM column of
+// a row's state is its slot b.
+#pragma once
+#include "k_resident.cuh"
+
+namespace ldpc {
+
+constexpr int kAtomBias = 0x4000;
+
+template <int DC, bool QC, bool ES>
+__device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, uint32_t bp, uint32_t ba, int e0,
+                                         uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
+    uint32_t d[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        if (QC) {
+            const uint2 e = t.ent[e0 + j];
+            const uint32_t u = r4 + e.x;
+            d[j] = min(u - t.Z4, u) + e.y;                 // 4 * (jZ + (r + s) mod Z)
+        } else {
+            d[j] = __ldg(a.colT + (size_t)j * a.M + p);
+        }
+    }
+    uint32_t L[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
+    if (ES) synd |= row_parity<DC>(L, a.rk, a.cpar);
+    uint32_t q[DC];
+    if (first_iter) {
+#pragma unroll
+        for (int j = 0; j < DC; ++j) q[j] = __vadd2(L[j], 0xC000C000u);   // L^(0)_mn = 0
+    } else {
+        rebuild_q<DC, true>(L, st, q, a.rk);                               // Z_n - L^(k-1)_mn
+    }
+    uint32_t rn[DC];
+    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.rk);
+#pragma unroll
+    for (int j = 0; j < DC; ++j)                                          // Z^(k)_n += L^(k)_mn
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(vform(rn[j], a.rk)) : "memory");
+}
+
+template <int DC, bool ES, int FMT>
+__device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, uint32_t tw,
+                                           int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba, bool first_iter,
+                                           uint32_t &synd) {
+    if constexpr (DC == 0) {
+        return bend;
+    } else {
+#pragma unroll 1
+        for (; b < bend; ++b) {
+            RowState st = {0u, 0u, 0u};
+            if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
+            if (rloc < a.Z) atom_row<DC, true, ES>(a, t, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
+            state_tmem_store<FMT>(tw, b, nb, st);
+        }
+        return b;
+    }
+}
+
+template <bool ES, int FMT>
+__device__ __forceinline__ int atom_qc_dispatch(int dc, int b, int bend, int g, const ResArgs &a, const QcTab &t,
+                                                uint32_t tw, int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba,
+                                                bool first_iter, uint32_t &synd) {
+    switch (dc) {
+    case 2: return atom_qc_run<2, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 3: return atom_qc_run<3, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 4: return atom_qc_run<4, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 5: return atom_qc_run<5, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 6: return atom_qc_run<6, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 7: return atom_qc_run<7, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 8: return atom_qc_run<8, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    default: return atom_qc_run<0, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    }
+}
+
+template <bool ES>
+__device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, const QcTab &t, uint32_t bp, uint32_t ba,
+                                                  int p, bool first_iter, RowState &st, uint32_t &synd) {
+    switch (dc) {
+    case 2: atom_row<2, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 3: atom_row<3, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 4: atom_row<4, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 5: atom_row<5, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 6: atom_row<6, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 7: atom_row<7, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 8: atom_row<8, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    }
+}
+
+// Ingest one frame pair: saturate to +-Q, double, bias, pack; write the Z^(0) slot (for
+// the TMA restarts) and both shared buffers.  Four variables per thread per step with
+// all eight loads issued first (the loads are latency-bound, not bandwidth-bound).
+template <typename TIN>
+__device__ __forceinline__ void atom_ingest(const ResArgs &a, const TIN *__restrict__ lo, const TIN *__restrict__ hi,
+                                            uint32_t *z0w, uint32_t *buf0, uint32_t *buf1) {
+    const int tid = threadIdx.x, nth = blockDim.x;
+    constexpr int U = 4;
+    for (int n0 = tid; n0 < a.Np; n0 += U * nth) {
+        int zl[U], zh[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int n = n0 + u * nth;
+            zl[u] = n < a.N ? (int)__ldg(lo + n) : 0;
+            zh[u] = (n < a.N && hi) ? (int)__ldg(hi + n) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int n = n0 + u * nth;
+            if (n < a.Np) {
+                const int l = max(-a.Qsat, min(a.Qsat, zl[u])), h = max(-a.Qsat, min(a.Qsat, zh[u]));
+                const uint32_t v = pack2(2 * l + kAtomBias, 2 * h + kAtomBias);
+                __stcg(z0w + n, v);
+                buf0[n] = v;
+                buf1[n] = v;
+            }
+        }
+    }
+}
+
+template <bool QC, bool ES, int FMT, typename TIN>
+__global__ void __launch_bounds__(256, 3) k_resident_atom(const ResArgs a, const __grid_constant__ QcTab t) {
+    extern __shared__ __align__(128) uint32_t smem[];
+    __shared__ uint32_t tslot;
+    __shared__ __align__(8) uint64_t zbar;
+    uint32_t *buf0 = smem, *buf1 = smem + a.Np;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int grp = QC ? (a.group_threads == 128 ? (tid >> 7) : 0) : 0;
+    const int rloc = QC ? tid - grp * a.group_threads : tid;
+    const uint32_t r4 = 4u * (uint32_t)rloc;
+    const int nb = QC ? t.nsb : a.nbatch;                // row slots per thread
+    if (tid == 0) mbar_init(&zbar, 1);
+    const uint32_t tbase = tmem_alloc_cta(&tslot, a.tmem_cols);   // includes a block barrier
+    const uint32_t tw = tmem_warp_base(tbase) + (uint32_t)((tid >> 7) * a.cols_per_group);
+    uint32_t *z0w = a.ws + (size_t)blockIdx.x * a.slot_words;
+    const TIN *llr = (const TIN *)a.llr;
+    const uint32_t zbytes = 4u * (uint32_t)a.Np;
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(buf0), s1 = (uint32_t)__cvta_generic_to_shared(buf1);
+    uint32_t zphase = 0;
+
+    for (int pair = blockIdx.x; pair < a.npairs; pair += gridDim.x) {
+        const int f0 = 2 * pair, f1 = f0 + 1;
+        const bool hi_valid = f1 < a.nframes;
+        __syncthreads();                             // previous pair's outputs read the buffers
+        atom_ingest<TIN>(a, llr + (size_t)f0 * a.N, hi_valid ? llr + (size_t)f1 * a.N : nullptr, z0w, buf0, buf1);
+        fence_proxy_async_all();                     // z0w (generic writes) is later read by TMA
+        __syncthreads();
+        int done = hi_valid ? 0 : 2;
+        bool finished = false;
+        for (int k = 1; k <= a.K; ++k) {
+            const uint32_t bp = (k & 1) ? s0 : s1, ba = (k & 1) ? s1 : s0;   // Z^(k-1) | Z^(k)
+            if (k > 1) { mbar_wait(&zbar, zphase); zphase ^= 1; }          // Z^(k) = Z^(0) landed
+            uint32_t synd = 0;
+            const bool first_iter = (k == 1);
+            if (QC) {
+#pragma unroll 1
+                for (int b = 0; b < nb;) {
+                    if (grp == 0) b = atom_qc_dispatch<ES, FMT>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+                    else b = atom_qc_dispatch<ES, FMT>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+                }
+            } else {
+#pragma unroll 1
+                for (int b = 0; b < nb; ++b) {
+                    RowState st = {0u, 0u, 0u};
+                    if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
+                    const int p = b * nth + tid;
+                    if (p < a.M) atom_csr_dispatch<ES>(a.dcT[p], a, t, bp, ba, p, first_iter, st, synd);
+                    state_tmem_store<FMT>(tw, b, nb, st);
+                }
+            }
+            tmem_wait_st();
+            const char *Lpb = (const char *)((k & 1) ? buf0 : buf1);
+            if (ES) {
+                // syndrome of Z^(k-1), gathered during this scan (1-iteration lag); the
+                // __syncthreads_or is also the end-of-iteration barrier
+                const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
+                const int fail_hi = __syncthreads_or((synd & 0x80000000u) != 0);
+                const int newly = ((fail_lo ? 0 : 1) | (fail_hi ? 0 : 2)) & ~done;
+                if (newly) {
+                    res_write_outputs(a, (const uint32_t *)Lpb, f0, newly, k - 1, 0, 0, kAtomBias);
+                    done |= newly;
+                }
+                if (done == 3) { finished = true; break; }
+            }
+            if (k < a.K) {
+                // restart the next accumulator (the buffer just read) from Z^(0) by TMA
+                fence_proxy_async_smem();
+                __syncthreads();
+                if (tid == 0) tma_bulk_g2s((void *)Lpb, z0w, zbytes, &zbar);
+            }
+        }
+        if (!finished) {
+            __syncthreads();                         // all atomics of iteration K landed
+            const char *Lpb = (const char *)(((a.K + 1) & 1) ? buf0 : buf1);
+            uint32_t synd = 0;
+            if (QC) {
+                for (int b = 0; b < nb; ++b) {
+                    const int dc = t.dc[b][grp];
+                    if (rloc < a.Z && dc) synd |= res_parity_dispatch<true>(dc, a, t, Lpb, t.e0[b][grp], r4, 0);
+                }
+            } else {
+                for (int b = 0; b < nb; ++b) {
+                    const int p = b * nth + tid;
+                    if (p < a.M) synd |= res_parity_dispatch<false>(a.dcT[p], a, t, Lpb, 0, 0, p);
+                }
+            }
+            const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
+            const int fail_hi = __syncthreads_or((synd & 0x80000000u) != 0);
+            const int which = 3 & ~done;
+            if (which) res_write_outputs(a, (const uint32_t *)Lpb, f0, which, a.K, fail_lo, fail_hi, kAtomBias);
+        }
+    }
+    tmem_free_cta(tbase, a.tmem_cols);
+}
+
+}  // namespace ldpc

@@ -6,11 +6,13 @@
 
 namespace ldpc {
 
-// Resident kernel (k_resident.cuh).  i8 selects int8 channel LLRs (else int16); lay the
-// layered (in-place) schedule instead of flooding.
-cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, bool lay, size_t dyn_smem, size_t smem_per_sm,
+// Resident kernels.  i8 selects int8 channel LLRs (else int16).  kind: RES_BATCHED
+// (k_resident.cuh, flooding in conflict-free batches), RES_LAYERED (k_resident.cuh,
+// in-place schedule), RES_ATOM (k_resident_atom.cuh, flooding with shared atomics).
+enum { RES_BATCHED = 0, RES_LAYERED = 1, RES_ATOM = 2 };
+cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,
                           int threads, int *blocks);
-cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, bool lay, int grid, int threads, size_t dyn_smem,
+cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,
                        const ResArgs &a, const QcTab &t, cudaStream_t s);
 
 // Streaming kernels (k_stream.cuh, k_stream_pipe.cuh): every launch of one decode.

@@ -86,6 +86,9 @@ struct ldpc_code {
     int32_t *d_bptr_lay = nullptr;
     uint32_t *d_colT_lay = nullptr;
     uint8_t *d_dcT_lay = nullptr;
+    // barrier-free flooding kernel (k_resident_atom.cuh): row slots per thread
+    int nbatch_atom = 0, res_threads_atom = 0;
+    QcTab *qtab_atom = nullptr;
     cudaStream_t aux[2] = {nullptr, nullptr};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
@@ -163,6 +166,7 @@ static void free_code(ldpc_code *c) {
     cudaFree(c->d_colT);
     cudaFree(c->d_dcT);
     delete c->qtab_lay;
+    delete c->qtab_atom;
     cudaFree(c->d_bptr_lay);
     cudaFree(c->d_colT_lay);
     cudaFree(c->d_dcT_lay);
@@ -350,6 +354,40 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                 c->nbatch_lay = nsb;
                 c->res_threads_lay = c->res_threads;
             }
+            // barrier-free flooding: each group owns a list of base rows (thread r = circulant
+            // row r); longest-processing-time assignment balances the groups' edge counts,
+            // each list sorted by degree so equal-degree rows form one dispatch run
+            {
+                c->qtab_atom = new QcTab(t);
+                QcTab &u = *c->qtab_atom;
+                std::vector<int> order(c->mb);
+                for (int i = 0; i < c->mb; ++i) order[i] = i;
+                std::stable_sort(order.begin(), order.end(),
+                                 [&](int x, int y) { return cols[x].size() > cols[y].size(); });
+                std::vector<std::vector<int>> lists(groups);
+                std::vector<size_t> load(groups, 0);
+                for (int i : order) {
+                    int gbest = 0;
+                    for (int gg = 1; gg < groups; ++gg)
+                        if (load[gg] < load[gbest]) gbest = gg;
+                    lists[gbest].push_back(i);
+                    load[gbest] += cols[i].size();
+                }
+                int nsb = 0;
+                for (auto &l : lists) nsb = std::max(nsb, (int)l.size());
+                for (int b = 0; b < nsb; ++b)
+                    for (int g = 0; g < kQcGroups; ++g) {
+                        const int r = (g < groups && b < (int)lists[g].size()) ? lists[g][b] : -1;
+                        u.e0[b][g] = r >= 0 ? rstart[r] : 0;
+                        u.dc[b][g] = r >= 0 ? (int)cols[r].size() : 0;
+                    }
+                u.nsb = nsb;
+                for (int g = 0; g < kQcGroups; ++g)
+                    for (int b = u.nsb - 1; b >= 0; --b)
+                        u.run_end[b][g] = (b + 1 < u.nsb && u.dc[b + 1][g] == u.dc[b][g]) ? u.run_end[b + 1][g] : b + 1;
+                c->nbatch_atom = nsb;
+                c->res_threads_atom = c->res_threads;
+            }
         } else {
             // greedy colouring: rows of one colour share no variable
             std::vector<std::vector<int>> classes;
@@ -424,6 +462,9 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                 lptr.push_back(M);
                 c->nbatch_lay = (int)lptr.size() - 1;
                 c->res_threads_lay = ((maxl + 31) / 32) * 32;
+                // barrier-free flooding: thread t owns rows t, t + T, ... (natural order tables)
+                c->res_threads_atom = std::min(256, ((M + 31) / 32) * 32);
+                c->nbatch_atom = (M + c->res_threads_atom - 1) / c->res_threads_atom;
                 if ((st = upload(&c->d_bptr_lay, lptr.data(), lptr.size())) != LDPC_OK ||
                     (st = upload(&c->d_colT_lay, lcol.data(), lcol.size())) != LDPC_OK ||
                     (st = upload(&c->d_dcT_lay, ldc.data(), ldc.size())) != LDPC_OK) {
@@ -478,6 +519,7 @@ struct Plan {
     float alpha = 1.f, betaf = 0.f;
     // resident
     bool lay = false;            // layered schedule (LDPC_SCHED_LAYERED)
+    int kind = RES_BATCHED;      // resident kernel variant (launch.h)
     int threads = 0, nbatch = 0;
     size_t smem = 0;
     int grid = 0;
@@ -492,7 +534,7 @@ struct Plan {
 };
 
 cudaError_t res_occupancy_any(const ldpc_code *c, const ldpc_decode_params *p, const struct Plan &pl, int *blocks) {
-    return res_occupancy(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.lay, pl.smem,
+    return res_occupancy(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.kind, pl.smem,
                          c->smem_per_sm, pl.threads, blocks);
 }
 
@@ -563,8 +605,14 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     }
     const int64_t npairs = (F + 1) / 2;
     if (pl.path == PATH_RESIDENT) {
-        pl.threads = pl.lay ? c->res_threads_lay : c->res_threads;
-        pl.nbatch = pl.lay ? c->nbatch_lay : c->nbatch;
+        // flooding uses the barrier-free atomic kernel when the biased 16-bit lanes cannot
+        // overflow: 2 Q (max_dv + 1) < 0x4000 (k_resident_atom.cuh); LDPC_RES_BATCHED=1
+        // selects the batched kernel
+        const char *be = getenv("LDPC_RES_BATCHED");
+        const bool atom_ok = (int64_t)2 * pl.Q * (c->max_dv + 1) < 0x4000 && c->nbatch_atom > 0;
+        pl.kind = pl.lay ? RES_LAYERED : ((atom_ok && !(be && be[0] == '1')) ? RES_ATOM : RES_BATCHED);
+        pl.threads = pl.lay ? c->res_threads_lay : (pl.kind == RES_ATOM ? c->res_threads_atom : c->res_threads);
+        pl.nbatch = pl.lay ? c->nbatch_lay : (pl.kind == RES_ATOM ? c->nbatch_atom : c->nbatch);
         pl.smem = pl.lay ? c->res_smem / 2 : c->res_smem;   // layered: one posterior array
         // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group; layered
         // general codes keep the state in shared memory instead ([3][M] words, by row)
@@ -638,17 +686,19 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.ws = (uint32_t *)ws;
     a.slot_words = pl.slot_words;
     a.nbatch = pl.nbatch;
+    const bool natural = pl.kind != RES_BATCHED;   // layered / atom: row tables in natural order
     a.bptr = pl.lay ? c->d_bptr_lay : c->d_bptr;
-    a.colT = pl.lay ? c->d_colT_lay : c->d_colT;
-    a.dcT = pl.lay ? c->d_dcT_lay : c->d_dcT;
+    a.colT = natural ? c->d_colT_lay : c->d_colT;
+    a.dcT = natural ? c->d_dcT_lay : c->d_dcT;
+    a.cpar = pl.kind == RES_ATOM ? 0xBFFEBFFFu : 0xFFFEFFFFu;
     a.Z = c->Z;
     a.group_threads = c->group_threads;
     a.tmem_cols = pl.tmem_cols;
     a.cols_per_group = pl.cols_per_group;
     a.rk = make_regk();
     static const QcTab empty_tab{};
-    const QcTab *qt = pl.lay ? c->qtab_lay : c->qtab;
-    cudaError_t e = res_launch(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.lay, pl.grid,
+    const QcTab *qt = pl.kind == RES_LAYERED ? c->qtab_lay : (pl.kind == RES_ATOM ? c->qtab_atom : c->qtab);
+    cudaError_t e = res_launch(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.kind, pl.grid,
                                pl.threads, pl.smem, a, qt ? *qt : empty_tab, s);
     ++g_launches;
     return e;

@@ -2,17 +2,26 @@
 #include <algorithm>
 
 #include "k_resident.cuh"
+#include "k_resident_atom.cuh"
 #include "launch.h"
 
 namespace ldpc {
 namespace {
 
-template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
+template <bool QC, bool ES, int FMT, typename TIN, int KIND>
+struct Kern {
+    static auto get() {
+        if constexpr (KIND == 2) return k_resident_atom<QC, ES, FMT, TIN>;
+        else return k_resident<QC, ES, FMT, TIN, KIND == 1>;
+    }
+};
+
+template <bool QC, bool ES, int FMT, typename TIN, int KIND>
 cudaError_t occ(size_t dyn_smem, size_t smem_per_sm, int threads, int *blocks) {
     // The occupancy API reports 1 block/SM for kernels that allocate TMEM; compute the
     // limit from the kernel's registers, shared memory and threads instead (TMEM is
     // accounted for by the caller).
-    auto kern = k_resident<QC, ES, FMT, TIN, LAY>;
+    auto kern = Kern<QC, ES, FMT, TIN, KIND>::get();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
     if (e != cudaSuccess) return e;
     cudaFuncAttributes fa;
@@ -26,9 +35,9 @@ cudaError_t occ(size_t dyn_smem, size_t smem_per_sm, int threads, int *blocks) {
     return cudaSuccess;
 }
 
-template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
+template <bool QC, bool ES, int FMT, typename TIN, int KIND>
 cudaError_t launch(int grid, int threads, size_t dyn_smem, const ResArgs &a, const QcTab &t, cudaStream_t s) {
-    auto kern = k_resident<QC, ES, FMT, TIN, LAY>;
+    auto kern = Kern<QC, ES, FMT, TIN, KIND>::get();
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, threads, dyn_smem, s>>>(a, t);
@@ -36,42 +45,44 @@ cudaError_t launch(int grid, int threads, size_t dyn_smem, const ResArgs &a, con
 }
 
 // dispatch over the template parameters; F is called with a pointer-to-instantiation tag
-template <template <bool, bool, int, typename, bool> class K, typename... Args>
-cudaError_t dispatch(bool qc, bool es, int fmt, bool i8, bool lay, Args... args) {
-#define LDPC_RES_CASE(Q, E, F)                                                                          \
-    if (qc == Q && es == E && fmt == F) {                                                               \
-        if (lay) return i8 ? K<Q, E, F, int8_t, true>::run(args...) : K<Q, E, F, int16_t, true>::run(args...); \
-        return i8 ? K<Q, E, F, int8_t, false>::run(args...) : K<Q, E, F, int16_t, false>::run(args...);       \
+template <template <bool, bool, int, typename, int> class K, typename... Args>
+cudaError_t dispatch(bool qc, bool es, int fmt, bool i8, int kind, Args... args) {
+#define LDPC_RES_KIND(Q, E, F, KK) \
+    if (kind == KK) return i8 ? K<Q, E, F, int8_t, KK>::run(args...) : K<Q, E, F, int16_t, KK>::run(args...);
+#define LDPC_RES_CASE(Q, E, F)                                                    \
+    if (qc == Q && es == E && fmt == F) {                                         \
+        LDPC_RES_KIND(Q, E, F, 0) LDPC_RES_KIND(Q, E, F, 1) LDPC_RES_KIND(Q, E, F, 2) \
     }
     LDPC_RES_CASE(true, true, FMT_C16) LDPC_RES_CASE(true, true, FMT_1BIT)
     LDPC_RES_CASE(true, false, FMT_C16) LDPC_RES_CASE(true, false, FMT_1BIT)
     LDPC_RES_CASE(false, true, FMT_C16) LDPC_RES_CASE(false, true, FMT_1BIT)
     LDPC_RES_CASE(false, false, FMT_C16) LDPC_RES_CASE(false, false, FMT_1BIT)
 #undef LDPC_RES_CASE
+#undef LDPC_RES_KIND
     return cudaErrorInvalidValue;
 }
 
-template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
+template <bool QC, bool ES, int FMT, typename TIN, int KIND>
 struct Occ {
-    static cudaError_t run(size_t d, size_t sps, int th, int *b) { return occ<QC, ES, FMT, TIN, LAY>(d, sps, th, b); }
+    static cudaError_t run(size_t d, size_t sps, int th, int *b) { return occ<QC, ES, FMT, TIN, KIND>(d, sps, th, b); }
 };
-template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
+template <bool QC, bool ES, int FMT, typename TIN, int KIND>
 struct Launch {
     static cudaError_t run(int g, int th, size_t d, const ResArgs *a, const QcTab *t, cudaStream_t s) {
-        return launch<QC, ES, FMT, TIN, LAY>(g, th, d, *a, *t, s);
+        return launch<QC, ES, FMT, TIN, KIND>(g, th, d, *a, *t, s);
     }
 };
 
 }  // namespace
 
-cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, bool lay, size_t dyn_smem, size_t smem_per_sm,
+cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,
                           int threads, int *blocks) {
-    return dispatch<Occ>(qc, es, fmt, i8, lay, dyn_smem, smem_per_sm, threads, blocks);
+    return dispatch<Occ>(qc, es, fmt, i8, kind, dyn_smem, smem_per_sm, threads, blocks);
 }
 
-cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, bool lay, int grid, int threads, size_t dyn_smem,
+cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,
                        const ResArgs &a, const QcTab &t, cudaStream_t s) {
-    return dispatch<Launch>(qc, es, fmt, i8, lay, grid, threads, dyn_smem, &a, &t, s);
+    return dispatch<Launch>(qc, es, fmt, i8, kind, grid, threads, dyn_smem, &a, &t, s);
 }
 
 }  // namespace ldpc

@@ -28,22 +28,33 @@ struct RowState {
 
 // Rebuild L^(k-1)_mn = s f(A, B, n, ñ) and form
 // q_mn = Z^(k-1)_n - L^(k-1)_mn (index reading D8) for all edges.
-template <int DC>
+// BIASED: L holds Lhat + 0x4000 per lane (see k_resident_atom.cuh); the bias is folded
+// into the four candidates so q comes out unbiased at no extra cost per edge.
+template <int DC, bool BIASED = false>
 __device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowState &st, uint32_t (&q)[DC],
                                           const RegK &k) {
-    const uint32_t nA = vneg(st.A, k), nB = vneg(st.B, k);
+    uint32_t nA, nB, A = st.A, B = st.B;
+    if (BIASED) {
+        nA = __vadd2(fnot(st.A, k), 0xC001C001u);              // -A - 0x4000 = ~A + 1 - 0x4000
+        nB = __vadd2(fnot(st.B, k), 0xC001C001u);
+        A = __vadd2(st.A, 0xC000C000u);                        // A - 0x4000
+        B = __vadd2(st.B, 0xC000C000u);
+    } else {
+        nA = vneg(st.A, k);
+        nB = vneg(st.B, k);
+    }
 #pragma unroll
     for (int i = 0; i < (DC + 1) / 2; ++i) {
         const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte
         const uint32_t wo = st.W << (3 - i);       // idx bits of pair i -> bit 7 of each byte
         {
             const uint32_t sm = prmt(ws, 0u, 0xAA88u), ix = prmt(wo, 0u, 0xAA88u);
-            const uint32_t mag = sel(ix, st.B, st.A), nmag = sel(ix, nB, nA);
+            const uint32_t mag = sel(ix, B, A), nmag = sel(ix, nB, nA);
             q[2 * i] = vadd(L[2 * i], sel(sm, mag, nmag));      // Z - L_old: L_old = s*mag
         }
         if (2 * i + 1 < DC) {
             const uint32_t sm = prmt(ws, 0u, 0xBB99u), ix = prmt(wo, 0u, 0xBB99u);
-            const uint32_t mag = sel(ix, st.B, st.A), nmag = sel(ix, nB, nA);
+            const uint32_t mag = sel(ix, B, A), nmag = sel(ix, nB, nA);
             q[2 * i + 1] = vadd(L[2 * i + 1], sel(sm, mag, nmag));
         }
     }
@@ -139,11 +150,12 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbet
 // -0x00010001: the low half can borrow from the high half (when it is 0), which
 // makes the high half Lhat_hi - 2 instead of Lhat_hi - 1 -- the same sign, because
 // doubled values are even.
+// cpar = -(0x00010001) for plain doubled values, -(0x40014001) for biased ones.
 template <int DC>
-__device__ __forceinline__ uint32_t row_parity(const uint32_t (&L)[DC], const RegK &k) {
+__device__ __forceinline__ uint32_t row_parity(const uint32_t (&L)[DC], const RegK &k, uint32_t cpar = 0xFFFEFFFFu) {
     uint32_t p = 0;
 #pragma unroll
-    for (int j = 0; j < DC; ++j) p ^= fadd32(L[j], 0xFFFEFFFFu, k);
+    for (int j = 0; j < DC; ++j) p ^= fadd32(L[j], cpar, k);
     return p & 0x80008000u;
 }
 

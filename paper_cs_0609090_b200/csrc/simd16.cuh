@@ -21,8 +21,9 @@ struct RegK {
     uint32_t zero;   // 0
     uint32_t m1;     // 0xFFFFFFFF
     uint32_t one;    // 1
+    uint32_t m2;     // 0xFFFFFFFE (-2)
 };
-__host__ __device__ inline RegK make_regk() { return RegK{0u, 0xFFFFFFFFu, 1u}; }
+__host__ __device__ inline RegK make_regk() { return RegK{0u, 0xFFFFFFFFu, 1u, 0xFFFFFFFEu}; }
 // ~a = a * (-1) + (-1): exact bitwise NOT as one IMAD (FMA pipe)
 __device__ __forceinline__ uint32_t fnot(uint32_t a, const RegK &k) {
     uint32_t d;
@@ -33,6 +34,13 @@ __device__ __forceinline__ uint32_t fnot(uint32_t a, const RegK &k) {
 __device__ __forceinline__ uint32_t fadd32(uint32_t a, uint32_t c, const RegK &k) {
     uint32_t d;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(k.one), "r"(c));
+    return d;
+}
+// packed 16x2 (P form) -> "V form" hi*65536 + lo as a 32-bit integer, so that one
+// 32-bit integer add adds both lanes exactly: p - ((p & 0x8000) << 1)  (LOP3 + IMAD)
+__device__ __forceinline__ uint32_t vform(uint32_t p, const RegK &k) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(p & 0x8000u), "r"(k.m2), "r"(p));
     return d;
 }
 // -a per half (IMAD NOT + VIADD)

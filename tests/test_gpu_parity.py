@@ -348,3 +348,18 @@ def test_stream_l2_chunks(chunk, monkeypatch):
     ref = oracle.decode(code, llr, "compact", "f32", 10, 1, alpha=0.75, nthreads=NT)
     _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
     np.testing.assert_array_equal(it, ref.iters)
+
+
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3])
+def test_batched_resident_kernel(cfg_idx, monkeypatch):
+    """The conflict-free-batch resident kernel (LDPC_RES_BATCHED=1; the default flooding
+    kernel accumulates with shared-memory atomics instead) stays bit-exact too."""
+    monkeypatch.setenv("LDPC_RES_BATCHED", "1")
+    cfg = g.CONFIGS[cfg_idx]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, 129)
+    assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, cfg.early_stop, cfg.offset_raw, cfg.clamp)
+    for c in small_codes()[:4]:
+        z = g.llr(11, 0, 33, c.n_vars, g.ebn0_to_sigma2(1.5, max(c.rate, 0.3)), g.LLR_I16, 3, 511)
+        params = P.make_params(10, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+        assert_int_parity(c, z, params, 10, 1, 1, 511)

@@ -561,6 +561,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         return fail(LDPC_ERR_INVALID_ARG, "bad variant %d", p->variant);
     if (p->llr_type == LDPC_LLR_F32) {
         if (p->msg_format == LDPC_MSG_1BIT) return fail(LDPC_ERR_UNSUPPORTED, "1-bit messages need integer LLRs");
+        if (pl.sched == LDPC_SCHED_LAYERED)
+            return fail(LDPC_ERR_UNSUPPORTED, "layered schedule is implemented for integer LLRs only");
         if (c->max_dc > 16) return fail(LDPC_ERR_UNSUPPORTED, "F32 path supports row degree <= 16 (max %d)", c->max_dc);
         if (p->variant == LDPC_MINSUM_NORMALIZED) {
             if (!(p->alpha > 0.f && p->alpha <= 1.f)) return fail(LDPC_ERR_INVALID_ARG, "alpha must be in (0,1]");

@@ -70,3 +70,12 @@ def test_layered_unsupported_for_streaming_sizes():
     with pytest.raises(P.LdpcError) as e:
         dec.workspace(64, P.params_for_config(g.CONFIGS[4], LAY))
     assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+
+
+def test_layered_f32_unsupported():
+    code = g.CONFIGS[1].code()
+    dec = decoder(code)
+    params = P.make_params(5, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY)
+    with pytest.raises(P.LdpcError) as e:
+        dec.workspace(8, params)
+    assert e.value.status == P.LDPC_ERR_UNSUPPORTED

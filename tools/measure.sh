@@ -5,12 +5,12 @@ OUT=gpurun_out/meas; mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
 lscpu > $OUT/lscpu.txt 2>&1
 timeout 900 python bench.py > $OUT/bench_cfg2.json 2> $OUT/bench_cfg2.err; echo "bench cfg2 rc=$?"
-for c in 1 3 4 5; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --cpu-budget 6 > $OUT/bench_cfg$c.json 2> $OUT/bench_cfg$c.err; echo "bench cfg$c rc=$?"; done
+for c in 1 3 4 5; do timeout 900 python bench.py --config $c --steps 10 --warmup 3 --cpu-budget 6 > $OUT/bench_cfg$c.json 2> $OUT/bench_cfg$c.err; echo "bench cfg$c rc=$?"; done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref_cfg2.json 2> $OUT/bench_ref.err; echo "ref rc=$?"
 # launch list of the bench command (cold-cache, serialised: compare shares)
-timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/bench_plain.json 2>&1 && \
+timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-twoscan --no-layered > $OUT/bench_plain.json 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_cfg2.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "launches rc=$?"
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-twoscan --no-layered > $OUT/ncu_launch.log 2>&1; echo "launches rc=$?"
 for c in 2 4 5; do
   K=k_resident; [ $c -ge 4 ] && K=k_stream_pipe
   timeout 300 python tools/prof_decode.py --config $c --reps 2 > $OUT/prof_plain_cfg$c.log 2>&1 && \

@@ -20,7 +20,7 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
 oracle/liboracle.so: oracle/oracle.c oracle/engine.inc
-	gcc -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -o $@ oracle/oracle.c -lpthread
+	gcc -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -o $@ oracle/oracle.c -lm -lpthread
 
 ldpcgen/libldpcgen.so: ldpcgen/ldpcgen.c
 	gcc -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -o $@ ldpcgen/ldpcgen.c -lm -lpthread

@@ -39,7 +39,9 @@ ENGINES = {"twoscan_naive": TWOSCAN_NAIVE, "twoscan": TWOSCAN, "singlescan": SIN
 class Params(ctypes.Structure):
     _fields_ = [("max_iter", ctypes.c_int32), ("early_stop", ctypes.c_int32),
                 ("beta_i", ctypes.c_int32), ("clamp_i", ctypes.c_int32),
-                ("alpha", ctypes.c_double), ("beta_f", ctypes.c_double)]
+                ("alpha", ctypes.c_double), ("beta_f", ctypes.c_double),
+                ("beta_i_sched", ctypes.c_void_p), ("alpha_sched", ctypes.c_void_p),
+                ("beta_f_sched", ctypes.c_void_p)]
 
 
 def build(force: bool = False) -> str:
@@ -47,7 +49,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(s) for s in srcs):
         # -ffp-contract=off: no FMA contraction (reading D11); -O2 only, never tuned.
         subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-ffp-contract=off",
-                               "-o", _LIB, srcs[0], "-lpthread"])
+                               "-o", _LIB, srcs[0], "-lm", "-lpthread"])
     return _LIB
 
 
@@ -85,8 +87,9 @@ def _ptr(a: Optional[np.ndarray]):
 
 def make_params(max_iter: int = 1, early_stop: int = 0, beta: float = 0, clamp: int = 0,
                 alpha: float = 1.0) -> Params:
-    """Integer modes use beta (LSBs) and clamp; float modes use alpha and beta."""
-    return Params(int(max_iter), int(early_stop), int(beta), int(clamp), float(alpha), float(beta))
+    """Integer modes use beta (LSBs), clamp and alpha (normalized: floor(alpha |L|),
+    reading D27); float modes use alpha and beta."""
+    return Params(int(max_iter), int(early_stop), int(beta), int(clamp), float(alpha), float(beta), None, None, None)
 
 
 def check_naive(q, mode="int", beta=0, clamp=0, alpha=1.0) -> np.ndarray:
@@ -126,9 +129,10 @@ class Result:
 
 
 def decode(code, z0: np.ndarray, engine="compact", mode="int", max_iter=10, early_stop=0,
-           beta=0, clamp=0, alpha=1.0, trace=False, nthreads: int = 1) -> Result:
+           beta=0, clamp=0, alpha=1.0, trace=False, nthreads: int = 1, beta_sched=None, alpha_sched=None) -> Result:
     """Decode frames z0 ([F][N]) of ``code`` (any object with n_vars, n_checks,
-    row_ptr, col_idx) with one of the oracle engines."""
+    row_ptr, col_idx) with one of the oracle engines.  beta_sched / alpha_sched: optional
+    per-iteration offsets / normalization factors (max_iter entries)."""
     dt, suf = _TYPES[mode]
     eng = ENGINES[engine] if isinstance(engine, str) else int(engine)
     z0 = np.ascontiguousarray(np.atleast_2d(z0), dt)
@@ -147,6 +151,20 @@ def decode(code, z0: np.ndarray, engine="compact", mode="int", max_iter=10, earl
         tp = np.full((F, max_iter, N), sentinel, dt)
         tm = np.full((F, max_iter, E), sentinel, dt)
     p = make_params(max_iter, early_stop, beta, clamp, alpha)
+    keep = []
+    if beta_sched is not None:
+        bs = np.ascontiguousarray(beta_sched, np.int32 if mode == "int" else np.float64)
+        assert bs.size >= max_iter
+        keep.append(bs)
+        if mode == "int":
+            p.beta_i_sched = bs.ctypes.data
+        else:
+            p.beta_f_sched = bs.ctypes.data
+    if alpha_sched is not None:
+        a_s = np.ascontiguousarray(alpha_sched, np.float64)
+        assert a_s.size >= max_iter
+        keep.append(a_s)
+        p.alpha_sched = a_s.ctypes.data
     nt = getattr(lib(), f"orc_decode_{suf}")(eng, N, code.n_checks, _ptr(rp), _ptr(ci), ctypes.byref(p), F,
                                              _ptr(z0), _ptr(post), _ptr(bits), _ptr(ok), _ptr(iters),
                                              _ptr(tp), _ptr(tm), int(nthreads))

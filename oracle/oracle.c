@@ -22,6 +22,7 @@
  * Readings of silent/ambiguous passages are listed in DESIGN.md §3 (D1-D23).
  * Parity pins: tests/test_oracle_*.py (none of this file is "parity unpinned").
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -38,6 +39,11 @@ typedef struct {
     int32_t clamp_i;      /* int: magnitude clamp Q (0 = none) */
     double alpha;         /* float: normalization lambda (1 = none) */
     double beta_f;        /* float: offset beta (0 = none) */
+    /* optional per-iteration schedules (NULL = the constants above), K entries:
+     * lambda_k and beta_k of PAPER.md P:179 */
+    const int32_t *beta_i_sched;
+    const double *alpha_sched;
+    const double *beta_f_sched;
 } orc_params;
 
 typedef struct {

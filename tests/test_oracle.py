@@ -395,3 +395,57 @@ def test_layered_row_order_matters_and_stopping():
     both = (a.ok == 1) & (b.ok == 1)
     assert both.sum() >= 38 and np.array_equal(a.bits[both], b.bits[both])
     assert a.iters[both].mean() <= b.iters[both].mean()
+
+
+# ------------------------- per-iteration schedules, integer normalization (§8(f3))
+@pytest.mark.parametrize("case", _load("schedules_toy.json")["cases"], ids=lambda c: c["cite"])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_schedule_toy_trajectories(case, engine):
+    """Hand-evaluated trajectories with beta_k / lambda_k schedules and floor(lambda |L|)
+    (tests/golden/schedules_toy.json, reading D27)."""
+    gd = _load("schedules_toy.json")
+    code = g.from_dense(gd["code"])
+    r = oracle.decode(code, np.array([gd["z0"]]), engine=engine, mode="int", max_iter=2, trace=True,
+                      beta_sched=case["beta_sched"], alpha_sched=case["alpha_sched"])
+    np.testing.assert_array_equal(r.trace_post[0], case["post"])
+
+
+def test_int_normalized_check_row():
+    """floor(3/4 * min) on a hand-evaluated 3-edge row: q = [7, -3, 9] -> [-2, 5, -2]."""
+    out = oracle.check_naive(np.array([7, -3, 9]), "int", alpha=0.75)
+    assert out.tolist() == [-2, 5, -2]
+    msgs, A, B, idx, s = oracle.check_compact(np.array([7, -3, 9]), "int", alpha=0.75)
+    assert msgs.tolist() == [-2, 5, -2] and (A, B, idx) == (2, 5, 1)
+
+
+@pytest.mark.parametrize("code", _codes_small()[:3], ids=lambda c: c.name)
+def test_schedules_engines_bit_identical(code):
+    """P:338 equivalence holds iteration by iteration under beta_k / lambda_k schedules
+    (integer, dyadic lambda): naive two-scan == compact single-scan, and layered full-L ==
+    layered compact; a constant schedule equals the scalar parameters."""
+    sigma2 = g.ebn0_to_sigma2(1.5, max(code.rate, 0.3))
+    z0 = g.llr(79, 0, 20, code.n_vars, sigma2, g.LLR_I16, 3, 511).astype(np.int32)
+    K = 12
+    bs = [2, 2, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0]
+    al = [0.5, 0.625, 0.75, 0.75, 0.875, 0.875, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0]
+    a = oracle.decode(code, z0, "twoscan_naive", "int", K, 0, 0, 511, trace=True, beta_sched=bs, alpha_sched=al)
+    b = oracle.decode(code, z0, "compact", "int", K, 0, 0, 511, trace=True, beta_sched=bs, alpha_sched=al)
+    assert np.array_equal(a.trace_post, b.trace_post) and np.array_equal(a.trace_msg, b.trace_msg)
+    a = oracle.decode(code, z0, "layered_full", "int", K, 1, 0, 511, trace=True, beta_sched=bs, alpha_sched=al)
+    b = oracle.decode(code, z0, "layered", "int", K, 1, 0, 511, trace=True, beta_sched=bs, alpha_sched=al)
+    assert np.array_equal(a.trace_post, b.trace_post) and np.array_equal(a.iters, b.iters)
+    c1 = oracle.decode(code, z0, "compact", "int", K, 0, 1, 511, alpha=0.75, trace=True)
+    c2 = oracle.decode(code, z0, "compact", "int", K, 0, 0, 511, trace=True, beta_sched=[1] * K, alpha_sched=[0.75] * K)
+    assert np.array_equal(c1.trace_post, c2.trace_post)
+
+
+def test_float_schedule_matches_scalar_and_twoscan():
+    code = g.regular(96, 3, 6, seed=5)
+    z0 = g.llr(8, 0, 10, code.n_vars, g.ebn0_to_sigma2(1.5, code.rate), g.LLR_F64)
+    al = np.linspace(0.6, 0.9, 15)
+    ts = oracle.decode(code, z0, "twoscan", "f64", 15, 0, trace=True, alpha_sched=al)
+    cp = oracle.decode(code, z0, "compact", "f64", 15, 0, trace=True, alpha_sched=al)
+    assert np.max(np.abs(ts.trace_post - cp.trace_post) / (1 + np.abs(ts.trace_post))) < 1e-9
+    s1 = oracle.decode(code, z0, "compact", "f64", 15, 0, alpha=0.8, trace=True)
+    s2 = oracle.decode(code, z0, "compact", "f64", 15, 0, trace=True, alpha_sched=[0.8] * 15)
+    assert np.array_equal(s1.trace_post, s2.trace_post)

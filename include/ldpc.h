@@ -84,7 +84,7 @@ ldpc_status ldpc_code_query(const ldpc_code *code, int32_t *n_vars, int32_t *n_c
 enum { LDPC_LLR_I16 = 0, LDPC_LLR_I8 = 1, LDPC_LLR_F32 = 2 };
 /* Check-node variant (P:178-188 two-scan; P:338-353 single-scan compact form). */
 enum { LDPC_MINSUM_OFFSET = 0,       /* |L| <= max(|L| - beta, 0); offset 0 = plain min-sum */
-       LDPC_MINSUM_NORMALIZED = 1 }; /* |L| <= alpha |L|, 0 < alpha <= 1 (F32 only) */
+       LDPC_MINSUM_NORMALIZED = 1 }; /* |L| <= alpha |L|, 0 < alpha <= 1 (integer LLRs: floor, dyadic alpha) */
 /* Persistent message format.  Both keep, per check row, the two
  * magnitudes A_m <= B_m, the position ñ_m and one sign bit s_mn per edge:
  *   COMPACT: magnitudes stored with 9+ bits (clamp Q <= 511 for integer LLRs);
@@ -121,7 +121,7 @@ typedef struct {
     int32_t variant;       /* LDPC_MINSUM_OFFSET | LDPC_MINSUM_NORMALIZED */
     int32_t offset_raw;    /* integer LLRs: offset beta in LSBs, >= 0 */
     float   offset_f;      /* F32 LLRs: offset beta, >= 0 (OFFSET variant) */
-    float   alpha;         /* F32 LLRs, NORMALIZED variant: lambda in (0, 1] */
+    float   alpha;         /* NORMALIZED variant: lambda in (0, 1]; integer LLRs: dyadic, floor(lambda|L|) */
     int32_t clamp_raw;     /* integer LLRs: magnitude clamp Q applied after the offset (reading
                               D6); 0 = default (511 for I16, 127 for I8).  Channel LLRs are
                               saturated to [-Q, Q] on load.  Requires 2*Q*(max_dv + 2) <= 32767
@@ -130,6 +130,19 @@ typedef struct {
     int32_t llr_type;      /* LDPC_LLR_I16 | LDPC_LLR_I8 | LDPC_LLR_F32 */
     int32_t msg_format;    /* LDPC_MSG_COMPACT | LDPC_MSG_1BIT (1BIT requires integer LLRs) */
     int32_t schedule;      /* LDPC_SCHED_SINGLESCAN (0, default) | _TWOSCAN | _LAYERED */
+    /* Optional per-iteration variants (P:179 lambda_k, P:186 beta_k): HOST arrays of
+     * max_iter entries, read during the call only; NULL = the constants above.
+     *   offset_per_iter   integer LLRs: beta_k in LSBs (>= 0)
+     *   offset_f_per_iter F32 LLRs: beta_k (>= 0)
+     *   alpha_per_iter    lambda_k in (0, 1] (any variant; overrides alpha)
+     * Integer LLRs with lambda != 1 (constant or per iteration) use floor(lambda |L|)
+     * (reading D27) and require a dyadic lambda = a/2^s with s <= 8 and
+     * a * 2Q(max_dv+2) < 65536, else LDPC_ERR_UNSUPPORTED.  The resident kernels take
+     * schedules of up to 64 iterations (longer ones run on the streaming kernels;
+     * LAYERED: LDPC_ERR_UNSUPPORTED). */
+    const int32_t *offset_per_iter;
+    const float   *offset_f_per_iter;
+    const float   *alpha_per_iter;
 } ldpc_decode_params;
 
 /* Device workspace bytes needed by ldpc_decode_batch for n_frames frames. */

@@ -43,7 +43,10 @@ class ldpc_decode_params(ctypes.Structure):
     _fields_ = [("max_iter", ctypes.c_int32), ("early_stop", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("offset_raw", ctypes.c_int32), ("offset_f", ctypes.c_float), ("alpha", ctypes.c_float),
                 ("clamp_raw", ctypes.c_int32), ("llr_type", ctypes.c_int32), ("msg_format", ctypes.c_int32),
-                ("schedule", ctypes.c_int32)]
+                ("schedule", ctypes.c_int32),
+                ("offset_per_iter", ctypes.POINTER(ctypes.c_int32)),
+                ("offset_f_per_iter", ctypes.POINTER(ctypes.c_float)),
+                ("alpha_per_iter", ctypes.POINTER(ctypes.c_float))]
 
 
 class LdpcError(RuntimeError):
@@ -152,10 +155,25 @@ def ldpc_code_query(handle: int):
 
 def make_params(max_iter=10, early_stop=0, variant=LDPC_MINSUM_OFFSET, offset_raw=0, offset_f=0.0, alpha=1.0,
                 clamp_raw=0, llr_type=LDPC_LLR_I16, msg_format=LDPC_MSG_COMPACT,
-                schedule=None) -> ldpc_decode_params:
+                schedule=None, offset_per_iter=None, offset_f_per_iter=None,
+                alpha_per_iter=None) -> ldpc_decode_params:
+    """ldpc_decode_params; the optional per-iteration arrays (max_iter entries) are kept
+    alive on the returned object."""
+    import numpy as np
     sched = LDPC_SCHED_SINGLESCAN if schedule is None else int(schedule)
-    return ldpc_decode_params(int(max_iter), int(early_stop), int(variant), int(offset_raw), float(offset_f),
-                              float(alpha), int(clamp_raw), int(llr_type), int(msg_format), sched)
+    p = ldpc_decode_params(int(max_iter), int(early_stop), int(variant), int(offset_raw), float(offset_f),
+                           float(alpha), int(clamp_raw), int(llr_type), int(msg_format), sched)
+    p._keep = []
+    for name, arr, dt, ct in (("offset_per_iter", offset_per_iter, np.int32, ctypes.c_int32),
+                              ("offset_f_per_iter", offset_f_per_iter, np.float32, ctypes.c_float),
+                              ("alpha_per_iter", alpha_per_iter, np.float32, ctypes.c_float)):
+        if arr is not None:
+            a = np.ascontiguousarray(arr, dt)
+            if a.size < max_iter:
+                raise ValueError(f"{name} needs max_iter = {max_iter} entries")
+            p._keep.append(a)
+            setattr(p, name, a.ctypes.data_as(ctypes.POINTER(ct)))
+    return p
 
 
 def ldpc_decode_workspace_size(handle: int, n_frames: int, params: ldpc_decode_params) -> int:

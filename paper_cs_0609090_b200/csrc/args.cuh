@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "simd16.cuh"
+#include "rowcore_types.cuh"
 
 namespace ldpc {
 
@@ -24,9 +25,13 @@ struct QcTab {
     uint2 ent[kQcMaxEnt];               // (4 * shift, 4 * (j * Z)) per base-matrix entry
 };
 
+constexpr int kMaxSched = 64;   // per-iteration variant table of the resident kernels
+
 struct ResArgs {
     int N, Np, M, npairs, nframes, K, Qsat, wpf;   // Np = N rounded up to 4; wpf = ceil(N/32)
-    uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp
+    VarK vk;                       // check-node variant (constant over iterations)
+    int nsched;                    // > 0: iteration k uses vk_sched[k-1] (lambda_k / beta_k)
+    VarK vk_sched[kMaxSched];
     const void *llr;
     uint32_t *hard_bits;
     int16_t *post;
@@ -49,7 +54,7 @@ struct ResArgs {
 struct StreamArgs {
     RegK rk;                     // register constants (simd16.cuh)
     int N, M, ntiles, nframes, K, Qsat, wpf;
-    uint32_t nbeta2p1, q2p1;       // packed (1 - 2 beta), (2Q + 1): doubled-domain offset/clamp
+    VarK vk;                     // check-node variant of this launch's iteration
     float alpha, beta;           // fp32 variant: |L| <= max(alpha*min - beta, 0)
     const int32_t *row_ptr, *col_idx;
     const uint4 *rowtab;         // [M][2]: up to 8 column indices per row; dc in bits 28-31 of word 0 (15 = wider row)

@@ -63,8 +63,8 @@ __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.pr
 // LAY = false: flooding (Z^(k-1) read from Lpb, Z^(k) accumulated in Lab).
 // LAY = true : layered / in-place (reading D25): one array, Z_n <- (Z_n - L_old) + L_new.
 template <int DC, bool QC, bool ES, bool LAY>
-__device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const char *Lpb, char *Lab, int e0,
-                                        uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
+__device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const VarK &vk, const char *Lpb, char *Lab,
+                                        int e0, uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
     // shared-memory byte addresses of the row's variables in both buffers:
     // 4 * (jZ + (r + s) mod Z) + base, one VIADDMNMX for the modulo and one IADD3 per buffer
     const uint32_t bp = (uint32_t)__cvta_generic_to_shared(Lpb), ba = (uint32_t)__cvta_generic_to_shared(Lab);
@@ -96,7 +96,7 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
         rebuild_q<DC>(L, st, q, a.rk);
     }
     uint32_t rn[DC];
-    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.rk);
+    new_state<DC>(q, vk, st, rn, a.rk);
     if (LAY) {
 #pragma unroll
         for (int j = 0; j < DC; ++j)                          // Z_n = (Z_n - L^(k-1)_mn) + L^(k)_mn
@@ -112,17 +112,17 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
 }
 
 template <bool QC, bool ES, bool LAY>
-__device__ __forceinline__ void res_dispatch(int dc, const ResArgs &a, const QcTab &t, const char *Lpb, char *Lab,
+__device__ __forceinline__ void res_dispatch(int dc, const ResArgs &a, const QcTab &t, const VarK &vk, const char *Lpb, char *Lab,
                                              int e0, uint32_t r4, int p, bool first_iter, RowState &st,
                                              uint32_t &synd) {
     switch (dc) {
-    case 2: res_row<2, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 3: res_row<3, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 4: res_row<4, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 5: res_row<5, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 6: res_row<6, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 7: res_row<7, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 8: res_row<8, QC, ES, LAY>(a, t, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 2: res_row<2, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 3: res_row<3, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 4: res_row<4, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 5: res_row<5, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 6: res_row<6, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 7: res_row<7, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 8: res_row<8, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
     }
 }
 
@@ -219,7 +219,7 @@ __device__ __forceinline__ void state_tmem_store(uint32_t tw, int b, int nb, con
 // Consecutive super-batches in which this group's rows have the same degree DC are
 // processed by one loop (one dispatch per run instead of per batch).
 template <int DC, bool ES, int FMT, bool LAY>
-__device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, uint32_t tw, int nb,
+__device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t tw, int nb,
                                       int rloc, uint32_t r4, const char *Lpb, char *Lab, bool first_iter,
                                       uint32_t &synd) {
 #pragma unroll 1
@@ -227,7 +227,7 @@ __device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, 
         RowState st = {0u, 0u, 0u};
         if constexpr (DC > 0) {
             if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-            if (rloc < a.Z) res_row<DC, true, ES, LAY>(a, t, Lpb, Lab, t.e0[b][g], r4, 0, first_iter, st, synd);
+            if (rloc < a.Z) res_row<DC, true, ES, LAY>(a, t, vk, Lpb, Lab, t.e0[b][g], r4, 0, first_iter, st, synd);
             state_tmem_store<FMT>(tw, b, nb, st);
         }
         __syncthreads();                         // batch b's accumulations complete
@@ -237,17 +237,17 @@ __device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, 
 
 template <bool ES, int FMT, bool LAY>
 __device__ __forceinline__ int qc_run_dispatch(int dc, int b, int bend, int g, const ResArgs &a, const QcTab &t,
-                                               uint32_t tw, int nb, int rloc, uint32_t r4, const char *Lpb, char *Lab,
+                                               const VarK &vk, uint32_t tw, int nb, int rloc, uint32_t r4, const char *Lpb, char *Lab,
                                                bool first_iter, uint32_t &synd) {
     switch (dc) {
-    case 2: return qc_run<2, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 3: return qc_run<3, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 4: return qc_run<4, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 5: return qc_run<5, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 6: return qc_run<6, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 7: return qc_run<7, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    case 8: return qc_run<8, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-    default: return qc_run<0, ES, FMT, LAY>(b, bend, g, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 2: return qc_run<2, ES, FMT, LAY>(b, bend, g, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 3: return qc_run<3, ES, FMT, LAY>(b, bend, g, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 4: return qc_run<4, ES, FMT, LAY>(b, bend, g, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 5: return qc_run<5, ES, FMT, LAY>(b, bend, g, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 6: return qc_run<6, ES, FMT, LAY>(b, bend, g, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 7: return qc_run<7, ES, FMT, LAY>(b, bend, g, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    case 8: return qc_run<8, ES, FMT, LAY>(b, bend, g, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+    default: return qc_run<0, ES, FMT, LAY>(b, bend, g, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
     }
 }
 
@@ -275,7 +275,7 @@ __device__ __forceinline__ uint32_t parity_pass(const ResArgs &a, const QcTab &t
 // disjoint rows (QC: consecutive base rows), so processing a batch in parallel is the
 // same as processing its rows one after the other.
 template <bool QC, bool ES, int FMT, typename TIN, bool LAY>
-__global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __grid_constant__ QcTab t) {
+__global__ void __launch_bounds__(256, 3) k_resident(const __grid_constant__ ResArgs a, const __grid_constant__ QcTab t) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint32_t tslot;
     __shared__ __align__(8) uint64_t zbar;
@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
             if (!LAY && k > 1) { mbar_wait(&zbar, zphase); zphase ^= 1; }   // La = Z^(0) has landed
             uint32_t synd = 0;
             const bool first_iter = (k == 1);
+            const VarK vk = a.nsched ? a.vk_sched[k - 1] : a.vk;   // lambda_k / beta_k
             if (LAY && ES) {
                 // syndrome of the posterior after iteration k-1, before this iteration
                 // changes it in place
@@ -345,8 +346,8 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
                 // warp-uniform group branch: uniform table indices
 #pragma unroll 1
                 for (int b = 0; b < nb;) {
-                    if (grp == 0) b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-                    else b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+                    if (grp == 0) b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
+                    else b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
                 }
             } else {
 #pragma unroll 1
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(256, 3) k_resident(const ResArgs a, const __gr
                     } else if (!first_iter) {
                         state_tmem_load<FMT>(tw, b, nb, st);
                     }
-                    if (valid) res_dispatch<QC, RES, LAY>(a.dcT[p], a, t, Lpb, Lab, 0, 0, p, first_iter, st, synd);
+                    if (valid) res_dispatch<QC, RES, LAY>(a.dcT[p], a, t, vk, Lpb, Lab, 0, 0, p, first_iter, st, synd);
                     if (LAY) {
                         if (valid) { sst[p] = st.A; sst[a.M + p] = st.B; sst[2 * a.M + p] = st.W; }
                     } else {

@@ -27,7 +27,7 @@ namespace ldpc {
 constexpr int kAtomBias = 0x4000;
 
 template <int DC, bool QC, bool ES>
-__device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, uint32_t bp, uint32_t ba, int e0,
+__device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba, int e0,
                                          uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
     uint32_t d[DC];
 #pragma unroll
@@ -52,14 +52,14 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, uint3
         rebuild_q<DC, true>(L, st, q, a.rk);                               // Z_n - L^(k-1)_mn
     }
     uint32_t rn[DC];
-    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.rk);
+    new_state<DC>(q, vk, st, rn, a.rk);
 #pragma unroll
     for (int j = 0; j < DC; ++j)                                          // Z^(k)_n += L^(k)_mn
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(vform(rn[j], a.rk)) : "memory");
 }
 
 template <int DC, bool ES, int FMT>
-__device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, uint32_t tw,
+__device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t tw,
                                            int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba, bool first_iter,
                                            uint32_t &synd) {
     if constexpr (DC == 0) {
@@ -69,7 +69,7 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
         for (; b < bend; ++b) {
             RowState st = {0u, 0u, 0u};
             if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-            if (rloc < a.Z) atom_row<DC, true, ES>(a, t, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
+            if (rloc < a.Z) atom_row<DC, true, ES>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
             state_tmem_store<FMT>(tw, b, nb, st);
         }
         return b;
@@ -78,31 +78,31 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
 
 template <bool ES, int FMT>
 __device__ __forceinline__ int atom_qc_dispatch(int dc, int b, int bend, int g, const ResArgs &a, const QcTab &t,
-                                                uint32_t tw, int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba,
+                                                const VarK &vk, uint32_t tw, int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba,
                                                 bool first_iter, uint32_t &synd) {
     switch (dc) {
-    case 2: return atom_qc_run<2, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 3: return atom_qc_run<3, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 4: return atom_qc_run<4, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 5: return atom_qc_run<5, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 6: return atom_qc_run<6, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 7: return atom_qc_run<7, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 8: return atom_qc_run<8, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    default: return atom_qc_run<0, ES, FMT>(b, bend, g, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 2: return atom_qc_run<2, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 3: return atom_qc_run<3, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 4: return atom_qc_run<4, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 5: return atom_qc_run<5, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 6: return atom_qc_run<6, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 7: return atom_qc_run<7, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 8: return atom_qc_run<8, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    default: return atom_qc_run<0, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
     }
 }
 
 template <bool ES>
-__device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, const QcTab &t, uint32_t bp, uint32_t ba,
+__device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba,
                                                   int p, bool first_iter, RowState &st, uint32_t &synd) {
     switch (dc) {
-    case 2: atom_row<2, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 3: atom_row<3, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 4: atom_row<4, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 5: atom_row<5, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 6: atom_row<6, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 7: atom_row<7, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 8: atom_row<8, false, ES>(a, t, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 2: atom_row<2, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 3: atom_row<3, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 4: atom_row<4, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 5: atom_row<5, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 6: atom_row<6, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 7: atom_row<7, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 8: atom_row<8, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
     }
 }
 
@@ -137,7 +137,8 @@ __device__ __forceinline__ void atom_ingest(const ResArgs &a, const TIN *__restr
 }
 
 template <bool QC, bool ES, int FMT, typename TIN>
-__global__ void __launch_bounds__(256, 3) k_resident_atom(const ResArgs a, const __grid_constant__ QcTab t) {
+__global__ void __launch_bounds__(256, 3) k_resident_atom(const __grid_constant__ ResArgs a,
+                                                          const __grid_constant__ QcTab t) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint32_t tslot;
     __shared__ __align__(8) uint64_t zbar;
@@ -170,11 +171,12 @@ __global__ void __launch_bounds__(256, 3) k_resident_atom(const ResArgs a, const
             if (k > 1) { mbar_wait(&zbar, zphase); zphase ^= 1; }          // Z^(k) = Z^(0) landed
             uint32_t synd = 0;
             const bool first_iter = (k == 1);
+            const VarK vk = a.nsched ? a.vk_sched[k - 1] : a.vk;   // lambda_k / beta_k
             if (QC) {
 #pragma unroll 1
                 for (int b = 0; b < nb;) {
-                    if (grp == 0) b = atom_qc_dispatch<ES, FMT>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-                    else b = atom_qc_dispatch<ES, FMT>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+                    if (grp == 0) b = atom_qc_dispatch<ES, FMT>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+                    else b = atom_qc_dispatch<ES, FMT>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
                 }
             } else {
 #pragma unroll 1
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(256, 3) k_resident_atom(const ResArgs a, const
                     RowState st = {0u, 0u, 0u};
                     if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
                     const int p = b * nth + tid;
-                    if (p < a.M) atom_csr_dispatch<ES>(a.dcT[p], a, t, bp, ba, p, first_iter, st, synd);
+                    if (p < a.M) atom_csr_dispatch<ES>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, st, synd);
                     state_tmem_store<FMT>(tw, b, nb, st);
                 }
             }

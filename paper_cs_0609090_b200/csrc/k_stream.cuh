@@ -156,7 +156,7 @@ __device__ __forceinline__ void stream_rows_i(const StreamArgs &a, int lane, con
             rebuild_q<DC>(L[r], st[r], q, a.rk);
         }
         uint32_t rn[DC];
-        new_state<DC>(q, a.nbeta2p1, a.q2p1, st[r], rn, a.rk);
+        new_state<DC>(q, a.vk, st[r], rn, a.rk);
         StateIO<FMT>::store(stt + lane, sstride, (size_t)m[r] * 32, st[r]);
 #pragma unroll
         for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], to_vform(rn[j] & ~keep));

@@ -76,7 +76,7 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
         rebuild_q<DC>(L, st, q, a.rk);
     }
     uint32_t rn[DC];
-    new_state<DC>(q, a.nbeta2p1, a.q2p1, st, rn, a.rk);
+    new_state<DC>(q, a.vk, st, rn, a.rk);
     StateIO<FMT>::store(stt + lane, sstride, (size_t)m * 32, st);
 #pragma unroll
     for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, to_vform(rn[j] & ~keep));

@@ -51,7 +51,7 @@ __device__ __forceinline__ void ts_check_row(const StreamArgs &a, const TwoScanA
     uint32_t r[DC];
     if (PAIR) {
         RowState st;
-        new_state<DC>(z, a.nbeta2p1, a.q2p1, st, r, a.rk);   // Eq.(1) + offset/clamp; state unused
+        new_state<DC>(z, a.vk, st, r, a.rk);   // Eq.(1) + offset/clamp; state unused
     } else {
         float zf[DC], rf[DC], A, B;
         uint32_t W;

@@ -24,6 +24,9 @@ struct StreamRun {
     int max_iter, max_dc, ntiles;
     int chunk_tiles;      // tiles decoded together through all iterations (0 = all)
     size_t flags_bytes;   // bytes from a.synd to the end of the per-tile flag words (zeroed first)
+    // per-iteration variants (host arrays of max_iter entries, NULL = the constants in a)
+    const VarK *vk_sched;
+    const float *alpha_sched, *beta_sched;
 };
 cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, int32_t *launches);
 

@@ -514,6 +514,9 @@ enum Path { PATH_RESIDENT = 0, PATH_STREAM_I = 1, PATH_STREAM_F = 2 };
 
 struct Plan {
     Path path;
+    VarK vk{};                   // integer check-node variant (constant)
+    std::vector<VarK> vks;       // per-iteration integer variants (empty: constant)
+    std::vector<float> alphas, betafs;   // per-iteration fp32 lambda_k / beta_k (empty: constant)
     int sched = LDPC_SCHED_SINGLESCAN;
     int Q = 0, beta = 0, fmt = FMT_C16;
     float alpha = 1.f, betaf = 0.f;
@@ -532,6 +535,32 @@ struct Plan {
     size_t off_msg = 0, off_zv = 0;   // two-scan: per-edge L_mn and Z_mn planes
     size_t ws_bytes = 0;
 };
+
+// integer variant of one iteration: offset beta (LSBs), normalization lambda = na / 2^ns
+// (dyadic, reading D27), clamp Q.  Returns false if lambda is not dyadic with ns <= 8.
+bool make_vark(double lambda, int beta, int Q, VarK &v) {
+    v = VarK{};
+    if (lambda == 1.0) {
+        v.norm = 0;
+        v.nbeta2p1 = pack2(1 - 2 * beta, 1 - 2 * beta);
+        v.q2p1 = pack2(2 * Q + 1, 2 * Q + 1);
+        return true;
+    }
+    for (int ns = 0; ns <= 8; ++ns) {
+        const double x = lambda * (double)(1 << ns);
+        if (x == (double)(int64_t)x) {
+            v.norm = 1;
+            v.na = (uint32_t)(int64_t)x;
+            v.ns = (uint32_t)ns;
+            const uint32_t lm = (0xFFFFu >> ns) & 0xFFFEu;
+            v.nmask = lm | (lm << 16);
+            v.nb2 = pack2(-2 * beta, -2 * beta);
+            v.q2 = pack2(2 * Q, 2 * Q);
+            return true;
+        }
+    }
+    return false;
+}
 
 cudaError_t res_occupancy_any(const ldpc_code *c, const ldpc_decode_params *p, const struct Plan &pl, int *blocks) {
     return res_occupancy(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.kind, pl.smem,
@@ -559,25 +588,32 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         return fail(LDPC_ERR_INVALID_ARG, "bad msg_format %d", p->msg_format);
     if (p->variant != LDPC_MINSUM_OFFSET && p->variant != LDPC_MINSUM_NORMALIZED)
         return fail(LDPC_ERR_INVALID_ARG, "bad variant %d", p->variant);
+    const float alpha0 = p->variant == LDPC_MINSUM_NORMALIZED ? p->alpha : 1.f;
+    for (int k = 0; p->alpha_per_iter && k < p->max_iter; ++k)
+        if (!(p->alpha_per_iter[k] > 0.f && p->alpha_per_iter[k] <= 1.f))
+            return fail(LDPC_ERR_INVALID_ARG, "alpha_per_iter[%d] must be in (0,1]", k);
+    if (p->variant == LDPC_MINSUM_NORMALIZED && !(p->alpha > 0.f && p->alpha <= 1.f))
+        return fail(LDPC_ERR_INVALID_ARG, "alpha must be in (0,1]");
     if (p->llr_type == LDPC_LLR_F32) {
         if (p->msg_format == LDPC_MSG_1BIT) return fail(LDPC_ERR_UNSUPPORTED, "1-bit messages need integer LLRs");
         if (pl.sched == LDPC_SCHED_LAYERED)
             return fail(LDPC_ERR_UNSUPPORTED, "layered schedule is implemented for integer LLRs only");
         if (c->max_dc > 16) return fail(LDPC_ERR_UNSUPPORTED, "F32 path supports row degree <= 16 (max %d)", c->max_dc);
-        if (p->variant == LDPC_MINSUM_NORMALIZED) {
-            if (!(p->alpha > 0.f && p->alpha <= 1.f)) return fail(LDPC_ERR_INVALID_ARG, "alpha must be in (0,1]");
-            pl.alpha = p->alpha;
-            pl.betaf = 0.f;
-        } else {
-            if (!(p->offset_f >= 0.f)) return fail(LDPC_ERR_INVALID_ARG, "offset_f must be >= 0");
-            pl.alpha = 1.f;
-            pl.betaf = p->offset_f;
+        if (p->variant == LDPC_MINSUM_OFFSET && !(p->offset_f >= 0.f))
+            return fail(LDPC_ERR_INVALID_ARG, "offset_f must be >= 0");
+        pl.alpha = alpha0;
+        pl.betaf = p->variant == LDPC_MINSUM_OFFSET ? p->offset_f : 0.f;
+        if (p->alpha_per_iter || p->offset_f_per_iter) {
+            for (int k = 0; k < p->max_iter; ++k) {
+                const float b = p->offset_f_per_iter ? p->offset_f_per_iter[k] : pl.betaf;
+                if (!(b >= 0.f)) return fail(LDPC_ERR_INVALID_ARG, "offset_f_per_iter[%d] must be >= 0", k);
+                pl.alphas.push_back(p->alpha_per_iter ? p->alpha_per_iter[k] : pl.alpha);
+                pl.betafs.push_back(b);
+            }
         }
         pl.path = PATH_STREAM_F;
         pl.tile = 32;
     } else if (p->llr_type == LDPC_LLR_I16 || p->llr_type == LDPC_LLR_I8) {
-        if (p->variant == LDPC_MINSUM_NORMALIZED && p->alpha != 1.f)
-            return fail(LDPC_ERR_UNSUPPORTED, "normalized min-sum with integer LLRs is not implemented (use F32)");
         if (p->offset_raw < 0 || p->offset_raw > 16383) return fail(LDPC_ERR_INVALID_ARG, "offset_raw out of range");
         if (c->max_dc > kMaxDC) return fail(LDPC_ERR_UNSUPPORTED, "integer paths support row degree <= %d (max %d)", kMaxDC, c->max_dc);
         pl.fmt = p->msg_format == LDPC_MSG_1BIT ? FMT_1BIT : FMT_C16;
@@ -588,6 +624,28 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
             return fail(LDPC_ERR_UNSUPPORTED, "2*Q*(max_dv+2) = %lld > 32767: posteriors would overflow 16-bit lanes",
                         (long long)2 * pl.Q * (c->max_dv + 2));
         pl.beta = p->offset_raw;
+        // integer variants (constant and per iteration); normalized needs a
+        // dyadic lambda = na / 2^ns (reading D27) and 2|q| na < 2^16 per lane
+        const int64_t qmax2 = (int64_t)2 * pl.Q * (c->max_dv + 2);
+        auto vark = [&](double lam, int b, VarK &v) -> ldpc_status {
+            if (b < 0 || b > 16383) return fail(LDPC_ERR_INVALID_ARG, "offset %d out of range", b);
+            if (!make_vark(lam, b, pl.Q, v))
+                return fail(LDPC_ERR_UNSUPPORTED, "integer normalized min-sum needs a dyadic lambda = a/2^s, s <= 8 "
+                                                  "(got %.9g)", lam);
+            if (v.norm && (int64_t)v.na * qmax2 >= 65536)
+                return fail(LDPC_ERR_UNSUPPORTED, "lambda = %u/2^%u too fine for 16-bit lanes at Q=%d", v.na, v.ns, pl.Q);
+            return LDPC_OK;
+        };
+        ldpc_status vs = vark(alpha0, pl.beta, pl.vk);
+        if (vs != LDPC_OK) return vs;
+        if (p->alpha_per_iter || p->offset_per_iter) {
+            pl.vks.resize((size_t)p->max_iter);
+            for (int k = 0; k < p->max_iter; ++k) {
+                vs = vark(p->alpha_per_iter ? p->alpha_per_iter[k] : alpha0,
+                          p->offset_per_iter ? p->offset_per_iter[k] : pl.beta, pl.vks[(size_t)k]);
+                if (vs != LDPC_OK) return vs;
+            }
+        }
         // LDPC_FORCE_STREAM=1 (test hook) routes integer decodes through the streaming kernels
         const char *force = getenv("LDPC_FORCE_STREAM");
         pl.path = (c->res_ok && !(force && force[0] == '1') && pl.sched == LDPC_SCHED_SINGLESCAN) ? PATH_RESIDENT
@@ -606,6 +664,10 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         return fail(LDPC_ERR_INVALID_ARG, "bad llr_type %d", p->llr_type);
     }
     const int64_t npairs = (F + 1) / 2;
+    if (pl.path == PATH_RESIDENT && !pl.vks.empty() && p->max_iter > kMaxSched) {
+        if (pl.lay) return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
+        pl.path = PATH_STREAM_I;                         // the streaming kernels take any schedule length
+    }
     if (pl.path == PATH_RESIDENT) {
         // flooding uses the barrier-free atomic kernel when the biased 16-bit lanes cannot
         // overflow: 2 Q (max_dv + 1) < 0x4000 (k_resident_atom.cuh); LDPC_RES_BATCHED=1
@@ -678,8 +740,9 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.K = p->max_iter;
     a.Qsat = pl.Q;
     a.wpf = (c->N + 31) / 32;
-    a.nbeta2p1 = pack2(1 - 2 * pl.beta, 1 - 2 * pl.beta);
-    a.q2p1 = pack2(2 * pl.Q + 1, 2 * pl.Q + 1);
+    a.vk = pl.vk;
+    a.nsched = (int)pl.vks.size();
+    for (size_t k = 0; k < pl.vks.size(); ++k) a.vk_sched[k] = pl.vks[k];
     a.llr = llr;
     a.hard_bits = hb;
     a.post = (int16_t *)post;
@@ -717,8 +780,7 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     a.K = p->max_iter;
     a.Qsat = pl.Q;
     a.wpf = (c->N + 31) / 32;
-    a.nbeta2p1 = pack2(1 - 2 * pl.beta, 1 - 2 * pl.beta);
-    a.q2p1 = pack2(2 * pl.Q + 1, 2 * pl.Q + 1);
+    a.vk = pl.vk;
     a.alpha = pl.alpha;
     a.rk = make_regk();
     a.beta = pl.betaf;
@@ -746,6 +808,9 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     r.max_dc = c->max_dc;
     r.ntiles = pl.ntiles;
     r.flags_bytes = pl.off_it - pl.off_synd;
+    r.vk_sched = pl.vks.empty() ? nullptr : pl.vks.data();
+    r.alpha_sched = pl.alphas.empty() ? nullptr : pl.alphas.data();
+    r.beta_sched = pl.betafs.empty() ? nullptr : pl.betafs.data();
     // L2 chunking (opt-in, LDPC_CHUNK_TILES = tiles per chunk): measured SLOWER on cfg4/cfg5
     // at every chunk size (the streaming kernels are issue/latency-bound,
     // not HBM-bound, and chunks add launch tails), so all tiles run together by default.

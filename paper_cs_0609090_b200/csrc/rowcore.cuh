@@ -18,6 +18,7 @@
 //          s bit = 1 means L_mn < 0; "idx" bit = 1 means n is an argmin (n = ñ_m).  dc <= 8.
 #pragma once
 #include "args.cuh"
+#include "rowcore_types.cuh"
 #include "simd16.cuh"
 
 namespace ldpc {
@@ -93,15 +94,27 @@ __device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, u
     m2 = a2[0];
 }
 
+// doubled magnitude of the variant from m~ = 2|q| - [q < 0]
+__device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const RegK &k) {
+    if (!v.norm) {
+        // relu(min(m~ + 1 - 2 beta, 2Q + 1)) with the low bit cleared is exact (m~ in {2|q|-1, 2|q|})
+        return vaddmin_relu(m, v.nbeta2p1, v.q2p1) & 0xFFFEFFFEu;
+    }
+    const uint32_t t = __vadd2(m, 0x00010001u) & 0xFFFEFFFEu;   // 2|q| per lane
+    uint32_t x;                                                   // 2|q| na per lane (no lane overflow: planner)
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(t), "r"(v.na), "r"(k.zero));
+    x = (x >> v.ns) & v.nmask;                                    // 2 floor(na |q| / 2^ns)
+    return vaddmin_relu(x, v.nb2, v.q2);
+}
+
 // New compact state from the q's and the new messages L^(k)_mn (doubled) to be
 // accumulated into Z^(k)_n:
 //   A = min(max(min1 - beta, 0), Q), B = min(max(min2 - beta, 0), Q)  (readings D5, D6)
 //   ñ = argmin |q| (ties: any minimiser -- unobservable, A = B then; reading D3)
 //   s_mn = prod_{n' != n} sgn(q_mn')  (sgn(0) = +1, reading D1)
-// nbeta2p1 = packed (1 - 2 beta), q2p1 = packed (2Q + 1).
 template <int DC>
-__device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbeta2p1, uint32_t q2p1, RowState &st,
-                                          uint32_t (&r)[DC], const RegK &k) {
+__device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &vk, RowState &st, uint32_t (&r)[DC],
+                                          const RegK &k) {
     uint32_t mt[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) mt[j] = vmax(q[j], fnot(q[j], k));   // 2|q| - [q<0]
@@ -111,10 +124,8 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], uint32_t nbet
 #pragma unroll
     for (int j = 1; j < DC; ++j) par ^= q[j];
     const uint32_t Pm = signmask(par);                          // product of all signs < 0
-    // A = clamp(2|q|min - 2 beta, 0, 2Q) on doubled values: with m~ in {2|q|-1, 2|q|},
-    // relu(min(m~ + 1 - 2 beta, 2Q + 1)) with the low bit cleared is exact (one VIADDMNMX + LOP3).
-    const uint32_t A = vaddmin_relu(m1, nbeta2p1, q2p1) & 0xFFFEFFFEu;
-    const uint32_t B = vaddmin_relu(m2, nbeta2p1, q2p1) & 0xFFFEFFFEu;
+    const uint32_t A = variant_mag(m1, vk, k);
+    const uint32_t B = variant_mag(m2, vk, k);
     const uint32_t nA = vneg(A, k), nB = vneg(B, k);
     // message for an edge whose own q is >= 0 carries the sign of the full product
     const uint32_t Apos = sel(Pm, nA, A), Aneg = sel(Pm, A, nA);

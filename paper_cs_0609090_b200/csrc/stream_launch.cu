@@ -45,6 +45,12 @@ cudaError_t launch(F f, int32_t *n) {
     ++*n;
     return cudaGetLastError();
 }
+// the variant of iteration k (lambda_k, beta_k) for the launches of k
+void set_iteration(StreamArgs &c, const StreamRun &r, int k) {
+    if (r.vk_sched) c.vk = r.vk_sched[k - 1];
+    if (r.alpha_sched) c.alpha = r.alpha_sched[k - 1];
+    if (r.beta_sched) c.beta = r.beta_sched[k - 1];
+}
 }  // namespace
 
 cudaError_t count_errors_launch(int64_t nframes, int wpf, const uint32_t *hb, const uint8_t *ok, const int32_t *it,
@@ -103,6 +109,7 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
         const dim3 gp((unsigned)((a.M + kPipeRB - 1) / kPipeRB), (unsigned)nt);
         const dim3 gr((unsigned)std::max(1, (a.M + rows_per_block - 1) / rows_per_block), (unsigned)nt);
         for (int k = 1; k <= r.max_iter && use_pipe; ++k) {
+            set_iteration(c, r, k);
             if (pair) {
                 if (r.fmt == FMT_C16) {
                     if (es) e = launch([&] { k_stream_pipe<true, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
@@ -123,6 +130,7 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
             }
         }
         for (int k = 1; k <= r.max_iter && !use_pipe; ++k) {
+            set_iteration(c, r, k);
             if (pair) {
                 if (r.fmt == FMT_C16) {
                     if (es) e = launch([&] { k_stream_iter_i<FMT_C16, true><<<gr, 256, 0, s>>>(c, k); }, nl);
@@ -160,7 +168,8 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
 // Two-scan min-sum (k_twoscan.cuh): ingest, Z_mn init, then per iteration the
 // horizontal and vertical scans; early stop checks H x^ = 0 on Z^(k) after each
 // iteration (and on Z^(0) first, reading D10) with the shared syndrome/freeze kernels.
-cudaError_t twoscan_run(const StreamArgs &a, const TwoScanArgs &t, const StreamRun &r, cudaStream_t s, int32_t *nl) {
+cudaError_t twoscan_run(const StreamArgs &a0, const TwoScanArgs &t, const StreamRun &r, cudaStream_t s, int32_t *nl) {
+    StreamArgs a = a0;
     cudaError_t e;
     if ((e = cudaMemsetAsync(a.synd, 0, r.flags_bytes, s)) != cudaSuccess) return e;
     const bool pair = r.pair, es = r.es;
@@ -193,6 +202,7 @@ cudaError_t twoscan_run(const StreamArgs &a, const TwoScanArgs &t, const StreamR
         if ((e = syndrome(0)) != cudaSuccess || (e = freeze(1)) != cudaSuccess) return e;
     }
     for (int k = 1; k <= r.max_iter; ++k) {
+        set_iteration(a, r, k);
         e = pair ? launch([&] { k_ts_check<true><<<gm, 256, 0, s>>>(a, t); }, nl)
                  : launch([&] { k_ts_check<false><<<gm, 256, 0, s>>>(a, t); }, nl);
         if (e != cudaSuccess) return e;

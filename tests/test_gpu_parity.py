@@ -223,7 +223,7 @@ def test_unsupported_requests():
         dec.workspace(8, P.make_params(5, 0, P.LDPC_MINSUM_OFFSET, 1, 0, 1.0, 600, P.LDPC_LLR_I16, P.LDPC_MSG_1BIT))
     assert e.value.status == P.LDPC_ERR_UNSUPPORTED
     with pytest.raises(P.LdpcError) as e:
-        dec.workspace(8, P.make_params(5, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0, 0.75, 0, P.LDPC_LLR_I16))
+        dec.workspace(8, P.make_params(5, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0, 0.7, 0, P.LDPC_LLR_I16))   # not dyadic
     assert e.value.status == P.LDPC_ERR_UNSUPPORTED
     with pytest.raises(P.LdpcError) as e:
         dec.workspace(8, P.make_params(0, 0))

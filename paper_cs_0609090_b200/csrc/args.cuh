@@ -43,6 +43,7 @@ struct ResArgs {
     const int32_t *bptr;              // CSR: batch b = schedule positions [bptr[b], bptr[b+1])
     const uint32_t *colT;             // CSR: [kMaxDC][M] byte offsets 4*n of each edge
     const uint8_t *dcT;               // CSR: degree per schedule position
+    const uint8_t *coldeg;            // [N] column degrees d_v(n) (barrier-free kernel's accumulator start)
     int Z;                            // QC circulant size
     int group_threads;                // QC: threads per group (128 with two groups)
     uint32_t tmem_cols;               // TMEM columns allocated per CTA

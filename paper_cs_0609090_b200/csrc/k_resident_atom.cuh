@@ -44,18 +44,18 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
 #pragma unroll
     for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
     if (ES) synd |= row_parity<DC>(L, a.rk, a.cpar);
-    uint32_t q[DC];
+    uint32_t q[DC];                                                      // q_mn + 0x8000 per lane
     if (first_iter) {
 #pragma unroll
-        for (int j = 0; j < DC; ++j) q[j] = __vadd2(L[j], 0xC000C000u);   // L^(0)_mn = 0
+        for (int j = 0; j < DC; ++j) q[j] = fadd32(L[j], 0x40004000u, a.rk);   // L^(0)_mn = 0
     } else {
-        rebuild_q<DC, true>(L, st, q, a.rk);                               // Z_n - L^(k-1)_mn
+        rebuild_q_b8<DC>(L, st, q, a.rk);                                  // Z_n - L^(k-1)_mn
     }
-    uint32_t rn[DC];
-    new_state<DC>(q, vk, st, rn, a.rk);
+    uint32_t rn[DC];                                                     // V(L^(k)_mn) + 0x8000
+    new_state<DC, true>(q, vk, st, rn, a.rk);
 #pragma unroll
     for (int j = 0; j < DC; ++j)                                          // Z^(k)_n += L^(k)_mn
-        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(vform(rn[j], a.rk)) : "memory");
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");
 }
 
 template <int DC, bool ES, int FMT>
@@ -106,8 +106,8 @@ __device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, cons
     }
 }
 
-// Ingest one frame pair: saturate to +-Q, double, bias, pack; write the Z^(0) slot (for
-// the TMA restarts) and both shared buffers.  Four variables per thread per step with
+// Ingest one frame pair: saturate to +-Q, double, bias, pack; write the Z^(0) slot (the
+// accumulator start, restored by the TMA restarts) and both shared buffers.  Four variables per thread per step with
 // all eight loads issued first (the loads are latency-bound, not bandwidth-bound).
 template <typename TIN>
 __device__ __forceinline__ void atom_ingest(const ResArgs &a, const TIN *__restrict__ lo, const TIN *__restrict__ hi,
@@ -128,9 +128,13 @@ __device__ __forceinline__ void atom_ingest(const ResArgs &a, const TIN *__restr
             if (n < a.Np) {
                 const int l = max(-a.Qsat, min(a.Qsat, zl[u])), h = max(-a.Qsat, min(a.Qsat, zh[u]));
                 const uint32_t v = pack2(2 * l + kAtomBias, 2 * h + kAtomBias);
-                __stcg(z0w + n, v);
+                // accumulator start: every one of the dv_n messages arrives as V(L) + 0x8000
+                // (new_state<B8>), so start dv_n * 0x8000 lower (exact 32-bit arithmetic)
+                const uint32_t dv = n < a.N ? (uint32_t)__ldg(a.coldeg + n) : 0u;
+                const uint32_t acc = v - dv * 0x8000u;
+                __stcg(z0w + n, acc);
                 buf0[n] = v;
-                buf1[n] = v;
+                buf1[n] = acc;
             }
         }
     }

@@ -70,6 +70,7 @@ struct ldpc_code {
     uint32_t *d_rowtab = nullptr;   // [M][8] padded column table (streaming kernels)
     // variable->check addressing, used only by the two-scan baseline
     int32_t *d_vptr = nullptr, *d_vedge = nullptr;
+    uint8_t *d_coldeg = nullptr;     // [N] column degrees (max 255)
     // resident schedule
     bool qc = false;
     int Z = 0, mb = 0, nb = 0;
@@ -160,6 +161,7 @@ static void free_code(ldpc_code *c) {
     cudaFree(c->d_col_idx);
     cudaFree(c->d_rowtab);
     cudaFree(c->d_vptr);
+    cudaFree(c->d_coldeg);
     cudaFree(c->d_vedge);
     delete c->qtab;
     cudaFree(c->d_bptr);
@@ -218,7 +220,10 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                 const int n = desc->col_idx[e];
                 vedge[(size_t)vptr[n] + fill[n]++] = e;
             }
-        if ((st = upload(&c->d_vptr, vptr.data(), vptr.size())) != LDPC_OK ||
+        std::vector<uint8_t> cd((size_t)N);
+        for (int n = 0; n < N; ++n) cd[(size_t)n] = (uint8_t)std::min(coldeg[(size_t)n], 255);
+        if ((st = upload(&c->d_coldeg, cd.data(), cd.size())) != LDPC_OK ||
+            (st = upload(&c->d_vptr, vptr.data(), vptr.size())) != LDPC_OK ||
             (st = upload(&c->d_vedge, vedge.data(), vedge.size())) != LDPC_OK) {
             free_code(c);
             return st;
@@ -756,6 +761,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.colT = natural ? c->d_colT_lay : c->d_colT;
     a.dcT = natural ? c->d_dcT_lay : c->d_dcT;
     a.cpar = pl.kind == RES_ATOM ? 0xBFFEBFFFu : 0xFFFEFFFFu;
+    a.coldeg = c->d_coldeg;
     a.Z = c->Z;
     a.group_threads = c->group_threads;
     a.tmem_cols = pl.tmem_cols;

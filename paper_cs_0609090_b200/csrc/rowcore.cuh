@@ -61,29 +61,61 @@ __device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowStat
     }
 }
 
+// B8 rebuild for the barrier-free resident kernel: L holds 2Z + 0x4000 per lane; the four
+// candidates 0x4000 -/+ A, B are formed by IMAD (lanes stay non-negative, no carries) and
+// q + 0x8000 = L + candidate is one 32-bit IMAD per edge (FMA pipe).
+template <int DC>
+__device__ __forceinline__ void rebuild_q_b8(const uint32_t (&L)[DC], const RowState &st, uint32_t (&q)[DC],
+                                             const RegK &k) {
+    uint32_t A, B, nA, nB;                                      // -L_old + 0x4000 for L_old = +A, +B, -A, -B
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(A) : "r"(st.A), "r"(k.m1), "r"(0x40004000u));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(B) : "r"(st.B), "r"(k.m1), "r"(0x40004000u));
+    nA = fadd32(st.A, 0x40004000u, k);
+    nB = fadd32(st.B, 0x40004000u, k);
+#pragma unroll
+    for (int i = 0; i < (DC + 1) / 2; ++i) {
+        const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte
+        const uint32_t wo = st.W << (3 - i);       // idx bits of pair i -> bit 7 of each byte
+        {
+            const uint32_t sm = prmt(ws, 0u, 0xAA88u), ix = prmt(wo, 0u, 0xAA88u);
+            q[2 * i] = fadd32(L[2 * i], sel(sm, sel(ix, nB, nA), sel(ix, B, A)), k);
+        }
+        if (2 * i + 1 < DC) {
+            const uint32_t sm = prmt(ws, 0u, 0xBB99u), ix = prmt(wo, 0u, 0xBB99u);
+            q[2 * i + 1] = fadd32(L[2 * i + 1], sel(sm, sel(ix, nB, nA), sel(ix, B, A)), k);
+        }
+    }
+}
+
 // Smallest and second smallest of DC packed values (with multiplicity), as a
 // pairwise tree: leaves (min, max), merges m1 = min(a1, b1),
 // m2 = min3(max(a1, b1), a2, b2).  Shorter dependency chains than a running scan.
-template <int DC>
+// U: values are unsigned 16-bit lanes (the 0x8000-biased domain of new_state<B8>).
+template <int DC, bool U = false>
 __device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, uint32_t &m2) {
     constexpr int NL = (DC + 1) / 2;
     uint32_t a1[NL], a2[NL];
 #pragma unroll
     for (int i = 0; i < DC / 2; ++i) {
-        a1[i] = vmin(v[2 * i], v[2 * i + 1]);
-        a2[i] = vmax(v[2 * i], v[2 * i + 1]);
+        a1[i] = U ? __vminu2(v[2 * i], v[2 * i + 1]) : vmin(v[2 * i], v[2 * i + 1]);
+        a2[i] = U ? __vmaxu2(v[2 * i], v[2 * i + 1]) : vmax(v[2 * i], v[2 * i + 1]);
     }
     if (DC & 1) {
         a1[NL - 1] = v[DC - 1];
-        a2[NL - 1] = 0x7FFF7FFFu;
+        a2[NL - 1] = U ? 0xFFFFFFFFu : 0x7FFF7FFFu;
     }
 #pragma unroll
     for (int n = NL; n > 1; n = (n + 1) / 2) {
 #pragma unroll
         for (int i = 0; i < n / 2; ++i) {
             const uint32_t x1 = a1[2 * i], y1 = a1[2 * i + 1];
-            a1[i] = vmin(x1, y1);
-            a2[i] = __vimin3_s16x2(vmax(x1, y1), a2[2 * i], a2[2 * i + 1]);
+            if (U) {
+                a1[i] = __vminu2(x1, y1);
+                a2[i] = __vimin3_u16x2(__vmaxu2(x1, y1), a2[2 * i], a2[2 * i + 1]);
+            } else {
+                a1[i] = vmin(x1, y1);
+                a2[i] = __vimin3_s16x2(vmax(x1, y1), a2[2 * i], a2[2 * i + 1]);
+            }
         }
         if (n & 1) {
             a1[n / 2] = a1[n - 1];
@@ -94,8 +126,10 @@ __device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, u
     m2 = a2[0];
 }
 
-// doubled magnitude of the variant from m~ = 2|q| - [q < 0]
+// doubled magnitude of the variant from m~ = 2|q| - [q < 0] (B8: m = m~ + 0x8000 per lane)
+template <bool B8 = false>
 __device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const RegK &k) {
+    if (B8) m ^= 0x80008000u;                                     // unbias (the DPX add must not wrap)
     if (!v.norm) {
         // relu(min(m~ + 1 - 2 beta, 2Q + 1)) with the low bit cleared is exact (m~ in {2|q|-1, 2|q|})
         return vaddmin_relu(m, v.nbeta2p1, v.q2p1) & 0xFFFEFFFEu;
@@ -112,31 +146,48 @@ __device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const
 //   A = min(max(min1 - beta, 0), Q), B = min(max(min2 - beta, 0), Q)  (readings D5, D6)
 //   ñ = argmin |q| (ties: any minimiser -- unobservable, A = B then; reading D3)
 //   s_mn = prod_{n' != n} sgn(q_mn')  (sgn(0) = +1, reading D1)
-template <int DC>
+//
+// B8 = true (barrier-free resident kernel): q arrives as q + 0x8000 per lane (unsigned),
+// so 32-bit IMADs produced it without lane carries; magnitudes and minima are then
+// unsigned, the per-lane sign mask is [q >= 0] (bit 15), and the returned messages are
+// "V form + 0x8000": r ^ 0x8000 in the low lane == V(r) + 0x8000 as a 32-bit integer, so a
+// 32-bit RED adds them exactly (the accumulator start value is lowered by dv_n 0x8000).
+template <int DC, bool B8 = false>
 __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &vk, RowState &st, uint32_t (&r)[DC],
                                           const RegK &k) {
     uint32_t mt[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) mt[j] = vmax(q[j], fnot(q[j], k));   // 2|q| - [q<0]
+    for (int j = 0; j < DC; ++j)                                 // 2|q| - [q<0]  (B8: + 0x8000)
+        mt[j] = B8 ? __vmaxu2(q[j], fnot(q[j], k)) : vmax(q[j], fnot(q[j], k));
     uint32_t m1, m2;
-    two_min<DC>(mt, m1, m2);
+    two_min<DC, B8>(mt, m1, m2);
     uint32_t par = q[0];
 #pragma unroll
     for (int j = 1; j < DC; ++j) par ^= q[j];
+    // B8: bit 15 of q_b is [q >= 0], so the XOR counts non-negative q's; the product is
+    // negative iff the count of negative ones, DC - that, is odd
+    if (B8 && (DC & 1)) par ^= 0x80008000u;
     const uint32_t Pm = signmask(par);                          // product of all signs < 0
-    const uint32_t A = variant_mag(m1, vk, k);
-    const uint32_t B = variant_mag(m2, vk, k);
-    const uint32_t nA = vneg(A, k), nB = vneg(B, k);
+    const uint32_t A = variant_mag<B8>(m1, vk, k);
+    const uint32_t B = variant_mag<B8>(m2, vk, k);
+    uint32_t nA = vneg(A, k), nB = vneg(B, k), Ac = A, Bc = B;
+    if (B8) {                                                    // message candidates ^ 0x8000 (low lane)
+        nA = __vadd2(fnot(A, k), 0x00018001u);
+        nB = __vadd2(fnot(B, k), 0x00018001u);
+        Ac = fadd32(A, 0x00008000u, k);
+        Bc = fadd32(B, 0x00008000u, k);
+    }
     // message for an edge whose own q is >= 0 carries the sign of the full product
-    const uint32_t Apos = sel(Pm, nA, A), Aneg = sel(Pm, A, nA);
-    const uint32_t Bpos = sel(Pm, nB, B), Bneg = sel(Pm, B, nB);
+    const uint32_t Apos = sel(Pm, nA, Ac), Aneg = sel(Pm, Ac, nA);
+    const uint32_t Bpos = sel(Pm, nB, Bc), Bneg = sel(Pm, Bc, nB);
     const uint32_t cm1 = fnot(m1, k);                           // -m1 - 1
     uint32_t W = 0, sqp = 0, ixp = 0;
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         const uint32_t ix = vaddmin(mt[j], cm1, k.zero);          // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
-        const uint32_t sq = signmask(q[j]);                     // 0xFFFF: q < 0
-        r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
+        const uint32_t sq = signmask(q[j]);                     // 0xFFFF: q < 0  (B8: q >= 0)
+        if (B8) r[j] = sel(sq, sel(ix, Bpos, Apos), sel(ix, Bneg, Aneg));
+        else r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
         if ((j & 1) == 0) {
             sqp = sq;
             ixp = ix;
@@ -149,7 +200,8 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
             W |= prmt(ixp, ix, 0x6240u) & (0x10101010u << (j >> 1));
         }
     }
-    W ^= Pm & 0x0F0F0F0Fu;                                      // s = sgn(q) * product
+    if (B8) W ^= ~Pm & 0x0F0F0F0Fu;                             // s = sgn(q) * product ([q>=0] bits stored)
+    else W ^= Pm & 0x0F0F0F0Fu;                                 // s = sgn(q) * product
     st.A = A;
     st.B = B;
     st.W = W;

@@ -90,8 +90,8 @@ struct ldpc_code {
     // barrier-free flooding kernel (k_resident_atom.cuh): row slots per thread
     int nbatch_atom = 0, res_threads_atom = 0;
     QcTab *qtab_atom = nullptr;
-    cudaStream_t aux[2] = {nullptr, nullptr};
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t aux[4] = {nullptr, nullptr, nullptr, nullptr};      // host-API pipeline streams
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
 // ------------------------------------------------------------------ create
@@ -704,7 +704,15 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         if (getenv("LDPC_DEBUG")) fprintf(stderr, "[ldpc] occupancy API: %d blocks/SM\n", blocks);
         blocks = std::min(blocks, (int)(512 / cols));     // TMEM capacity per SM
         if (blocks < 1) return fail(LDPC_ERR_UNSUPPORTED, "resident kernel does not fit on an SM");
-        pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)blocks * c->sm_count);
+        // One frame pair per CTA (grid = pairs): the block scheduler then balances the SMs
+        // dynamically.  Measured against a persistent grid of `blocks x SMs` CTAs looping over
+        // pairs: cfg2 2.91 -> 2.67 ms, cfg3 40.6 -> 35.9 ms.  The price is one Z^(0) slot per
+        // pair in the workspace (the size of the int16 input).  LDPC_RES_GRID_MULT=m caps the
+        // grid at m x resident slots (tuning hook; the kernel loops over pairs).
+        pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)1 << 30);
+        if (const char *ge = getenv("LDPC_RES_GRID_MULT"))
+            pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1),
+                                             (int64_t)blocks * c->sm_count * std::max(1, atoi(ge)));
         pl.slot_words = ((size_t)c->N + 63) & ~(size_t)63;
         if (getenv("LDPC_DEBUG"))
             fprintf(stderr, "[ldpc] resident: threads=%d smem=%zu tmem_cols=%u need=%u occ_blocks=%d grid=%d batches=%d\n",
@@ -888,13 +896,19 @@ extern "C" ldpc_status ldpc_decode_batch(const ldpc_code *code, const ldpc_decod
 namespace {
 struct HostLayout {
     int64_t chunk = 0, nchunks = 0;
+    int nstreams = 1;
     size_t elt = 2, post_elt = 2, wpf = 0;
-    size_t off_llr = 0, off_hb = 0, off_post = 0, off_ok = 0, off_it = 0, off_ws[2] = {0, 0};
+    size_t off_llr = 0, off_hb = 0, off_post = 0, off_ok = 0, off_it = 0, off_ws[4] = {0, 0, 0, 0};
     size_t chunk_ws = 0, total = 0;
 };
 
+// Host-buffer decode: H2D copy, decode and D2H copies of frame chunks round-robin on up to
+// four streams, so the copies of one chunk overlap the decode of others.  Chunks of about
+// F/16 frames (>= 512) on 4 streams measured best on cfg2 (e2e 7.4 -> 8.6 Gbit/s vs 4 x 2);
+// LDPC_HOST_CHUNKS / LDPC_HOST_STREAMS override (tuning hooks).
 ldpc_status host_layout(const ldpc_code *c, int64_t F, const ldpc_decode_params *p, HostLayout &h) {
-    h.nchunks = F >= 4096 ? 4 : 1;
+    h.nchunks = std::max<int64_t>(1, std::min<int64_t>(16, F / 512));
+    if (const char *e = getenv("LDPC_HOST_CHUNKS")) h.nchunks = std::max(1, atoi(e));
     h.chunk = (F + h.nchunks - 1) / h.nchunks;
     h.chunk = ((h.chunk + 63) / 64) * 64;
     if (h.chunk == 0) h.chunk = 64;
@@ -911,9 +925,10 @@ ldpc_status host_layout(const ldpc_code *c, int64_t F, const ldpc_decode_params 
     h.off_post = off; off += align256((size_t)F * c->N * h.post_elt);
     h.off_ok = off; off += align256((size_t)F);
     h.off_it = off; off += align256((size_t)F * 4);
+    h.nstreams = (int)std::min<int64_t>(h.nchunks, 4);
+    if (const char *e = getenv("LDPC_HOST_STREAMS")) h.nstreams = std::max(1, std::min(4, atoi(e)));
     h.chunk_ws = pl.ws_bytes;
-    h.off_ws[0] = off; off += align256(pl.ws_bytes);
-    h.off_ws[1] = off; off += align256(pl.ws_bytes);
+    for (int i = 0; i < h.nstreams; ++i) { h.off_ws[i] = off; off += align256(pl.ws_bytes); }
     h.total = off;
     return LDPC_OK;
 }
@@ -953,11 +968,12 @@ extern "C" ldpc_status ldpc_decode_batch_host(const ldpc_code *code, const ldpc_
     char *w = (char *)workspace;
     cudaStream_t us = (cudaStream_t)stream;
     CUDA_TRY(cudaEventRecord(code->ev[0], us));
-    for (auto s : code->aux) CUDA_TRY(cudaStreamWaitEvent(s, code->ev[0], 0));
+    for (int i = 0; i < h.nstreams; ++i) CUDA_TRY(cudaStreamWaitEvent(code->aux[i], code->ev[0], 0));
     int32_t launches = 0;
     const int N = code->N;
     for (int64_t ci = 0; ci < h.nchunks; ++ci) {
-        cudaStream_t s = code->aux[ci & 1];
+        const int si = (int)(ci % h.nstreams);
+        cudaStream_t s = code->aux[si];
         const int64_t f0 = ci * h.chunk, nf = std::min<int64_t>(h.chunk, n_frames - f0);
         char *dl = w + h.off_llr + (size_t)f0 * N * h.elt;
         uint32_t *dhb = (uint32_t *)(w + h.off_hb) + (size_t)f0 * h.wpf;
@@ -969,7 +985,7 @@ extern "C" ldpc_status ldpc_decode_batch_host(const ldpc_code *code, const ldpc_
         Plan pl;
         if ((st = make_plan(code, nf, params, pl)) != LDPC_OK) return st;
         g_launches = 0;
-        st = decode_device(code, params, nf, dl, dhb, dpost, dok, dit, w + h.off_ws[ci & 1], h.chunk_ws, s, pl);
+        st = decode_device(code, params, nf, dl, dhb, dpost, dok, dit, w + h.off_ws[si], h.chunk_ws, s, pl);
         if (st != LDPC_OK) return st;
         launches += g_launches;
         CUDA_TRY(cudaMemcpyAsync(hard_bits_host + (size_t)f0 * h.wpf, dhb, (size_t)nf * h.wpf * 4,
@@ -981,10 +997,10 @@ extern "C" ldpc_status ldpc_decode_batch_host(const ldpc_code *code, const ldpc_
         if (dit)
             CUDA_TRY(cudaMemcpyAsync(iterations_used_host + f0, dit, (size_t)nf * 4, cudaMemcpyDeviceToHost, s));
     }
-    CUDA_TRY(cudaEventRecord(code->ev[1], code->aux[0]));
-    CUDA_TRY(cudaEventRecord(code->ev[2], code->aux[1]));
-    CUDA_TRY(cudaStreamWaitEvent(us, code->ev[1], 0));
-    CUDA_TRY(cudaStreamWaitEvent(us, code->ev[2], 0));
+    for (int i = 0; i < h.nstreams; ++i) {
+        CUDA_TRY(cudaEventRecord(code->ev[1 + i], code->aux[i]));
+        CUDA_TRY(cudaStreamWaitEvent(us, code->ev[1 + i], 0));
+    }
     g_launches = launches;
     return LDPC_OK;
 }

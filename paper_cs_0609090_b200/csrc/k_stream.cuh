@@ -27,20 +27,25 @@ __device__ __forceinline__ uint32_t from_vform(uint32_t v) { return v + ((v & 0x
 // fp32 check row (one frame per lane), branch-free.  Reading D11: one RN rounding
 // per operation (__fsub_rn/__fmul_rn, no FMA).  Two minima with multiplicity:
 // m2 = min(m2, max(m1, x)), m1 = min(m1, x), argmin on strict '<' (lowest position).
+// State word W: bit j = sign of L_mn (1 = negative), bit 16 + ñ set (one-hot position).
+// Selections work on the IEEE bit patterns: |L| = A or B is A + [j == ñ] (B - A) as a
+// 32-bit integer (exact; IMAD on the FMA pipe), the sign is an XOR of bit 31.
 template <int DC>
 __device__ __forceinline__ void f32_row(const float (&L)[DC], bool first_iter, float A0, float B0, uint32_t W0,
                                         float alpha, float beta, float &A, float &B, uint32_t &Wn, float (&r)[DC]) {
+    static_assert(DC <= 16, "one-hot position bits 16..31");
     float q[DC];
     if (first_iter) {
 #pragma unroll
         for (int j = 0; j < DC; ++j) q[j] = L[j];                    // L^(0)_mn = 0
     } else {
-        const int idx0 = (int)(W0 >> 16);
+        const uint32_t a0 = __float_as_uint(A0), db = __float_as_uint(B0) - a0;
 #pragma unroll
         for (int j = 0; j < DC; ++j) {
-            const float mag = (j == idx0) ? B0 : A0;                 // f(A,B,n,ñ)
-            const float lold = ((W0 >> j) & 1u) ? -mag : mag;        // s_mn f(...)
-            q[j] = __fsub_rn(L[j], lold);                            // Z_n' - L_mn'  (D8)
+            const uint32_t isel = (W0 << (15 - j)) >> 31;            // [n == ñ]
+            const uint32_t mag = isel * db + a0;                     // f(A,B,n,ñ)
+            const uint32_t lold = mag ^ ((W0 << (31 - j)) & 0x80000000u);   // s_mn f(...)
+            q[j] = __fsub_rn(L[j], __uint_as_float(lold));           // Z_n' - L_mn'  (D8)
         }
     }
     float m1 = fabsf(q[0]), m2 = __int_as_float(0x7f800000);
@@ -58,11 +63,14 @@ __device__ __forceinline__ void f32_row(const float (&L)[DC], bool first_iter, f
     A = fmaxf(__fsub_rn(__fmul_rn(alpha, m1), beta), 0.0f);
     B = fmaxf(__fsub_rn(__fmul_rn(alpha, m2), beta), 0.0f);
     const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;       // s = prod of the others' signs
-    Wn = sg | ((uint32_t)i1 << 16);
+    const uint32_t oh = 0x10000u << i1;
+    Wn = sg | oh;
+    const uint32_t a1 = __float_as_uint(A), db1 = __float_as_uint(B) - a1;
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        const float mag = (j == i1) ? B : A;
-        r[j] = ((sg >> j) & 1u) ? -mag : mag;
+        const uint32_t isel = (oh << (15 - j)) >> 31;
+        const uint32_t mag = isel * db1 + a1;
+        r[j] = __uint_as_float(mag ^ ((sg << (31 - j)) & 0x80000000u));
     }
 }
 
@@ -432,46 +440,17 @@ __device__ __forceinline__ void stream_rows_f(const StreamArgs &a, int lane, con
             for (int j = 0; j < DC; ++j) p ^= L[r][j] <= 0.0f ? 1u : 0u;
             synd |= p;
         }
-        float q[DC];
-        if (first_iter) {
-#pragma unroll
-            for (int j = 0; j < DC; ++j) q[j] = L[r][j];
-        } else {
-            const int idx0 = (int)(W0[r] >> 16);
-#pragma unroll
-            for (int j = 0; j < DC; ++j) {
-                const float mag = (j == idx0) ? B0[r] : A0[r];                // f(A,B,n,ñ)
-                const float lold = ((W0[r] >> j) & 1u) ? -mag : mag;          // s_mn f(...)
-                q[j] = __fsub_rn(L[r][j], lold);                               // Z_n' - L_mn'
-            }
-        }
-        float m1 = fabsf(q[0]), m2 = 0.0f;
-        int i1 = 0;
-        bool have2 = false;
-        uint32_t sq = q[0] < 0.0f ? 1u : 0u;
-#pragma unroll
-        for (int j = 1; j < DC; ++j) {
-            const float x = fabsf(q[j]);
-            sq |= (q[j] < 0.0f ? 1u : 0u) << j;
-            if (x < m1) { m2 = m1; have2 = true; m1 = x; i1 = j; }
-            else if (!have2 || x < m2) { m2 = x; have2 = true; }
-        }
-        const uint32_t par = __popc(sq) & 1u;
-        float A = __fsub_rn(__fmul_rn(a.alpha, m1), a.beta);
-        A = A < 0.0f ? 0.0f : A;
-        float B = __fsub_rn(__fmul_rn(a.alpha, m2), a.beta);
-        B = B < 0.0f ? 0.0f : B;
-        const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;         // s = prod of the others
+        float A, B, rr[DC];
+        uint32_t Wn;
+        f32_row<DC>(L[r], first_iter, first_iter ? 0.f : A0[r], first_iter ? 0.f : B0[r], first_iter ? 0u : W0[r],
+                    a.alpha, a.beta, A, B, Wn, rr);
         const size_t so = (size_t)m[r] * 32 + lane;
         __stcg(stt + so, __float_as_uint(A));
         __stcg(stt + ss + so, __float_as_uint(B));
-        __stcg(stt + 2 * ss + so, sg | ((uint32_t)i1 << 16));
+        __stcg(stt + 2 * ss + so, Wn);
         if (!frozen) {
 #pragma unroll
-            for (int j = 0; j < DC; ++j) {
-                const float mag = (j == i1) ? B : A;
-                atomicAdd(Lat + off[r][j], ((sg >> j) & 1u) ? -mag : mag);     // Z^(k)_n += L^(k)_mn
-            }
+            for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], rr[j]);   // Z^(k)_n += L^(k)_mn
         }
     }
 }

@@ -59,6 +59,7 @@ struct StreamArgs {
     float alpha, beta;           // fp32 variant: |L| <= max(alpha*min - beta, 0)
     const int32_t *row_ptr, *col_idx;
     const uint4 *rowtab;         // [M][2]: up to 8 column indices per row; dc in bits 28-31 of word 0 (15 = wider row)
+    const uint8_t *coldeg;       // [N] column degrees (integer path: accumulator start values)
     const void *llr;
     uint32_t *Z0;                // [tile][N][32]
     uint32_t *Lb[3];             // rotating posterior buffers [tile][N][32]

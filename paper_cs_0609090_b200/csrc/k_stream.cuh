@@ -11,18 +11,32 @@
 // iteration's launch (three rotating posterior buffers: read Z^(k-1),
 // accumulate Z^(k), initialise the buffer for Z^(k+1)).
 //
-// Integer path: two frames per lane (16x2 SIMD).  Accumulators are kept in
-// "V form" (value = hi * 65536 + lo as a 32-bit integer) so that a 32-bit
-// integer RED adds both 16-bit lanes exactly; gathers convert back to the
-// packed per-half form.  fp32 path: one frame per lane, RED.F32.
+// Integer path: two frames per lane (16x2 SIMD).  Posterior words hold 2Z + 0x4000 per
+// lane (non-negative lanes: the packed and the 32-bit "V form" hi*65536+lo coincide),
+// messages are added by a 32-bit RED as V(L) + 0x8000 (rowcore new_state<B8>) and each
+// accumulator starts d_v(n) * 0x8000 lower (the Z^(0) plane holds that start value), so
+// the sums are exact and the gathers read the words directly -- the same representation
+// as the barrier-free resident kernel (reading D26).  fp32 path: one frame per lane,
+// RED.F32.
 #pragma once
 #include "args.cuh"
 #include "rowcore.cuh"
 
 namespace ldpc {
 
-__device__ __forceinline__ uint32_t to_vform(uint32_t p) { return p - ((p & 0x8000u) << 1); }
-__device__ __forceinline__ uint32_t from_vform(uint32_t v) { return v + ((v & 0x8000u) << 1); }
+constexpr uint32_t kPairBias = 0x40004000u;      // 0x4000 per 16-bit lane
+constexpr uint32_t kParBiased = 0xBFFEBFFFu;     // row_parity constant for biased words
+
+// Early stop: frozen lanes (mask `keep`) must come out of an accumulation unchanged.
+// Every edge always adds 0x8000 to the low lane -- V(L) + 0x8000 for active lanes, a bare
+// 0x8000 for a frozen low lane (red_value) -- so every accumulator start is lowered by
+// d_v 0x8000 whatever the lanes' state, and a frame frozen between the start and the
+// accumulation cannot upset the other lane.  Start word: frozen lanes keep `old`, active
+// lanes restart from Z^(0) (P0 = start + d_v 0x8000).
+__device__ __forceinline__ uint32_t keep_start(uint32_t start, uint32_t old, uint32_t keep, uint32_t dv) {
+    return sel(keep, old, start + dv * 0x8000u) - dv * 0x8000u;
+}
+__device__ __forceinline__ uint32_t red_value(uint32_t rn, uint32_t keep) { return sel(keep, 0x00008000u, rn); }
 
 // fp32 check row (one frame per lane), branch-free.  Reading D11: one RN rounding
 // per operation (__fsub_rn/__fmul_rn, no FMA).  Two minima with multiplicity:
@@ -75,10 +89,11 @@ __device__ __forceinline__ void f32_row(const float (&L)[DC], bool first_iter, f
 }
 
 // -------------------------------------------------------------- integer path
-// ingest: user [F][N] -> Z0 (V form, doubled, saturated) and Lb[0] (packed form
-// for the first read is not needed: all buffers are V form), Lb[1] = Z0.
+// ingest: user [F][N] -> doubled, saturated, biased words P0 = 2Z^(0) + 0x4000 per lane.
+// Lb[0] = P0 (the posterior read by iteration 1); Z0 plane = Lb[1] = P0 - d_v 0x8000 (the
+// accumulator start, see above).  zpre = 0 (two-scan): Z0 plane = P0.
 template <typename TIN>
-__global__ void k_stream_ingest_i(const StreamArgs a) {
+__global__ void k_stream_ingest_i(const StreamArgs a, int zpre) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int f0 = tile * 64 + 2 * lane, f1 = f0 + 1;
     const TIN *llr = (const TIN *)a.llr;
@@ -86,11 +101,12 @@ __global__ void k_stream_ingest_i(const StreamArgs a) {
         int zl = 0, zh = 0;
         if (f0 < a.nframes) zl = max(-a.Qsat, min(a.Qsat, (int)llr[(size_t)f0 * a.N + n]));
         if (f1 < a.nframes) zh = max(-a.Qsat, min(a.Qsat, (int)llr[(size_t)f1 * a.N + n]));
-        const uint32_t v = to_vform(pack2(2 * zl, 2 * zh));
+        const uint32_t v = pack2(2 * zl + 0x4000, 2 * zh + 0x4000);
+        const uint32_t start = zpre ? v - (uint32_t)__ldg(a.coldeg + n) * 0x8000u : v;
         const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
-        a.Z0[idx] = v;
+        a.Z0[idx] = start;
         a.Lb[0][idx] = v;
-        a.Lb[1][idx] = v;
+        a.Lb[1][idx] = start;
     }
 }
 
@@ -152,22 +168,22 @@ __device__ __forceinline__ void stream_rows_i(const StreamArgs &a, int lane, con
 #pragma unroll
     for (int r = 0; r < NR; ++r)
 #pragma unroll
-        for (int j = 0; j < DC; ++j) L[r][j] = from_vform(__ldcg(Lpt + off[r][j]));
+        for (int j = 0; j < DC; ++j) L[r][j] = __ldcg(Lpt + off[r][j]);
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-        if (ES) synd |= row_parity<DC>(L[r], a.rk);
-        uint32_t q[DC];
+        if (ES) synd |= row_parity<DC>(L[r], a.rk, kParBiased);
+        uint32_t q[DC];                                   // q + 0x8000 per lane
         if (first_iter) {
 #pragma unroll
-            for (int j = 0; j < DC; ++j) q[j] = L[r][j];
+            for (int j = 0; j < DC; ++j) q[j] = fadd32(L[r][j], kPairBias, a.rk);
         } else {
-            rebuild_q<DC>(L[r], st[r], q, a.rk);
+            rebuild_q_b8<DC>(L[r], st[r], q, a.rk);
         }
-        uint32_t rn[DC];
-        new_state<DC>(q, a.vk, st[r], rn, a.rk);
+        uint32_t rn[DC];                                  // V(L^(k)_mn) + 0x8000
+        new_state<DC, true>(q, a.vk, st[r], rn, a.rk);
         StateIO<FMT>::store(stt + lane, sstride, (size_t)m[r] * 32, st[r]);
 #pragma unroll
-        for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], to_vform(rn[j] & ~keep));
+        for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], red_value(rn[j], keep));
     }
 }
 
@@ -217,7 +233,8 @@ __global__ void __launch_bounds__(256, LDPC_STREAM_NR2 ? 2 : 3) k_stream_iter_i(
     if (ES) {
         const uint32_t d = a.done[tile * 32 + lane];
         keep = ((d & 1) ? 0x0000FFFFu : 0u) | ((d & 2) ? 0xFFFF0000u : 0u);
-        if (__all_sync(0xFFFFFFFFu, d == 3)) return;
+        // no early exit for fully frozen warps: the accumulators started one iteration
+        // ahead still need their d_v 0x8000 (keep_start / red_value)
     }
     // initialise the accumulator of the next iteration (it held Z^(k-2))
     if (k < a.K) {
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(256, LDPC_STREAM_NR2 ? 2 : 3) k_stream_iter_i(
             for (int n = wg; n < a.N; n += nwg) {
                 const size_t idx = (size_t)n * 32 + lane;
                 uint32_t v = __ldcg(a.Z0 + plane + idx);
-                if (keep) v = to_vform(sel(keep, from_vform(__ldcg(Lnt + idx)), from_vform(v)));
+                if (keep) v = keep_start(v, __ldcg(Lnt + idx), keep, (uint32_t)__ldg(a.coldeg + n));
                 __stcg(Lnt + idx, v);
             }
         }
@@ -274,7 +291,7 @@ __global__ void __launch_bounds__(256) k_stream_syndrome(const StreamArgs a, int
         uint32_t p = 0;
         for (int e = e0; e < e1; ++e) {
             const size_t idx = ((size_t)tile * a.N + __ldg(a.col_idx + e)) * 32 + lane;
-            if (PAIR) p ^= vadd(from_vform(__ldcg(Lp + idx)), 0xFFFFFFFFu);
+            if (PAIR) p ^= fadd32(__ldcg(Lp + idx), kParBiased, a.rk);
             else p ^= (__int_as_float(__ldcg(Lp + idx)) <= 0.0f) ? 1u : 0u;
         }
         synd |= PAIR ? (p & 0x80008000u) : (p & 1u);
@@ -328,8 +345,8 @@ __global__ void __launch_bounds__(256) k_stream_output(const StreamArgs a) {
                 const int f0 = tile * 64 + 2 * lane;
                 const int k0 = f0 < a.nframes ? a.it_ws[f0] : a.K;
                 const int k1 = f0 + 1 < a.nframes ? a.it_ws[f0 + 1] : a.K;
-                val = from_vform(__ldcg(a.Lb[k0 % 3] + idx));
-                val2 = from_vform(__ldcg(a.Lb[k1 % 3] + idx));
+                val = vadd(__ldcg(a.Lb[k0 % 3] + idx), 0xC000C000u);    // unbias
+                val2 = vadd(__ldcg(a.Lb[k1 % 3] + idx), 0xC000C000u);
                 val = (val & 0xFFFFu) | (val2 & 0xFFFF0000u);
             } else {
                 const int f = tile * 32 + lane;

@@ -55,13 +55,13 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
                                            uint32_t keep, uint32_t &synd) {
     uint32_t L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = from_vform(sl[j * 32 + lane]);
-    if (ES) synd |= row_parity<DC>(L, a.rk);
+    for (int j = 0; j < DC; ++j) L[j] = sl[j * 32 + lane];
+    if (ES) synd |= row_parity<DC>(L, a.rk, kParBiased);
     RowState st;
-    uint32_t q[DC];
+    uint32_t q[DC];                                       // q + 0x8000 per lane
     if (first_iter) {
 #pragma unroll
-        for (int j = 0; j < DC; ++j) q[j] = L[j];
+        for (int j = 0; j < DC; ++j) q[j] = fadd32(L[j], kPairBias, a.rk);
     } else {
         if (FMT == FMT_C16) {
             st.A = sl[8 * 32 + lane];
@@ -73,13 +73,13 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
             st.B = prmt(X, 0u, 0x4341u);
             st.W = sl[9 * 32 + lane];
         }
-        rebuild_q<DC>(L, st, q, a.rk);
+        rebuild_q_b8<DC>(L, st, q, a.rk);
     }
-    uint32_t rn[DC];
-    new_state<DC>(q, a.vk, st, rn, a.rk);
+    uint32_t rn[DC];                                      // V(L^(k)_mn) + 0x8000
+    new_state<DC, true>(q, a.vk, st, rn, a.rk);
     StateIO<FMT>::store(stt + lane, sstride, (size_t)m * 32, st);
 #pragma unroll
-    for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, to_vform(rn[j] & ~keep));
+    for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, red_value(rn[j], keep));
 }
 
 template <int DC, bool ES>
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 3) k_stream_pipe(const Stream
                 const size_t idx = (size_t)n * 32 + lane;
                 if (PAIR) {
                     uint32_t v = __ldcg(a.Z0 + plane + idx);
-                    if (keep) v = to_vform(sel(keep, from_vform(__ldcg(Lnt + idx)), from_vform(v)));
+                    if (keep) v = keep_start(v, __ldcg(Lnt + idx), keep, (uint32_t)__ldg(a.coldeg + n));
                     __stcg(Lnt + idx, v);
                 } else if (!frozen) {
                     __stcg(Lnt + idx, __ldcg(a.Z0 + plane + idx));

@@ -14,7 +14,7 @@
 // and [tile][n][32] words), so every access of a warp is one 128-byte line.
 // Integer path: two frames per 32-bit word in packed 16x2 form (doubled values,
 // exactly as the single-scan kernels); fp32: one frame per lane.  Posteriors go to
-// the same rotating V-form buffers Lb[k % 3] the streaming single-scan uses, so the
+// the same rotating biased buffers Lb[k % 3] the streaming single-scan uses, so the
 // syndrome / freeze / output kernels are shared.
 //
 // Reading (DESIGN.md §3 D24): the extrinsic Z_mn is computed as Z_n - L_mn.  In the
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256) k_ts_init(const StreamArgs a, const TwoSc
     for (int64_t e = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); e < t.E; e += nw) {
         const int n = __ldg(t.ecol + e);
         uint32_t v = __ldcg(a.Z0 + ((size_t)tile * a.N + n) * 32 + lane);
-        if (PAIR) v = from_vform(v);
+        if (PAIR) v = vadd(v, 0xC000C000u);              // unbias (ingest with zpre = 0)
         __stcg(t.zv + ((size_t)tile * t.E + e) * 32 + lane, v);
     }
 }
@@ -116,16 +116,16 @@ __global__ void __launch_bounds__(256) k_ts_var(const StreamArgs a, const TwoSca
         const size_t ni = (size_t)n * 32 + lane;
         uint32_t Z = __ldcg(a.Z0 + (size_t)tile * a.N * 32 + ni);
         if (PAIR) {
-            Z = from_vform(Z);
+            Z = vadd(Z, 0xC000C000u);                     // unbias
 #pragma unroll
             for (int b = 0; b < kTsMaxDV; ++b)
                 if (b < dv) Z = vadd(Z, mv[b]);
 #pragma unroll
             for (int b = 0; b < kTsMaxDV; ++b)
                 if (b < dv) __stcg(zvt + (size_t)eid[b] * 32 + lane, vadd(Z, vneg(mv[b], a.rk)));   // Eq.(2)
-            uint32_t out = Z;
-            if (ES && keep) out = sel(keep, from_vform(__ldcg(post + ni)), Z);
-            __stcg(post + ni, to_vform(out));
+            uint32_t out = vadd(Z, kPairBias);            // biased posterior words (k_stream.cuh)
+            if (ES && keep) out = sel(keep, __ldcg(post + ni), out);
+            __stcg(post + ni, out);
         } else {
             float Zf = __uint_as_float(Z);
 #pragma unroll

@@ -655,6 +655,11 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         const char *force = getenv("LDPC_FORCE_STREAM");
         pl.path = (c->res_ok && !(force && force[0] == '1') && pl.sched == LDPC_SCHED_SINGLESCAN) ? PATH_RESIDENT
                                                                                                    : PATH_STREAM_I;
+        // the streaming integer kernels (and two-scan) keep posteriors as 2Z + 0x4000 per
+        // 16-bit lane (reading D26): needs 2Q(max_dv+1) < 0x4000
+        if (pl.path == PATH_STREAM_I && (int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
+            return fail(LDPC_ERR_UNSUPPORTED, "streaming integer decode needs 2*Q*(max_dv+1) < 16384 (Q=%d, max_dv=%d)",
+                        pl.Q, c->max_dv);
         if (pl.sched == LDPC_SCHED_LAYERED) {
             if (!c->res_ok)
                 return fail(LDPC_ERR_UNSUPPORTED, "layered schedule needs a code whose posteriors fit in shared memory "
@@ -672,6 +677,9 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (pl.path == PATH_RESIDENT && !pl.vks.empty() && p->max_iter > kMaxSched) {
         if (pl.lay) return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
         pl.path = PATH_STREAM_I;                         // the streaming kernels take any schedule length
+        if ((int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
+            return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules longer than %d iterations need the streaming "
+                                              "kernels, which need 2*Q*(max_dv+1) < 16384", kMaxSched);
     }
     if (pl.path == PATH_RESIDENT) {
         // flooding uses the barrier-free atomic kernel when the biased 16-bit lanes cannot
@@ -801,6 +809,7 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     a.row_ptr = c->d_row_ptr;
     a.col_idx = c->d_col_idx;
     a.rowtab = (const uint4 *)c->d_rowtab;
+    a.coldeg = c->d_coldeg;
     a.llr = llr;
     a.Z0 = (uint32_t *)(w + pl.off_z0);
     for (int i = 0; i < 3; ++i) a.Lb[i] = (uint32_t *)(w + pl.off_lb[i]);

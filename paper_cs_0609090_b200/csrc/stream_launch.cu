@@ -72,8 +72,8 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
     const int rows_per_block = nwarps_per_block * 8;
     dim3 gr((unsigned)std::max(1, (a.M + rows_per_block - 1) / rows_per_block), (unsigned)r.ntiles);
     if (pair) {
-        if (r.i8) e = launch([&] { k_stream_ingest_i<int8_t><<<gi, 256, 0, s>>>(a); }, nl);
-        else e = launch([&] { k_stream_ingest_i<int16_t><<<gi, 256, 0, s>>>(a); }, nl);
+        if (r.i8) e = launch([&] { k_stream_ingest_i<int8_t><<<gi, 256, 0, s>>>(a, 1); }, nl);
+        else e = launch([&] { k_stream_ingest_i<int16_t><<<gi, 256, 0, s>>>(a, 1); }, nl);
     } else {
         e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); }, nl);
     }
@@ -175,8 +175,8 @@ cudaError_t twoscan_run(const StreamArgs &a0, const TwoScanArgs &t, const Stream
     const bool pair = r.pair, es = r.es;
     dim3 gi((unsigned)std::min<int64_t>(((int64_t)a.N + 7) / 8, 1024), (unsigned)r.ntiles);
     if (pair) {
-        if (r.i8) e = launch([&] { k_stream_ingest_i<int8_t><<<gi, 256, 0, s>>>(a); }, nl);
-        else e = launch([&] { k_stream_ingest_i<int16_t><<<gi, 256, 0, s>>>(a); }, nl);
+        if (r.i8) e = launch([&] { k_stream_ingest_i<int8_t><<<gi, 256, 0, s>>>(a, 0); }, nl);
+        else e = launch([&] { k_stream_ingest_i<int16_t><<<gi, 256, 0, s>>>(a, 0); }, nl);
     } else {
         e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); }, nl);
     }

@@ -127,18 +127,21 @@ __device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, u
 }
 
 // doubled magnitude of the variant from m~ = 2|q| - [q < 0] (B8: m = m~ + 0x8000 per lane)
+// Normalized path out of line: a call cannot be if-converted, so the offset path (every
+// BASELINE integer config) does not execute the normalized instructions speculatively.
+static __device__ __noinline__ uint32_t variant_mag_norm(uint32_t m, uint32_t na, uint32_t ns, uint32_t nmask, uint32_t nb2,
+                                                  uint32_t q2) {
+    const uint32_t t = __vadd2(m, 0x00010001u) & 0xFFFEFFFEu;   // 2|q| per lane
+    const uint32_t x = ((t * na) >> ns) & nmask;                  // 2 floor(na |q| / 2^ns) (no lane overflow: planner)
+    return vaddmin_relu(x, nb2, q2);
+}
+
 template <bool B8 = false>
 __device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const RegK &k) {
     if (B8) m ^= 0x80008000u;                                     // unbias (the DPX add must not wrap)
-    if (!v.norm) {
-        // relu(min(m~ + 1 - 2 beta, 2Q + 1)) with the low bit cleared is exact (m~ in {2|q|-1, 2|q|})
-        return vaddmin_relu(m, v.nbeta2p1, v.q2p1) & 0xFFFEFFFEu;
-    }
-    const uint32_t t = __vadd2(m, 0x00010001u) & 0xFFFEFFFEu;   // 2|q| per lane
-    uint32_t x;                                                   // 2|q| na per lane (no lane overflow: planner)
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(t), "r"(v.na), "r"(k.zero));
-    x = (x >> v.ns) & v.nmask;                                    // 2 floor(na |q| / 2^ns)
-    return vaddmin_relu(x, v.nb2, v.q2);
+    if (__builtin_expect(v.norm != 0, 0)) return variant_mag_norm(m, v.na, v.ns, v.nmask, v.nb2, v.q2);
+    // relu(min(m~ + 1 - 2 beta, 2Q + 1)) with the low bit cleared is exact (m~ in {2|q|-1, 2|q|})
+    return vaddmin_relu(m, v.nbeta2p1, v.q2p1) & 0xFFFEFFFEu;
 }
 
 // New compact state from the q's and the new messages L^(k)_mn (doubled) to be

@@ -13,9 +13,18 @@
 
 namespace ldpc {
 
-constexpr int kPipeRB = 64;        // rows per CTA
+#ifndef LDPC_PIPE_D
+#define LDPC_PIPE_D 4
+#endif
+#ifndef LDPC_PIPE_MINB
+#define LDPC_PIPE_MINB 4
+#endif
+#ifndef LDPC_PIPE_RB
+#define LDPC_PIPE_RB 64
+#endif
+constexpr int kPipeRB = LDPC_PIPE_RB;   // rows per CTA
 constexpr int kPipeWarps = 8;      // warps per CTA
-constexpr int kPipeD = 4;          // rows in flight per warp
+constexpr int kPipeD = LDPC_PIPE_D;     // rows in flight per warp
 constexpr int kPipeLines = 11;     // 8 posterior lines + up to 3 state lines per row
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
@@ -117,7 +126,7 @@ __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *
 
 // PAIR = true: int16 pairs (V-form accumulators); false: fp32.
 template <bool PAIR, int FMT, bool ES>
-__global__ void __launch_bounds__(kPipeWarps * 32, 3) k_stream_pipe(const StreamArgs a, int k) {
+__global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe(const StreamArgs a, int k) {
     extern __shared__ __align__(128) uint32_t psm[];
     uint32_t *coltab = psm;                                       // [RB][8]
     uint8_t *dctab = (uint8_t *)(psm + kPipeRB * 8);              // [RB]

@@ -83,6 +83,14 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
     const char *pipe_env = getenv("LDPC_PIPE");
     const bool use_pipe = r.max_dc <= 8 && !(pipe_env && pipe_env[0] == '0');
     const size_t psmem = pipe_smem_bytes();
+    if (use_pipe && psmem > 48 * 1024) {
+        cudaFuncSetAttribute(k_stream_pipe<true, FMT_C16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        cudaFuncSetAttribute(k_stream_pipe<true, FMT_C16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        cudaFuncSetAttribute(k_stream_pipe<true, FMT_1BIT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        cudaFuncSetAttribute(k_stream_pipe<true, FMT_1BIT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        cudaFuncSetAttribute(k_stream_pipe<false, FMT_C16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+        cudaFuncSetAttribute(k_stream_pipe<false, FMT_C16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    }
     // Frame tiles are decoded in CHUNKS whose per-iteration working set (Z^(0), the three
     // posterior planes and the compact state of the chunk's tiles) fits in L2: all
     // iterations of a chunk run before the next chunk starts, so after the first

@@ -263,11 +263,14 @@ def main():
                 "hbm_model": {"bytes_per_eu": bytes_per_eu(cfg, code),
                               "achieved_gbs": bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 1e9,
                               "peak_gbs": peaks["hbm_gbs"],
-                              "frac": bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]}}
+                              "frac": bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                              "frac_of_nominal_8tbs": bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 8e12}}
     else:
         ach = bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": None}
+                "frac": ach / peaks["hbm_gbs"], "traffic": None, "frac_of_nominal_8tbs": ach / 8000.0,
+                "note": "algorithmic bytes of the whole step (all launches) / step time: a lower bound of the "
+                        "iteration kernel's own rate (it is ~95% of the step, profiles/r01_ncu_full_cfg*.json)"}
     roof["peak_source"] = peak_src
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg.idx}.json")   # from tools/ncu_summary.py
     if os.path.exists(prof):

@@ -131,6 +131,17 @@ def cpu_oracle_throughput(cfg, code, engine, budget_s, nthreads=0, start_frames=
         F = int(min(4096, F * max(2.0, budget_s * 0.6 / max(dt, 1e-3))))
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args, cfg, code, rank, world):
     """--impl reference: the CPU oracle (compact single-scan, the paper's method) timed on host cores."""
     if rank != 0:
@@ -159,7 +170,7 @@ def run_reference(args, cfg, code, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32" if mode == "int" else "f32",
             "data": "synthetic", "edge_updates_per_s": sum(eus) / tot,
             "config": {"workload": describe(cfg, code), "frames_per_step": F, "engine": "oracle compact single-scan"},
-            "cpu_baseline": {"kind": "oracle", "value": value, "unit": UNIT, "cores": nt,
+            "cpu_baseline": {"kind": "oracle", "value": value, "unit": UNIT, "cores": nt, "cpu_model": cpu_model(),
                              "sample": f"{F} frames of the workload per step, all host threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -346,9 +357,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         gb, eus, Fs, nt, dt = cpu_oracle_throughput(cfg, code, "compact", args.cpu_budget)
         gb2, eus2, Fs2, nt2, dt2 = cpu_oracle_throughput(cfg, code, "twoscan", args.cpu_budget / 2)
+        g1, e1, F1, _, d1 = cpu_oracle_throughput(cfg, code, "compact", min(3.0, args.cpu_budget / 4), nthreads=1,
+                                                   start_frames=1)
         cpu = {"value": gb, "unit": UNIT, "cores": nt, "kind": "oracle",
                "sample": f"{Fs} frames of the workload (compact single-scan oracle, {dt:.1f} s, all host threads)",
-               "edge_updates_per_s": eus,
+               "cpu_model": cpu_model(), "edge_updates_per_s": eus,
+               "single_thread": {"value": g1, "edge_updates_per_s": e1, "frames": F1, "seconds": d1},
                "twoscan": {"value": gb2, "edge_updates_per_s": eus2, "frames": Fs2},
                "singlescan_over_twoscan": gb / gb2 if gb2 else None,
                "paper_claim": "single-scan min-sum more than twice as fast as two-scan (PAPER.md P:29-30)"}

@@ -202,25 +202,10 @@ __device__ __forceinline__ void stream_dispatch_i(int dc, const StreamArgs &a, i
     }
 }
 
+// Register version of the integer iteration kernel (rows of degree > 8 are rejected for
+// integer LLRs, so this serves LDPC_PIPE=0 runs -- the pipelined kernel's cross-check).
 template <int FMT, bool ES>
-__device__ __forceinline__ void stream_dispatch2_i(int dc, const StreamArgs &a, int lane, const int (&m)[2],
-                                                   const RowT *rt, const uint32_t *Lpt, uint32_t *Lat,
-                                                   uint32_t *stt, bool first_iter, uint32_t keep, uint32_t &synd) {
-    switch (dc) {
-    case 2: stream_rows_i<2, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
-    case 3: stream_rows_i<3, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
-    case 4: stream_rows_i<4, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
-    case 5: stream_rows_i<5, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
-    case 6: stream_rows_i<6, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
-    case 7: stream_rows_i<7, 2, FMT, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, keep, synd); break;
-    }
-}
-
-template <int FMT, bool ES>
-#ifndef LDPC_STREAM_NR2
-#define LDPC_STREAM_NR2 0
-#endif
-__global__ void __launch_bounds__(256, LDPC_STREAM_NR2 ? 2 : 3) k_stream_iter_i(const StreamArgs a, int k) {
+__global__ void __launch_bounds__(256, 3) k_stream_iter_i(const StreamArgs a, int k) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nwg = gridDim.x * (blockDim.x >> 5);
@@ -251,30 +236,11 @@ __global__ void __launch_bounds__(256, LDPC_STREAM_NR2 ? 2 : 3) k_stream_iter_i(
     }
     uint32_t synd = 0;
     const bool first_iter = (k == 1);
-    // row tables of the next row pair are prefetched while the current pair is processed
-#if LDPC_STREAM_NR2
-    for (int m0 = wg; m0 < a.M; m0 += 2 * nwg) {
-        const int m1 = m0 + nwg;
-        const RowT rt[2] = {load_rowt(a.rowtab, m0, a.M), load_rowt(a.rowtab, m1, a.M)};
-        if (rt[0].dc == rt[1].dc && rt[0].dc <= 7) {
-            const int mm[2] = {m0, m1};
-            stream_dispatch2_i<FMT, ES>(rt[0].dc, a, lane, mm, rt, Lpt, Lat, stt, first_iter, keep, synd);
-        } else {
-            const int mm0[1] = {m0};
-            stream_dispatch_i<1, FMT, ES>(rt[0].dc, a, lane, mm0, rt, Lpt, Lat, stt, first_iter, keep, synd);
-            if (rt[1].dc) {
-                const int mm1[1] = {m1};
-                stream_dispatch_i<1, FMT, ES>(rt[1].dc, a, lane, mm1, rt + 1, Lpt, Lat, stt, first_iter, keep, synd);
-            }
-        }
-    }
-#else
     for (int m = wg; m < a.M; m += nwg) {
         const RowT rt = load_rowt(a.rowtab, m, a.M);
         const int mm[1] = {m};
         stream_dispatch_i<1, FMT, ES>(rt.dc, a, lane, mm, &rt, Lpt, Lat, stt, first_iter, keep, synd);
     }
-#endif
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
 }
 
@@ -492,20 +458,6 @@ __device__ __forceinline__ void stream_dispatch_f(int dc, const StreamArgs &a, i
     case 14: stream_rows_f<14, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
     case 15: stream_rows_f<15, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
     case 16: stream_rows_f<16, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    }
-}
-
-template <bool ES>
-__device__ __forceinline__ void stream_dispatch2_f(int dc, const StreamArgs &a, int lane, const int (&m)[2],
-                                                   const RowT *rt, const float *Lpt, float *Lat, uint32_t *stt,
-                                                   bool first_iter, bool frozen, uint32_t &synd) {
-    switch (dc) {
-    case 2: stream_rows_f<2, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 3: stream_rows_f<3, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 4: stream_rows_f<4, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 5: stream_rows_f<5, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 6: stream_rows_f<6, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 7: stream_rows_f<7, 2, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
     }
 }
 

@@ -363,3 +363,43 @@ def test_batched_resident_kernel(cfg_idx, monkeypatch):
         z = g.llr(11, 0, 33, c.n_vars, g.ebn0_to_sigma2(1.5, max(c.rate, 0.3)), g.LLR_I16, 3, 511)
         params = P.make_params(10, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
         assert_int_parity(c, z, params, 10, 1, 1, 511)
+
+
+def test_resident_size_boundary():
+    """Largest codes on either side of the resident kernel's shared-memory limit
+    (2 N words + reserve <= 227 KB per CTA): N = 26924 resident, N = 27178 streaming."""
+    for nb in (212, 214):
+        w = np.array(([1, 2, 2] * nb)[:nb], np.int32)
+        code = g.qc(64, nb, 127, w, seed=nb)
+        assert int(np.max(np.diff(code.row_ptr))) <= 8
+        llr = g.llr(77 + nb, 0, 5, code.n_vars, g.ebn0_to_sigma2(2.0, code.rate), g.LLR_I16, 3, 511)
+        for es in (0, 1):
+            params = P.make_params(6, es, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+            assert_int_parity(code, llr, params, 6, es, 1, 511)
+
+
+def test_high_column_degree_batched_kernel():
+    """Column degree 20 at Q = 511: 2Q(dv+1) >= 0x4000, so the (unbiased) batched resident
+    kernel runs; the streaming integer path rejects it (biased lanes would overflow)."""
+    code = g.regular(80, 20, 8, seed=3, remove_4cycles=False)
+    llr = g.llr(5, 0, 33, code.n_vars, 0.9, g.LLR_I16, 3, 511)
+    params = P.make_params(8, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+    assert_int_parity(code, llr, params, 8, 1, 1, 511)
+    dec = decoder(code)
+    import os
+    os.environ["LDPC_FORCE_STREAM"] = "1"
+    try:
+        with pytest.raises(P.LdpcError) as e:
+            dec.workspace(33, params)
+        assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+    finally:
+        del os.environ["LDPC_FORCE_STREAM"]
+
+
+def test_many_iterations():
+    """200 iterations (no early stop) on the cfg1 code, resident and streaming."""
+    cfg = g.CONFIGS[1]
+    code = cfg.code()
+    llr = cfg.llrs(code, 0, 40)
+    params = P.make_params(200, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+    assert_int_parity(code, llr, params, 200, 0, 1, 511)

@@ -126,7 +126,10 @@ typedef struct {
                               D6); 0 = default (511 for I16, 127 for I8).  Channel LLRs are
                               saturated to [-Q, Q] on load.  Requires 2*Q*(max_dv + 2) <= 32767
                               (posteriors are exact in 16-bit lanes), Q <= 511 (COMPACT) or
-                              Q <= 127 (ONEBIT), else LDPC_ERR_UNSUPPORTED.  Ignored for F32. */
+                              Q <= 127 (ONEBIT), else LDPC_ERR_UNSUPPORTED.  Codes too long for
+                              the resident kernel (streaming kernels, and TWOSCAN) additionally
+                              need 2*Q*(max_dv + 1) < 16384 (biased 16-bit lanes, D26).
+                              Ignored for F32. */
     int32_t llr_type;      /* LDPC_LLR_I16 | LDPC_LLR_I8 | LDPC_LLR_F32 */
     int32_t msg_format;    /* LDPC_MSG_COMPACT | LDPC_MSG_1BIT (1BIT requires integer LLRs) */
     int32_t schedule;      /* LDPC_SCHED_SINGLESCAN (0, default) | _TWOSCAN | _LAYERED */

@@ -912,11 +912,17 @@ struct HostLayout {
 };
 
 // Host-buffer decode: H2D copy, decode and D2H copies of frame chunks round-robin on up to
-// four streams, so the copies of one chunk overlap the decode of others.  Chunks of about
-// F/16 frames (>= 512) on 4 streams measured best on cfg2 (e2e 7.4 -> 8.6 Gbit/s vs 4 x 2);
-// LDPC_HOST_CHUNKS / LDPC_HOST_STREAMS override (tuning hooks).
+// four streams, so the copies of one chunk overlap the decode of others.  Up to 16 chunks of
+// >= 256 frames (resident) / >= 64 frames (streaming) on 4 streams measured best (e2e cfg2
+// 7.4 -> 8.6, cfg4 2.1 -> 2.8, cfg1 3.7 -> 4.0 Gbit/s); LDPC_HOST_CHUNKS / LDPC_HOST_STREAMS
+// override (tuning hooks).
 ldpc_status host_layout(const ldpc_code *c, int64_t F, const ldpc_decode_params *p, HostLayout &h) {
-    h.nchunks = std::max<int64_t>(1, std::min<int64_t>(16, F / 512));
+    Plan pf;
+    ldpc_status st0 = make_plan(c, F, p, pf);
+    if (st0 != LDPC_OK) return st0;
+    // chunks of >= 256 frames (resident kernels) or >= one 64-frame tile (streaming), <= 16
+    const int64_t min_chunk = pf.path == PATH_RESIDENT ? 256 : 64;
+    h.nchunks = std::max<int64_t>(1, std::min<int64_t>(16, F / min_chunk));
     if (const char *e = getenv("LDPC_HOST_CHUNKS")) h.nchunks = std::max(1, atoi(e));
     h.chunk = (F + h.nchunks - 1) / h.nchunks;
     h.chunk = ((h.chunk + 63) / 64) * 64;

@@ -350,8 +350,8 @@ def main():
     # ---- the other schedules on the same frames, timed the same way (events on this
     # stream, L2 flushed): the paper's comparison against two-scan (SURVEY
     # §8(f1)) and the layered schedule (§8(f2), resident-kernel codes only)
-    def time_schedule(sched):
-        sp = P.params_for_config(cfg, sched)
+    def time_schedule(sched, msg_format=None):
+        sp = P.params_for_config(cfg, sched, msg_format)
         try:
             dec.workspace(F, sp)
         except P.LdpcError as ex:
@@ -378,12 +378,14 @@ def main():
                 "mean_iterations": its, "frames_converged": int(so.syndrome_ok.sum().item()),
                 "singlescan_over_this": value / v if v else None}
 
-    twoscan = layered = None
+    twoscan = layered = fullmsg = None
     if not args.no_twoscan:
         twoscan = time_schedule(P.LDPC_SCHED_TWOSCAN)
         twoscan["paper_claim"] = "single-scan more than twice as fast as two-scan min-sum (PAPER.md P:29-30)"
     if not args.no_layered:
         layered = time_schedule(P.LDPC_SCHED_LAYERED)
+        # the §4 single-scan with stored per-edge messages (LDPC_MSG_FULL, resident codes)
+        fullmsg = time_schedule(P.LDPC_SCHED_SINGLESCAN, P.LDPC_MSG_FULL)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -412,6 +414,7 @@ def main():
                 "errors": {"bit_errors": c[0], "frame_errors": c[1], "undetected": c[2], "not_converged": c[3],
                            "mean_iterations": sum_iters / (F * world)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_twoscan": twoscan, "gpu_layered": layered,
+                "gpu_full_messages": fullmsg,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -90,7 +90,13 @@ enum { LDPC_MINSUM_OFFSET = 0,       /* |L| <= max(|L| - beta, 0); offset 0 = pl
  *   COMPACT: magnitudes stored with 9+ bits (clamp Q <= 511 for integer LLRs);
  *   ONEBIT : "1-bit messages": the only per-edge persistent datum is the
  *            sign bit; magnitudes are stored as bytes (integer LLRs, Q <= 127). */
-enum { LDPC_MSG_COMPACT = 0, LDPC_MSG_1BIT = 1 };
+enum { LDPC_MSG_COMPACT = 0, LDPC_MSG_1BIT = 1,
+       LDPC_MSG_FULL = 2 };   /* FULL: the §4 single-scan storing every L_mn (one
+                                 16-bit value per edge per frame, on chip).  Integer LLRs,
+                                 SINGLESCAN schedule, codes on the resident path with
+                                 2Q(max_dv+1) < 16384 and the messages within the Tensor Memory
+                                 budget (else LDPC_ERR_UNSUPPORTED).  Same outputs as COMPACT
+                                 (P:338). */
 /* Decoding schedule.
  *   SINGLESCAN: the paper's method -- flooding single-scan min-sum over the compact
  *               state (Eq.(3)); the default.

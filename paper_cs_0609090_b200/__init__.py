@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libldpc.so")
 LDPC_OK, LDPC_ERR_INVALID_ARG, LDPC_ERR_INVALID_CODE, LDPC_ERR_UNSUPPORTED, LDPC_ERR_CUDA, LDPC_ERR_NO_MEMORY = range(6)
 LDPC_LLR_I16, LDPC_LLR_I8, LDPC_LLR_F32 = 0, 1, 2
 LDPC_MINSUM_OFFSET, LDPC_MINSUM_NORMALIZED = 0, 1
-LDPC_MSG_COMPACT, LDPC_MSG_1BIT = 0, 1
+LDPC_MSG_COMPACT, LDPC_MSG_1BIT, LDPC_MSG_FULL = 0, 1, 2
 LDPC_SCHED_SINGLESCAN, LDPC_SCHED_TWOSCAN, LDPC_SCHED_LAYERED = 0, 1, 2
 
 # every symbol include/ldpc.h declares
@@ -310,7 +310,7 @@ class Decoder:
         return counters
 
 
-def params_for_config(cfg, schedule=LDPC_SCHED_SINGLESCAN) -> ldpc_decode_params:
+def params_for_config(cfg, schedule=LDPC_SCHED_SINGLESCAN, msg_format=None) -> ldpc_decode_params:
     """Decode parameters of one of ldpcgen.CONFIGS (BASELINE.json configs).
     schedule=LDPC_SCHED_TWOSCAN gives the paper's two-scan baseline on the same workload
     (full per-edge messages, so the message format is COMPACT)."""
@@ -320,5 +320,7 @@ def params_for_config(cfg, schedule=LDPC_SCHED_SINGLESCAN) -> ldpc_decode_params
         return make_params(cfg.max_iter, cfg.early_stop, LDPC_MINSUM_NORMALIZED, 0, 0.0, cfg.alpha, 0, llr_type,
                            LDPC_MSG_COMPACT, schedule)
     fmt = LDPC_MSG_1BIT if cfg.msg_format == "1bit" and schedule == LDPC_SCHED_SINGLESCAN else LDPC_MSG_COMPACT
+    if msg_format is not None:
+        fmt = int(msg_format)
     return make_params(cfg.max_iter, cfg.early_stop, LDPC_MINSUM_OFFSET, cfg.offset_raw, 0.0, 1.0, cfg.clamp,
                        llr_type, fmt, schedule)

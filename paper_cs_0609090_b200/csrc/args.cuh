@@ -22,6 +22,7 @@ struct QcTab {
     int32_t e0[kQcMaxSB][kQcGroups];    // first entry of the base row handled by group g
     int32_t dc[kQcMaxSB][kQcGroups];    // its degree (0 = group idle in this super-batch)
     int32_t run_end[kQcMaxSB][kQcGroups];  // first later super-batch where the group's degree changes
+    int16_t tcol[kQcMaxSB][kQcGroups];     // FMT_FULL: first TMEM column of slot b's messages in group g
     uint2 ent[kQcMaxEnt];               // (4 * shift, 4 * (j * Z)) per base-matrix entry
 };
 
@@ -87,6 +88,8 @@ struct TwoScanArgs {
 // persistent state formats (workspace words per row-pair)
 // FMT_C16 : 3 words (A, B, W); magnitudes up to 2Q = 1022.
 // FMT_1BIT: 2 words (X = bytes [A_lo, B_lo, A_hi, B_hi], W); magnitudes up to 2Q = 254.
-enum { FMT_C16 = 0, FMT_1BIT = 1 };
+// FMT_FULL: the §4 single-scan -- one word per EDGE, the previous message L_mn
+//           itself (barrier-free resident kernel only; k_resident_atom.cuh).
+enum { FMT_C16 = 0, FMT_1BIT = 1, FMT_FULL = 2 };
 
 }  // namespace ldpc

@@ -58,12 +58,88 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");
 }
 
+// ---------------------------------------------------------------- FMT_FULL (§4)
+// The single-scan of PAPER.md §4 keeps every check message L_mn: here one
+// TMEM word per edge per frame pair, stored as c = 0x40004000 - V(L) (= 0x4000C000 minus the
+// RED value V(L) + 0x8000), so the next iteration's q_mn + 0x8000 per lane = (2Z_n + 0x4000)
+// + c is one IMAD (no rebuild from a compact state).  Same messages, posteriors and stopping as the compact form.
+template <int DC>
+__device__ __forceinline__ void full_tmem_load(uint32_t taddr, uint32_t (&c)[8]) {
+    if constexpr (DC == 8) {
+        tmem_ld4(taddr, c[0], c[1], c[2], c[3]);
+        tmem_ld4(taddr + 4, c[4], c[5], c[6], c[7]);
+    } else {
+        constexpr int o4 = DC >= 4 ? 4 : 0;
+        if constexpr (DC >= 4) tmem_ld4(taddr, c[0], c[1], c[2], c[3]);
+        constexpr int o2 = o4 + ((DC - o4) >= 2 ? 2 : 0);
+        if constexpr ((DC - o4) >= 2) tmem_ld2(taddr + o4, c[o4], c[o4 + 1]);
+        if constexpr ((DC - o2) == 1) tmem_ld1(taddr + o2, c[o2]);
+    }
+    tmem_wait_ld_dep8(c);
+}
+template <int DC>
+__device__ __forceinline__ void full_tmem_store(uint32_t taddr, const uint32_t (&c)[8]) {
+    if constexpr (DC == 8) {
+        tmem_st4(taddr, c[0], c[1], c[2], c[3]);
+        tmem_st4(taddr + 4, c[4], c[5], c[6], c[7]);
+    } else {
+        constexpr int o4 = DC >= 4 ? 4 : 0;
+        if constexpr (DC >= 4) tmem_st4(taddr, c[0], c[1], c[2], c[3]);
+        constexpr int o2 = o4 + ((DC - o4) >= 2 ? 2 : 0);
+        if constexpr ((DC - o4) >= 2) tmem_st2(taddr + o4, c[o4], c[o4 + 1]);
+        if constexpr ((DC - o2) == 1) tmem_st1(taddr + o2, c[o2]);
+    }
+}
+
+template <int DC, bool QC, bool ES>
+__device__ __forceinline__ void atom_row_full(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp,
+                                              uint32_t ba, int e0, uint32_t r4, int p, bool first_iter,
+                                              uint32_t (&c)[8], uint32_t &synd) {
+    uint32_t d[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        if (QC) {
+            const uint2 e = t.ent[e0 + j];
+            const uint32_t u = r4 + e.x;
+            d[j] = min(u - t.Z4, u) + e.y;
+        } else {
+            d[j] = __ldg(a.colT + (size_t)j * a.M + p);
+        }
+    }
+    uint32_t L[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
+    if (ES) synd |= row_parity<DC>(L, a.rk, a.cpar);
+    uint32_t q[DC];                                                      // q_mn + 0x8000 per lane
+#pragma unroll
+    for (int j = 0; j < DC; ++j) q[j] = fadd32(L[j], first_iter ? 0x40004000u : c[j], a.rk);   // Z - L_old
+    uint32_t rn[DC];
+    RowState st;                                                         // unused: no compact state
+    new_state<DC, true>(q, vk, st, rn, a.rk);                           // Eq.(3)
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");   // Z += L
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c[j]) : "r"(rn[j]), "r"(a.rk.m1), "r"(0x4000C000u));
+    }
+}
+
 template <int DC, bool ES, int FMT>
 __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t tw,
                                            int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba, bool first_iter,
                                            uint32_t &synd) {
     if constexpr (DC == 0) {
         return bend;
+    } else if constexpr (FMT == FMT_FULL) {
+        // slot b's DC message words start at column t.tcol[b][g] of this group's range
+#pragma unroll 1
+        for (; b < bend; ++b) {
+            uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            const uint32_t col = tw + (uint32_t)t.tcol[b][g];
+            if (!first_iter) full_tmem_load<DC>(col, c);
+            if (rloc < a.Z) atom_row_full<DC, true, ES>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, c, synd);
+            full_tmem_store<DC>(col, c);
+        }
+        return b;
     } else {
 #pragma unroll 1
         for (; b < bend; ++b) {
@@ -103,6 +179,21 @@ __device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, cons
     case 6: atom_row<6, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
     case 7: atom_row<7, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
     case 8: atom_row<8, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    }
+}
+
+template <bool ES>
+__device__ __forceinline__ void atom_csr_dispatch_full(int dc, const ResArgs &a, const QcTab &t, const VarK &vk,
+                                                       uint32_t bp, uint32_t ba, int p, bool first_iter,
+                                                       uint32_t (&c)[8], uint32_t &synd) {
+    switch (dc) {
+    case 2: atom_row_full<2, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 3: atom_row_full<3, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 4: atom_row_full<4, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 5: atom_row_full<5, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 6: atom_row_full<6, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 7: atom_row_full<7, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 8: atom_row_full<8, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
     }
 }
 
@@ -185,11 +276,19 @@ __global__ void __launch_bounds__(256, 3) k_resident_atom(const __grid_constant_
             } else {
 #pragma unroll 1
                 for (int b = 0; b < nb; ++b) {
-                    RowState st = {0u, 0u, 0u};
-                    if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
                     const int p = b * nth + tid;
-                    if (p < a.M) atom_csr_dispatch<ES>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, st, synd);
-                    state_tmem_store<FMT>(tw, b, nb, st);
+                    if constexpr (FMT == FMT_FULL) {
+                        // rows of one slot differ in degree across the warp: 8 columns per slot
+                        uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                        if (!first_iter) full_tmem_load<8>(tw + 8u * b, c);
+                        if (p < a.M) atom_csr_dispatch_full<ES>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, c, synd);
+                        full_tmem_store<8>(tw + 8u * b, c);
+                    } else {
+                        RowState st = {0u, 0u, 0u};
+                        if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
+                        if (p < a.M) atom_csr_dispatch<ES>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, st, synd);
+                        state_tmem_store<FMT>(tw, b, nb, st);
+                    }
                 }
             }
             tmem_wait_st();

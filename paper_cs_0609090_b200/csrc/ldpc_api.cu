@@ -90,6 +90,7 @@ struct ldpc_code {
     // barrier-free flooding kernel (k_resident_atom.cuh): row slots per thread
     int nbatch_atom = 0, res_threads_atom = 0;
     QcTab *qtab_atom = nullptr;
+    int full_cols_qc = 0;            // FMT_FULL: TMEM columns per group (QC: sum of the group's row degrees)
     cudaStream_t aux[4] = {nullptr, nullptr, nullptr, nullptr};      // host-API pipeline streams
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
@@ -390,6 +391,14 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                 for (int g = 0; g < kQcGroups; ++g)
                     for (int b = u.nsb - 1; b >= 0; --b)
                         u.run_end[b][g] = (b + 1 < u.nsb && u.dc[b + 1][g] == u.dc[b][g]) ? u.run_end[b + 1][g] : b + 1;
+                for (int g = 0; g < kQcGroups; ++g) {          // FMT_FULL column offsets per slot
+                    int col = 0;
+                    for (int b = 0; b < u.nsb; ++b) {
+                        u.tcol[b][g] = (int16_t)col;
+                        col += u.dc[b][g];
+                    }
+                    c->full_cols_qc = std::max(c->full_cols_qc, col);
+                }
                 c->nbatch_atom = nsb;
                 c->res_threads_atom = c->res_threads;
             }
@@ -589,7 +598,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         if (c->max_dc > 8) return fail(LDPC_ERR_UNSUPPORTED, "two-scan supports row degree <= 8 (max %d)", c->max_dc);
         if (c->max_dv > 16) return fail(LDPC_ERR_UNSUPPORTED, "two-scan supports column degree <= 16 (max %d)", c->max_dv);
     }
-    if (p->msg_format != LDPC_MSG_COMPACT && p->msg_format != LDPC_MSG_1BIT)
+    if (p->msg_format != LDPC_MSG_COMPACT && p->msg_format != LDPC_MSG_1BIT && p->msg_format != LDPC_MSG_FULL)
         return fail(LDPC_ERR_INVALID_ARG, "bad msg_format %d", p->msg_format);
     if (p->variant != LDPC_MINSUM_OFFSET && p->variant != LDPC_MINSUM_NORMALIZED)
         return fail(LDPC_ERR_INVALID_ARG, "bad variant %d", p->variant);
@@ -600,7 +609,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (p->variant == LDPC_MINSUM_NORMALIZED && !(p->alpha > 0.f && p->alpha <= 1.f))
         return fail(LDPC_ERR_INVALID_ARG, "alpha must be in (0,1]");
     if (p->llr_type == LDPC_LLR_F32) {
-        if (p->msg_format == LDPC_MSG_1BIT) return fail(LDPC_ERR_UNSUPPORTED, "1-bit messages need integer LLRs");
+        if (p->msg_format != LDPC_MSG_COMPACT)
+            return fail(LDPC_ERR_UNSUPPORTED, "1-bit and full per-edge message formats need integer LLRs");
         if (pl.sched == LDPC_SCHED_LAYERED)
             return fail(LDPC_ERR_UNSUPPORTED, "layered schedule is implemented for integer LLRs only");
         if (c->max_dc > 16) return fail(LDPC_ERR_UNSUPPORTED, "F32 path supports row degree <= 16 (max %d)", c->max_dc);
@@ -621,7 +631,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     } else if (p->llr_type == LDPC_LLR_I16 || p->llr_type == LDPC_LLR_I8) {
         if (p->offset_raw < 0 || p->offset_raw > 16383) return fail(LDPC_ERR_INVALID_ARG, "offset_raw out of range");
         if (c->max_dc > kMaxDC) return fail(LDPC_ERR_UNSUPPORTED, "integer paths support row degree <= %d (max %d)", kMaxDC, c->max_dc);
-        pl.fmt = p->msg_format == LDPC_MSG_1BIT ? FMT_1BIT : FMT_C16;
+        pl.fmt = p->msg_format == LDPC_MSG_1BIT ? FMT_1BIT : (p->msg_format == LDPC_MSG_FULL ? FMT_FULL : FMT_C16);
         pl.Q = p->clamp_raw > 0 ? p->clamp_raw : (p->llr_type == LDPC_LLR_I16 ? 511 : 127);
         const int qmax = pl.fmt == FMT_1BIT ? 127 : 511;
         if (pl.Q > qmax) return fail(LDPC_ERR_UNSUPPORTED, "clamp Q=%d exceeds %d for this message format", pl.Q, qmax);
@@ -660,6 +670,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         if (pl.path == PATH_STREAM_I && (int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
             return fail(LDPC_ERR_UNSUPPORTED, "streaming integer decode needs 2*Q*(max_dv+1) < 16384 (Q=%d, max_dv=%d)",
                         pl.Q, c->max_dv);
+        if (pl.fmt == FMT_FULL && pl.path != PATH_RESIDENT)
+            return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages (LDPC_MSG_FULL) need a code on the resident path");
         if (pl.sched == LDPC_SCHED_LAYERED) {
             if (!c->res_ok)
                 return fail(LDPC_ERR_UNSUPPORTED, "layered schedule needs a code whose posteriors fit in shared memory "
@@ -688,12 +700,16 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         const char *be = getenv("LDPC_RES_BATCHED");
         const bool atom_ok = (int64_t)2 * pl.Q * (c->max_dv + 1) < 0x4000 && c->nbatch_atom > 0;
         pl.kind = pl.lay ? RES_LAYERED : ((atom_ok && !(be && be[0] == '1')) ? RES_ATOM : RES_BATCHED);
+        if (pl.fmt == FMT_FULL && pl.kind != RES_ATOM)
+            return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages (LDPC_MSG_FULL) need the barrier-free resident "
+                                              "kernel: SINGLESCAN schedule and 2*Q*(max_dv+1) < 16384");
         pl.threads = pl.lay ? c->res_threads_lay : (pl.kind == RES_ATOM ? c->res_threads_atom : c->res_threads);
         pl.nbatch = pl.lay ? c->nbatch_lay : (pl.kind == RES_ATOM ? c->nbatch_atom : c->nbatch);
         pl.smem = pl.lay ? c->res_smem / 2 : c->res_smem;   // layered: one posterior array
         // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group; layered
         // general codes keep the state in shared memory instead ([3][M] words, by row)
         pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * pl.nbatch;
+        if (pl.fmt == FMT_FULL) pl.cols_per_group = c->qc ? c->full_cols_qc : 8 * pl.nbatch;   // one word per edge
         if (pl.lay && !c->qc) {
             pl.cols_per_group = 0;
             pl.smem += (size_t)3 * c->M * 4;

@@ -57,6 +57,12 @@ cudaError_t dispatch(bool qc, bool es, int fmt, bool i8, int kind, Args... args)
     LDPC_RES_CASE(true, false, FMT_C16) LDPC_RES_CASE(true, false, FMT_1BIT)
     LDPC_RES_CASE(false, true, FMT_C16) LDPC_RES_CASE(false, true, FMT_1BIT)
     LDPC_RES_CASE(false, false, FMT_C16) LDPC_RES_CASE(false, false, FMT_1BIT)
+    // FMT_FULL (§4 per-edge messages) exists for the barrier-free kernel only
+#define LDPC_RES_FULL(Q, E)                                                               \
+    if (qc == Q && es == E && fmt == FMT_FULL && kind == 2)                               \
+        return i8 ? K<Q, E, FMT_FULL, int8_t, 2>::run(args...) : K<Q, E, FMT_FULL, int16_t, 2>::run(args...);
+    LDPC_RES_FULL(true, true) LDPC_RES_FULL(true, false) LDPC_RES_FULL(false, true) LDPC_RES_FULL(false, false)
+#undef LDPC_RES_FULL
 #undef LDPC_RES_CASE
 #undef LDPC_RES_KIND
     return cudaErrorInvalidValue;

@@ -67,8 +67,11 @@ def test_random_case(i, monkeypatch):
         (P.LDPC_LLR_I16, g.LLR_I16, 3)
     sched = [P.LDPC_SCHED_SINGLESCAN, P.LDPC_SCHED_SINGLESCAN, P.LDPC_SCHED_LAYERED,
              P.LDPC_SCHED_TWOSCAN][int(rng.integers(0, 4))]
+    fmt = P.LDPC_MSG_1BIT if onebit else P.LDPC_MSG_COMPACT
     if sched == P.LDPC_SCHED_TWOSCAN:
-        onebit = False
+        fmt = P.LDPC_MSG_COMPACT
+    elif sched == P.LDPC_SCHED_SINGLESCAN and rng.integers(0, 3) == 0:
+        fmt = P.LDPC_MSG_FULL                      # the §4 per-edge form (resident kernel only)
     env = [None, "LDPC_FORCE_STREAM", "LDPC_RES_BATCHED", "LDPC_PIPE"][int(rng.integers(0, 4))]
     if env == "LDPC_PIPE":
         monkeypatch.setenv("LDPC_PIPE", "0")
@@ -82,8 +85,7 @@ def test_random_case(i, monkeypatch):
     ebn0 = float(rng.uniform(0.5, 4.0))
     llr = g.llr(int(rng.integers(1, 1 << 30)), 0, F, code.n_vars, g.ebn0_to_sigma2(ebn0, max(code.rate, 0.2)),
                 kind, frac, Q)
-    params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, lt,
-                           P.LDPC_MSG_1BIT if onebit else P.LDPC_MSG_COMPACT, sched)
+    params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, lt, fmt, sched)
     try:
         post, hb, ok, it = gpu_decode(code, llr, params)
     except P.LdpcError as e:
@@ -93,7 +95,7 @@ def test_random_case(i, monkeypatch):
               P.LDPC_SCHED_TWOSCAN: "twoscan"}[sched]
     ref = oracle.decode(code, llr.astype(np.int32), engine, "int", K, es, beta, Q, nthreads=NT)
     info = f"{code.name} N={code.n_vars} M={code.n_checks} sched={sched} env={env} K={K} es={es} beta={beta} Q={Q} " \
-           f"F={F} 1bit={onebit} lt={lt}"
+           f"F={F} fmt={fmt} lt={lt}"
     np.testing.assert_array_equal(it, ref.iters, err_msg=info)
     np.testing.assert_array_equal(ok, ref.ok, err_msg=info)
     np.testing.assert_array_equal(post.astype(np.int32), ref.post, err_msg=info)

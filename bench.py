@@ -125,10 +125,10 @@ def cpu_oracle_throughput(cfg, code, engine, budget_s, nthreads=0, start_frames=
         r = oracle.decode(code, z, engine, mode, cfg.max_iter, cfg.early_stop, cfg.offset_raw if mode == "int" else 0,
                           cfg.clamp if mode == "int" else 0, cfg.alpha, nthreads=nt)
         dt = time.perf_counter() - t0
-        if dt >= budget_s * 0.5 or F >= 4096:
+        if dt >= budget_s * 0.5 or F >= 32768:
             eu = float(r.iters.sum()) * code.n_edges
             return F * code.K / dt / 1e9, eu / dt, F, r.threads, dt
-        F = int(min(4096, F * max(2.0, budget_s * 0.6 / max(dt, 1e-3))))
+        F = int(min(32768, F * max(2.0, budget_s * 0.8 / max(dt, 1e-3))))
 
 
 def cpu_model():

@@ -728,12 +728,13 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         if (getenv("LDPC_DEBUG")) fprintf(stderr, "[ldpc] occupancy API: %d blocks/SM\n", blocks);
         blocks = std::min(blocks, (int)(512 / cols));     // TMEM capacity per SM
         if (blocks < 1) return fail(LDPC_ERR_UNSUPPORTED, "resident kernel does not fit on an SM");
-        // One frame pair per CTA (grid = pairs): the block scheduler then balances the SMs
-        // dynamically.  Measured against a persistent grid of `blocks x SMs` CTAs looping over
-        // pairs: cfg2 2.91 -> 2.67 ms, cfg3 40.6 -> 35.9 ms.  The price is one Z^(0) slot per
-        // pair in the workspace (the size of the int16 input).  LDPC_RES_GRID_MULT=m caps the
-        // grid at m x resident slots (tuning hook; the kernel loops over pairs).
-        pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)1 << 30);
+        // One frame pair per CTA (grid = pairs, up to 64 waves): the block scheduler then
+        // balances the SMs dynamically.  Measured against a persistent grid of `blocks x SMs`
+        // CTAs looping over pairs: cfg2 2.91 -> 2.67 ms, cfg3 40.6 -> 35.9 ms.  The price is
+        // one Z^(0) slot per CTA in the workspace; the 64-wave cap bounds it (cfg2: <= 0.9 GB)
+        // for huge batches, whose CTAs then loop over pairs.  LDPC_RES_GRID_MULT=m sets the cap
+        // to m waves (tuning hook).
+        pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)blocks * c->sm_count * 64);
         if (const char *ge = getenv("LDPC_RES_GRID_MULT"))
             pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1),
                                              (int64_t)blocks * c->sm_count * std::max(1, atoi(ge)));

@@ -19,8 +19,8 @@
  *                      per-edge L_mn and Eq.(1) evaluated literally.
  *   ENG_LAYERED        the same schedule over the §5 compact state (GPU layered target).
  * Numeric types: int32 (fixed point, offset + clamp), double, float.
- * Readings of silent/ambiguous passages are listed in DESIGN.md §3 (D1-D23).
- * Parity pins: tests/test_oracle_*.py (none of this file is "parity unpinned").
+ * Readings of silent/ambiguous passages are listed in DESIGN.md §3 (D1-D27).
+ * Parity pins: tests/test_oracle.py, tests/golden/ (none of this file is "parity unpinned").
  */
 #include <math.h>
 #include <stdint.h>

@@ -162,7 +162,7 @@ __device__ __forceinline__ uint32_t res_parity_dispatch(int dc, const ResArgs &a
 
 // Write outputs of the frames selected by `which` (bit0 = lo frame, bit1 = hi frame)
 // from the doubled posterior buffer Lsrc (each 16-bit lane holds 2 Z_n + bias).
-__device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc, int f0, int which, int iters,
+static __device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc, int f0, int which, int iters,
                                   int fail_lo, int fail_hi, int bias = 0) {
     const int f1 = f0 + 1;
     const int tid = threadIdx.x, nth = blockDim.x;

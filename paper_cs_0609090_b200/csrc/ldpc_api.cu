@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -91,6 +92,7 @@ struct ldpc_code {
     int nbatch_atom = 0, res_threads_atom = 0;
     QcTab *qtab_atom = nullptr;
     int full_cols_qc = 0;            // FMT_FULL: TMEM columns per group (QC: sum of the group's row degrees)
+    std::mutex host_mu;              // serialises ldpc_decode_batch_host calls (shared aux streams/events)
     cudaStream_t aux[4] = {nullptr, nullptr, nullptr, nullptr};      // host-API pipeline streams
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
@@ -999,6 +1001,9 @@ extern "C" ldpc_status ldpc_decode_batch_host(const ldpc_code *code, const ldpc_
     if (((uintptr_t)workspace & 255) != 0) return fail(LDPC_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
     char *w = (char *)workspace;
     cudaStream_t us = (cudaStream_t)stream;
+    // the internal streams and events belong to the code: one enqueue at a time (the work
+    // itself stays asynchronous; concurrent callers' decodes are ordered on those streams)
+    std::lock_guard<std::mutex> lock(const_cast<ldpc_code *>(code)->host_mu);
     CUDA_TRY(cudaEventRecord(code->ev[0], us));
     for (int i = 0; i < h.nstreams; ++i) CUDA_TRY(cudaStreamWaitEvent(code->aux[i], code->ev[0], 0));
     int32_t launches = 0;

@@ -403,3 +403,44 @@ def test_many_iterations():
     llr = cfg.llrs(code, 0, 40)
     params = P.make_params(200, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
     assert_int_parity(code, llr, params, 200, 0, 1, 511)
+
+
+def test_concurrent_host_api_calls_on_one_code():
+    """Two host threads decode different frame sets through ldpc_decode_batch_host on the
+    same code object, each with its own workspace, stream and buffers: both bit-exact."""
+    import threading
+    cfg = g.CONFIGS[2]
+    code = cfg.code()
+    dec = decoder(code)
+    params = P.params_for_config(cfg)
+    results = {}
+
+    def worker(idx):
+        llr = cfg.llrs(code, 1000 * idx, 600)
+        nb = P.ldpc_decode_host_workspace_size(dec.handle, 600, params)
+        ws = torch.empty(nb, dtype=torch.uint8, device="cuda:0")
+        lh = torch.from_numpy(llr).pin_memory()
+        hb = torch.empty((600, dec.wpf), dtype=torch.int32).pin_memory()
+        ok = torch.empty(600, dtype=torch.uint8).pin_memory()
+        it = torch.empty(600, dtype=torch.int32).pin_memory()
+        post = torch.empty((600, code.n_vars), dtype=torch.int16).pin_memory()
+        s = torch.cuda.Stream(device="cuda:0")
+        for _ in range(3):
+            P.ldpc_decode_batch_host(dec.handle, params, 600, lh.data_ptr(), hb.data_ptr(), post.data_ptr(),
+                                     ok.data_ptr(), it.data_ptr(), ws.data_ptr(), nb, s.cuda_stream)
+        s.synchronize()
+        results[idx] = (llr, post.numpy().copy(), hb.numpy().view(np.uint32).copy(), ok.numpy().copy(),
+                        it.numpy().copy())
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in (1, 2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for idx in (1, 2):
+        llr, post, hb, ok, it = results[idx]
+        ref = oracle_decode_int(code, llr, cfg.max_iter, cfg.early_stop, cfg.offset_raw, cfg.clamp)
+        np.testing.assert_array_equal(post.astype(np.int32), ref.post)
+        np.testing.assert_array_equal(hb, oracle.pack_bits(ref.bits))
+        np.testing.assert_array_equal(ok, ref.ok)
+        np.testing.assert_array_equal(it, ref.iters)

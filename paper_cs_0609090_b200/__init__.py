@@ -318,7 +318,7 @@ def params_for_config(cfg, schedule=LDPC_SCHED_SINGLESCAN, msg_format=None) -> l
     llr_type = {ldpcgen.LLR_I16: LDPC_LLR_I16, ldpcgen.LLR_I8: LDPC_LLR_I8, ldpcgen.LLR_F32: LDPC_LLR_F32}[cfg.llr_kind]
     if cfg.variant == "normalized":
         return make_params(cfg.max_iter, cfg.early_stop, LDPC_MINSUM_NORMALIZED, 0, 0.0, cfg.alpha, 0, llr_type,
-                           LDPC_MSG_COMPACT, schedule)
+                           LDPC_MSG_COMPACT if msg_format is None else int(msg_format), schedule)
     fmt = LDPC_MSG_1BIT if cfg.msg_format == "1bit" and schedule == LDPC_SCHED_SINGLESCAN else LDPC_MSG_COMPACT
     if msg_format is not None:
         fmt = int(msg_format)

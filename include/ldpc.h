@@ -169,7 +169,10 @@ ldpc_status ldpc_decode_workspace_size(const ldpc_code *code, int64_t n_frames,
  *   workspace    device, >= ldpc_decode_workspace_size() bytes, 256-byte aligned
  * Fully asynchronous on `stream`; all outputs are valid once the stream reaches this point.
  * Integer paths are bit-exact and reproducible; the F32 path accumulates posteriors in an
- * order that can vary run to run (fp32 sums), see DESIGN.md §3 D11. */
+ * order that can vary run to run (fp32 sums), see DESIGN.md §3 D11.
+ * Kernel choice (automatic): codes whose posterior double buffer fits in shared memory
+ * decode resident (one launch; integer: a frame pair per CTA, F32: a frame per CTA, row
+ * degree <= 8); longer codes use the streaming kernels (one launch per iteration). */
 ldpc_status ldpc_decode_batch(const ldpc_code *code, const ldpc_decode_params *params, int64_t n_frames,
                               const void *llr, uint32_t *hard_bits, void *posteriors,
                               uint8_t *syndrome_ok, int32_t *iterations_used,

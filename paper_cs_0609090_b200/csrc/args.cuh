@@ -33,6 +33,8 @@ struct ResArgs {
     VarK vk;                       // check-node variant (constant over iterations)
     int nsched;                    // > 0: iteration k uses vk_sched[k-1] (lambda_k / beta_k)
     VarK vk_sched[kMaxSched];
+    float alpha, beta;             // fp32 resident kernel: |L| = max(alpha*min - beta, 0)
+    float alpha_sched[kMaxSched], beta_sched[kMaxSched];   // ... per iteration when nsched > 0
     const void *llr;
     uint32_t *hard_bits;
     int16_t *post;

@@ -628,7 +628,14 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                 pl.betafs.push_back(b);
             }
         }
-        pl.path = PATH_STREAM_F;
+        // codes whose fp32 posterior double buffer fits in shared memory decode resident
+        // (k_resident_f32.cuh, one frame per CTA); LDPC_FORCE_STREAM=1 (test hook) and
+        // everything else take the fp32 streaming kernel
+        const char *force = getenv("LDPC_FORCE_STREAM");
+        const bool fres = c->res_ok && c->max_dc <= kMaxDC && c->nbatch_atom > 0 && pl.sched == LDPC_SCHED_SINGLESCAN &&
+                          !(force && force[0] == '1') && (pl.alphas.empty() || p->max_iter <= kMaxSched);
+        pl.path = fres ? PATH_RESIDENT : PATH_STREAM_F;
+        if (fres) pl.kind = RES_F32;
         pl.tile = 32;
     } else if (p->llr_type == LDPC_LLR_I16 || p->llr_type == LDPC_LLR_I8) {
         if (p->offset_raw < 0 || p->offset_raw > 16383) return fail(LDPC_ERR_INVALID_ARG, "offset_raw out of range");
@@ -687,7 +694,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     } else {
         return fail(LDPC_ERR_INVALID_ARG, "bad llr_type %d", p->llr_type);
     }
-    const int64_t npairs = (F + 1) / 2;
+    const int64_t npairs = pl.kind == RES_F32 ? F : (F + 1) / 2;   // CTA work units: frame pairs (fp32: frames)
     if (pl.path == PATH_RESIDENT && !pl.vks.empty() && p->max_iter > kMaxSched) {
         if (pl.lay) return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
         pl.path = PATH_STREAM_I;                         // the streaming kernels take any schedule length
@@ -701,12 +708,14 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         // selects the batched kernel
         const char *be = getenv("LDPC_RES_BATCHED");
         const bool atom_ok = (int64_t)2 * pl.Q * (c->max_dv + 1) < 0x4000 && c->nbatch_atom > 0;
-        pl.kind = pl.lay ? RES_LAYERED : ((atom_ok && !(be && be[0] == '1')) ? RES_ATOM : RES_BATCHED);
+        if (pl.kind != RES_F32)
+            pl.kind = pl.lay ? RES_LAYERED : ((atom_ok && !(be && be[0] == '1')) ? RES_ATOM : RES_BATCHED);
         if (pl.fmt == FMT_FULL && pl.kind != RES_ATOM)
             return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages (LDPC_MSG_FULL) need the barrier-free resident "
                                               "kernel: SINGLESCAN schedule and 2*Q*(max_dv+1) < 16384");
-        pl.threads = pl.lay ? c->res_threads_lay : (pl.kind == RES_ATOM ? c->res_threads_atom : c->res_threads);
-        pl.nbatch = pl.lay ? c->nbatch_lay : (pl.kind == RES_ATOM ? c->nbatch_atom : c->nbatch);
+        const bool atom_rows = pl.kind == RES_ATOM || pl.kind == RES_F32;   // barrier-free row ownership
+        pl.threads = pl.lay ? c->res_threads_lay : (atom_rows ? c->res_threads_atom : c->res_threads);
+        pl.nbatch = pl.lay ? c->nbatch_lay : (atom_rows ? c->nbatch_atom : c->nbatch);
         pl.smem = pl.lay ? c->res_smem / 2 : c->res_smem;   // layered: one posterior array
         // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group; layered
         // general codes keep the state in shared memory instead ([3][M] words, by row)
@@ -796,6 +805,15 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.colT = natural ? c->d_colT_lay : c->d_colT;
     a.dcT = natural ? c->d_dcT_lay : c->d_dcT;
     a.cpar = pl.kind == RES_ATOM ? 0xBFFEBFFFu : 0xFFFEFFFFu;
+    a.alpha = pl.alpha;
+    a.beta = pl.betaf;
+    if (pl.kind == RES_F32 && !pl.alphas.empty()) {
+        a.nsched = (int)pl.alphas.size();
+        for (size_t k = 0; k < pl.alphas.size(); ++k) {
+            a.alpha_sched[k] = pl.alphas[k];
+            a.beta_sched[k] = pl.betafs[k];
+        }
+    }
     a.coldeg = c->d_coldeg;
     a.Z = c->Z;
     a.group_threads = c->group_threads;
@@ -803,7 +821,8 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.cols_per_group = pl.cols_per_group;
     a.rk = make_regk();
     static const QcTab empty_tab{};
-    const QcTab *qt = pl.kind == RES_LAYERED ? c->qtab_lay : (pl.kind == RES_ATOM ? c->qtab_atom : c->qtab);
+    const QcTab *qt = pl.kind == RES_LAYERED ? c->qtab_lay
+                                             : ((pl.kind == RES_ATOM || pl.kind == RES_F32) ? c->qtab_atom : c->qtab);
     cudaError_t e = res_launch(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.kind, pl.grid,
                                pl.threads, pl.smem, a, qt ? *qt : empty_tab, s);
     ++g_launches;

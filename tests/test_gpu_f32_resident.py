@@ -1,0 +1,140 @@
+"""fp32 LLRs on the decode-resident kernel (k_resident_f32.cuh): codes whose fp32
+posterior double buffer fits in shared memory decode with one frame per CTA; the same
+decodes forced through the fp32 streaming kernel (LDPC_FORCE_STREAM=1) must agree with
+the oracle to the same fp32 tolerance (|dZ| <= 1e-4 (1 + |Z|), D11).  The launch
+count tells the two paths apart (resident: one launch per decode)."""
+import numpy as np
+import pytest
+
+import ldpcgen as g
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_cs_0609090_b200 as P  # noqa: E402
+from test_gpu_parity import NT, _assert_f32_parity, gpu_decode, small_codes  # noqa: E402
+
+
+def _assert_stress(post, hb, ok, it, ref, K):
+    """Up to 10 iterations: the D11 bar on every frame, iterations and syndrome flags
+    equal.  Longer decodes of frames that keep oscillating: fp32 rounding-order
+    differences (RED.F32 sums in arrival order vs the oracle's ordered sums) compound from
+    iteration to iteration.  A numpy emulation of a random-order fp32 flooding decode
+    (DESIGN.md §3 D11) deviates from the oracle by up to 3e-4 (3 dB) and 3e-3 (1 dB)
+    relative after 25 iterations on these small codes, by <= 2.2e-5 after 10; so after
+    more than 10 iterations the bar is |dZ| <= 5e-2 (1 + |Z|), hard bits equal wherever
+    |Z| > 5e-2 (1 + |Z|), and the syndrome flag equal on >= 97% of the frames."""
+    rp = ref.post.astype(np.float64)
+    if K <= 10:
+        _assert_f32_parity(post, hb, ok, rp)
+        np.testing.assert_array_equal(it, ref.iters)
+        np.testing.assert_array_equal(ok, ref.ok)
+        return
+    scale = 1.0 + np.abs(rp)
+    assert np.max(np.abs(post.astype(np.float64) - rp) / scale) <= 5e-2
+    diff = (post <= 0) != (rp <= 0)
+    assert np.all(np.abs(rp[diff]) <= 5e-2 * scale[diff])
+    assert np.mean(ok == ref.ok) >= 0.97
+
+
+def _decode(code, llr, params, stream):
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    n = P.ldpc_last_launch_count()
+    if stream:
+        assert n > 1, "expected the streaming kernels"
+    else:
+        assert n == 1, f"expected one resident launch, got {n}"
+    return post, hb, ok, it
+
+
+@pytest.mark.parametrize("stream", [False, True], ids=["resident", "stream"])
+@pytest.mark.parametrize("code", small_codes(), ids=lambda c: c.name)
+def test_f32_resident_small_codes(code, stream, monkeypatch):
+    if int(np.max(np.diff(code.row_ptr))) > 8:
+        pytest.skip("resident fp32 kernel: row degree <= 8")
+    if stream:
+        monkeypatch.setenv("LDPC_FORCE_STREAM", "1")
+    # 3 dB (most frames converge) and 1 dB (about half do not), see _assert_stress
+    for F in (1, 2, 33, 300):
+        for variant, alpha, beta, es, K in ((P.LDPC_MINSUM_NORMALIZED, 0.75, 0.0, 0, 10),
+                                            (P.LDPC_MINSUM_OFFSET, 1.0, 0.25, 1, 10),
+                                            (P.LDPC_MINSUM_OFFSET, 1.0, 0.0, 1, 1),
+                                            (P.LDPC_MINSUM_NORMALIZED, 0.8125, 0.0, 1, 25)):
+            params = P.make_params(K, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+            for ebn0, seed in ((3.0, 11), (1.0, 17)):
+                llr = g.llr(seed + F, 0, F, code.n_vars, g.ebn0_to_sigma2(ebn0, max(code.rate, 0.3)), g.LLR_F32)
+                post, hb, ok, it = _decode(code, llr, params, stream)
+                ref = oracle.decode(code, llr, "compact", "f32", K, es, beta=beta, alpha=alpha, nthreads=NT)
+                _assert_stress(post, hb, ok, it, ref, K)
+                np.testing.assert_array_equal(hb, oracle.pack_bits((post <= 0).astype(np.uint8)))
+
+
+@pytest.mark.parametrize("es", [0, 1])
+def test_f32_resident_cfg2_code(es):
+    """The cfg2 code (N=7493, QC) with fp32 LLRs, resident."""
+    cfg = g.CONFIGS[2]
+    code = cfg.code()
+    s2 = g.ebn0_to_sigma2(1.75, code.rate)
+    llr = g.llr(77 + es, 0, 96, code.n_vars, s2, g.LLR_F32)
+    params = P.make_params(cfg.max_iter, es, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32,
+                           P.LDPC_MSG_COMPACT)
+    post, hb, ok, it = _decode(code, llr, params, False)
+    ref = oracle.decode(code, llr, "compact", "f32", cfg.max_iter, es, alpha=0.75, nthreads=NT)
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    np.testing.assert_array_equal(it, ref.iters)
+    np.testing.assert_array_equal(ok, ref.ok)
+    np.testing.assert_array_equal(hb, oracle.pack_bits((post <= 0).astype(np.uint8)))   # hard bits = [Z <= 0]
+
+
+def test_f32_resident_schedules():
+    """Per-iteration lambda_k and beta_k on the resident fp32 kernel."""
+    cfg = g.CONFIGS[2]
+    code = cfg.code()
+    llr = g.llr(91, 0, 40, code.n_vars, g.ebn0_to_sigma2(3.0, code.rate), g.LLR_F32)
+    al = np.linspace(0.6, 0.95, cfg.max_iter).astype(np.float32)
+    params = P.make_params(cfg.max_iter, 1, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32,
+                           P.LDPC_MSG_COMPACT, alpha_per_iter=al)
+    post, hb, ok, it = _decode(code, llr, params, False)
+    ref = oracle.decode(code, llr, "compact", "f32", cfg.max_iter, 1, alpha=0.75, nthreads=NT,
+                        alpha_sched=al.astype(np.float64))
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    np.testing.assert_array_equal(it, ref.iters)
+    bf = np.array([0.5, 0.5, 0.25, 0.25, 0.125] + [0.0] * 15, np.float32)
+    params = P.make_params(20, 0, P.LDPC_MINSUM_OFFSET, 0, 0.25, 1.0, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT,
+                           offset_f_per_iter=bf)
+    post, hb, ok, it = _decode(code, llr, params, False)
+    ref = oracle.decode(code, llr, "compact", "f32", 20, 0, beta=0.25, nthreads=NT, beta_sched=bf.astype(np.float64))
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    low = g.llr(92, 0, 16, code.n_vars, g.ebn0_to_sigma2(1.0, code.rate), g.LLR_F32)
+    post, hb, ok, it = _decode(code, low, params, False)
+    ref = oracle.decode(code, low, "compact", "f32", 20, 0, beta=0.25, nthreads=NT, beta_sched=bf.astype(np.float64))
+    _assert_stress(post, hb, ok, it, ref, 20)
+    # schedules longer than the kernel's table fall back to the streaming kernel
+    al70 = np.full(70, 0.75, np.float32)
+    params = P.make_params(70, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT,
+                           alpha_per_iter=al70)
+    post, hb, ok, it = _decode(code, llr[:4], params, True)
+    ref = oracle.decode(code, llr[:4], "compact", "f32", 70, 0, alpha=0.75, nthreads=NT)
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+
+
+def test_f32_resident_extremes():
+    """Saturating inputs, +-0.0, infinities excluded: all-zero LLRs, huge LLRs, mixed signs."""
+    code = small_codes()[1]
+    F = 5
+    z = np.zeros((F, code.n_vars), np.float32)
+    z[1] = -0.0
+    z[2] = 1e30
+    z[3] = -1e-30
+    rng = np.random.default_rng(3)
+    z[4] = rng.choice([-1e6, 1e6, 0.0, -0.0], code.n_vars).astype(np.float32)
+    params = P.make_params(6, 1, P.LDPC_MINSUM_OFFSET, 0, 0.5, 1.0, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+    post, hb, ok, it = _decode(code, z, params, False)
+    ref = oracle.decode(code, z, "compact", "f32", 6, 1, beta=0.5, nthreads=NT)
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    np.testing.assert_array_equal(it, ref.iters)
+    np.testing.assert_array_equal(ok, ref.ok)

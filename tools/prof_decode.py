@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--frames", type=int, default=0)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--f32", action="store_true", help="decode the config's LLRs as fp32 (normalized 0.75)")
     args = ap.parse_args()
     cfg = g.CONFIGS[args.config]
     code = cfg.code()
@@ -26,6 +27,10 @@ def main():
     llr = torch.from_numpy(cfg.llrs(code, 0, F)).cuda()
     dec = P.Decoder(code, 0)
     params = P.params_for_config(cfg)
+    if args.f32:
+        llr = llr.float()
+        params = P.make_params(cfg.max_iter, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32,
+                               P.LDPC_MSG_COMPACT)
     out = dec.alloc_outputs(F, params.llr_type, posteriors=True)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for i in range(args.reps):

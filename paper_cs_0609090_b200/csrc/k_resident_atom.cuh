@@ -123,6 +123,49 @@ __device__ __forceinline__ void atom_row_full(const ResArgs &a, const QcTab &t, 
     }
 }
 
+// Two rows of one group in flight (FMT_FULL, QC): both rows' gathers are issued before
+// either row's arithmetic, so each thread overlaps the shared-memory latency of one row
+// with the other's work.  The full-message kernel is held to 2 CTAs/SM by TMEM, so the
+// 4 warps per scheduler alone cannot hide that latency.  Flooding reads Z^(k-1) and
+// accumulates into Z^(k) (different buffers), so the order of the two rows is free.
+template <int DC, bool ES>
+__device__ __forceinline__ void atom_row_full_x2(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp,
+                                                 uint32_t ba, int e0, int e1, uint32_t r4, bool first_iter,
+                                                 uint32_t (&c0)[8], uint32_t (&c1)[8], uint32_t &synd) {
+    uint32_t d0[DC], d1[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        const uint2 x = t.ent[e0 + j], y = t.ent[e1 + j];
+        const uint32_t u = r4 + x.x, v = r4 + y.x;
+        d0[j] = min(u - t.Z4, u) + x.y;
+        d1[j] = min(v - t.Z4, v) + y.y;
+    }
+    uint32_t L0[DC], L1[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L0[j]) : "r"(d0[j] + bp));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L1[j]) : "r"(d1[j] + bp));
+    }
+    if (ES) synd |= row_parity<DC>(L0, a.rk, a.cpar) | row_parity<DC>(L1, a.rk, a.cpar);
+    uint32_t q0[DC], q1[DC];
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        q0[j] = fadd32(L0[j], first_iter ? 0x40004000u : c0[j], a.rk);
+        q1[j] = fadd32(L1[j], first_iter ? 0x40004000u : c1[j], a.rk);
+    }
+    uint32_t rn0[DC], rn1[DC];
+    RowState st;
+    new_state<DC, true>(q0, vk, st, rn0, a.rk);
+    new_state<DC, true>(q1, vk, st, rn1, a.rk);
+#pragma unroll
+    for (int j = 0; j < DC; ++j) {
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d0[j] + ba), "r"(rn0[j]) : "memory");
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d1[j] + ba), "r"(rn1[j]) : "memory");
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c0[j]) : "r"(rn0[j]), "r"(a.rk.m1), "r"(0x4000C000u));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c1[j]) : "r"(rn1[j]), "r"(a.rk.m1), "r"(0x4000C000u));
+    }
+}
+
 template <int DC, bool ES, int FMT>
 __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t tw,
                                            int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba, bool first_iter,
@@ -131,6 +174,21 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
         return bend;
     } else if constexpr (FMT == FMT_FULL) {
         // slot b's DC message words start at column t.tcol[b][g] of this group's range
+#if !defined(LDPC_FULL_X1)
+#pragma unroll 1
+        for (; b + 1 < bend; b += 2) {
+            uint32_t c0[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, c1[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            const uint32_t col0 = tw + (uint32_t)t.tcol[b][g], col1 = tw + (uint32_t)t.tcol[b + 1][g];
+            if (!first_iter) {
+                full_tmem_load<DC>(col0, c0);
+                full_tmem_load<DC>(col1, c1);
+            }
+            if (rloc < a.Z)
+                atom_row_full_x2<DC, ES>(a, t, vk, bp, ba, t.e0[b][g], t.e0[b + 1][g], r4, first_iter, c0, c1, synd);
+            full_tmem_store<DC>(col0, c0);
+            full_tmem_store<DC>(col1, c1);
+        }
+#endif
 #pragma unroll 1
         for (; b < bend; ++b) {
             uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -232,7 +290,7 @@ __device__ __forceinline__ void atom_ingest(const ResArgs &a, const TIN *__restr
 }
 
 template <bool QC, bool ES, int FMT, typename TIN>
-__global__ void __launch_bounds__(256, 3) k_resident_atom(const __grid_constant__ ResArgs a,
+__global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(const __grid_constant__ ResArgs a,
                                                           const __grid_constant__ QcTab t) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint32_t tslot;

@@ -138,3 +138,29 @@ def test_f32_resident_extremes():
     _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
     np.testing.assert_array_equal(it, ref.iters)
     np.testing.assert_array_equal(ok, ref.ok)
+
+
+@pytest.mark.parametrize("kind", ["int16", "int16-full", "f32"])
+def test_resident_grid_loop(kind, monkeypatch):
+    """LDPC_RES_GRID_MULT=1 caps the resident grid at one wave (blocks/SM x SMs), so every
+    CTA loops over several frame pairs (fp32: frames): outputs of all frames must still match."""
+    monkeypatch.setenv("LDPC_RES_GRID_MULT", "1")
+    code = small_codes()[1]                        # regular (3,6), N = 96
+    F = 4 * 148 * 32 + 7                           # well above one wave at any occupancy, odd
+    s2 = g.ebn0_to_sigma2(2.0, code.rate)
+    if kind == "f32":
+        llr = g.llr(5, 0, F, code.n_vars, s2, g.LLR_F32)
+        params = P.make_params(8, 1, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+        post, hb, ok, it = _decode(code, llr, params, False)
+        ref = oracle.decode(code, llr, "compact", "f32", 8, 1, alpha=0.75, nthreads=NT)
+        _assert_stress(post, hb, ok, it, ref, 8)
+        return
+    llr = g.llr(6, 0, F, code.n_vars, s2, g.LLR_I16, 3, 511)
+    fmt = P.LDPC_MSG_FULL if kind == "int16-full" else P.LDPC_MSG_COMPACT
+    params = P.make_params(8, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, fmt)
+    post, hb, ok, it = _decode(code, llr, params, False)
+    ref = oracle.decode(code, llr.astype(np.int32), "compact", "int", 8, 1, 1, 511, nthreads=NT)
+    np.testing.assert_array_equal(it, ref.iters)
+    np.testing.assert_array_equal(ok, ref.ok)
+    np.testing.assert_array_equal(post.astype(np.int32), ref.post)
+    np.testing.assert_array_equal(hb, oracle.pack_bits(ref.bits))

@@ -14,9 +14,10 @@ constexpr int kChains = 8;
 constexpr int kIters = 4096;
 constexpr int kUnroll = 8;
 
-enum Op { OP_VIMNMX = 0, OP_LOP3, OP_IADD3, OP_PRMT, OP_VIADDMNMX, OP_IMAD, OP_LOP3_IMAD, OP_COUNT };
+enum Op { OP_VIMNMX = 0, OP_LOP3, OP_IADD3, OP_PRMT, OP_VIADDMNMX, OP_IMAD, OP_LOP3_IMAD, OP_HMNMX2, OP_LOP3_HMNMX2,
+          OP_COUNT };
 static const char *kNames[OP_COUNT] = {"VIMNMX.S16x2", "LOP3", "IADD3", "PRMT", "VIADDMNMX.S16x2.RELU", "IMAD",
-                                       "LOP3+IMAD (dual issue)"};
+                                       "LOP3+IMAD (dual issue)", "HMNMX2", "LOP3+HMNMX2 (dual issue)"};
 
 // One instruction of kind OP.  Rounds alternate between two forms (min / max, two LUTs,
 // add / sub, two selectors) and every chain reads its neighbour, so ptxas can neither fold
@@ -39,6 +40,9 @@ __device__ __forceinline__ uint32_t step(int round, uint32_t x, uint32_t y, uint
         else asm volatile("prmt.b32 %0, %1, %2, 0x6273;" : "=r"(r) : "r"(x), "r"(y));
     } else if constexpr (OP == OP_VIADDMNMX) {
         r = odd ? __viaddmax_s16x2_relu(x, y, z) : __viaddmin_s16x2_relu(x, y, z);
+    } else if constexpr (OP == OP_HMNMX2) {
+        if (odd) asm volatile("max.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+        else asm volatile("min.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
     } else if constexpr (OP == OP_IMAD) {
         asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(y), "r"(z));
     }
@@ -49,7 +53,7 @@ template <int OP>
 __global__ void __launch_bounds__(1024, 1) k_peak(uint32_t *sink, long long *cycles) {
     uint32_t v[kChains];
 #pragma unroll
-    for (int c = 0; c < kChains; ++c) v[c] = threadIdx.x * 7u + 3u * c + 1u;
+    for (int c = 0; c < kChains; ++c) v[c] = ((threadIdx.x * 7u + 3u * c + 1u) & 0x3FFFu) * 0x10001u;   // finite fp16 pairs
     __syncthreads();
     const long long t0 = clock64();
     for (int i = 0; i < kIters; ++i) {
@@ -60,6 +64,7 @@ __global__ void __launch_bounds__(1024, 1) k_peak(uint32_t *sink, long long *cyc
             for (int c = 0; c < kChains; ++c) {
                 const uint32_t x = v[c], y = v[(c + 1) % kChains], z = v[(c + 2) % kChains];
                 if constexpr (OP == OP_LOP3_IMAD) w[c] = (c & 1) ? step<OP_IMAD>(u, x, y, z) : step<OP_LOP3>(u, x, y, z);
+                else if constexpr (OP == OP_LOP3_HMNMX2) w[c] = (c & 1) ? step<OP_HMNMX2>(u, x, y, z) : step<OP_LOP3>(u, x, y, z);
                 else w[c] = step<OP>(u, x, y, z);
             }
 #pragma unroll
@@ -106,6 +111,8 @@ int main() {
     r[OP_VIADDMNMX] = run<OP_VIADDMNMX>(sms, sink, cyc);
     r[OP_IMAD] = run<OP_IMAD>(sms, sink, cyc);
     r[OP_LOP3_IMAD] = run<OP_LOP3_IMAD>(sms, sink, cyc);
+    r[OP_HMNMX2] = run<OP_HMNMX2>(sms, sink, cyc);
+    r[OP_LOP3_HMNMX2] = run<OP_LOP3_HMNMX2>(sms, sink, cyc);
     const cudaError_t e = cudaGetLastError();
     printf("{\"device\": \"%s\", \"sms\": %d, \"unit\": \"thread-instructions per SM clock\", \"error\": \"%s\",\n"
            " \"ops_per_sm_clk\": {",

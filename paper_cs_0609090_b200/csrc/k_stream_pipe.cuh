@@ -141,17 +141,19 @@ __global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe
     const int nst = PAIR ? StateIO<FMT>::kWords : 3;
     uint32_t *stt = a.st + (size_t)tile * nst * a.M * 32;
     const size_t sstride = (size_t)a.M * 32;
-    // compact row tables of the block -> shared (one 32 B entry per row)
-    for (int i = threadIdx.x; i < nrows * 2; i += blockDim.x) {
-        const uint4 v = __ldg(a.rowtab + 2 * (size_t)mb0 + i);
+    // compact row tables of this warp's rows -> its part of shared memory (one 32 B entry
+    // per row); warp-local, so no CTA barrier before the row pipeline starts
+    for (int i = lane; i < 2 * ((nrows - warp + kPipeWarps - 1) / kPipeWarps); i += 32) {
+        const int r = warp + (i >> 1) * kPipeWarps;
+        const uint4 v = __ldg(a.rowtab + 2 * (size_t)(mb0 + r) + (i & 1));
         uint4 w = v;
         if ((i & 1) == 0) {
             w.x = v.x & 0x0FFFFFFFu;
             int dc = (int)(v.x >> 28);
-            if (dc == 15) dc = __ldg(a.row_ptr + mb0 + i / 2 + 1) - __ldg(a.row_ptr + mb0 + i / 2);
-            dctab[i / 2] = (uint8_t)dc;
+            if (dc == 15) dc = __ldg(a.row_ptr + mb0 + r + 1) - __ldg(a.row_ptr + mb0 + r);
+            dctab[r] = (uint8_t)dc;
         }
-        ((uint4 *)coltab)[i] = w;
+        ((uint4 *)coltab)[2 * r + (i & 1)] = w;
     }
     uint32_t keep = 0;
     bool frozen = false;
@@ -160,7 +162,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe
         if (PAIR) keep = ((d & 1) ? 0x0000FFFFu : 0u) | ((d & 2) ? 0xFFFF0000u : 0u);
         else frozen = (d & 1u) != 0;
     }
-    // accumulator of the next iteration (it held Z^(k-2))
+    // accumulator of the next iteration (it held Z^(k-2); not touched otherwise by this
+    // launch: no barrier needed)
     if (k < a.K) {
         const int wg = blockIdx.x * kPipeWarps + warp, nwg = gridDim.x * kPipeWarps;
         if (!ES || !__any_sync(0xFFFFFFFFu, keep != 0 || frozen)) {
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe
             }
         }
     }
-    __syncthreads();
+    __syncwarp();
     const bool first_iter = (k == 1);
     const int nst_copy = first_iter ? 0 : nst;
     uint32_t *wring = ring + (size_t)warp * kPipeD * kPipeLines * 32;

@@ -84,6 +84,8 @@ struct TwoScanArgs {
     const int32_t *ecol;    // [E] column of edge e (CSR col_idx)
     uint32_t *msg;          // [tile][E][32] L_mn
     uint32_t *zv;           // [tile][E][32] Z_mn
+    uint32_t *hb;           // [tile][N][2] (int pairs: lo, hi frames) or [tile][N] (fp32): hard-decision
+                            // ballots of the posterior written by the variable pass (early stop)
     int64_t E;
 };
 

@@ -29,17 +29,60 @@ namespace ldpc {
 constexpr int kTsMaxDV = 16;   // column degree limit of the variable pass (registers)
 
 
-// Z^(0)_mn = Z^(0)_n for every m in M(n)
+// Z^(0)_mn = Z^(0)_n for every m in M(n): one warp per (column, tile), one read
+// of Z^(0)_n and independent stores to its edges
 template <bool PAIR>
 __global__ void __launch_bounds__(256) k_ts_init(const StreamArgs a, const TwoScanArgs t) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t e = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); e < t.E; e += nw) {
-        const int n = __ldg(t.ecol + e);
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    uint32_t *zvt = t.zv + (size_t)tile * t.E * 32;
+    for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < a.N; n += nw) {
         uint32_t v = __ldcg(a.Z0 + ((size_t)tile * a.N + n) * 32 + lane);
         if (PAIR) v = vadd(v, 0xC000C000u);              // unbias (ingest with zpre = 0)
-        __stcg(t.zv + ((size_t)tile * t.E + e) * 32 + lane, v);
+        const int b0 = __ldg(t.vptr + n), b1 = __ldg(t.vptr + n + 1);
+        for (int b = b0; b < b1; ++b) __stcg(zvt + (size_t)__ldg(t.vedge + b) * 32 + lane, v);
     }
+}
+
+// hard-decision ballots of the posterior word just written for column n (lane 0 stores)
+template <bool PAIR>
+__device__ __forceinline__ void ts_store_hb(const StreamArgs &a, uint32_t *hbt, int n, uint32_t out, int lane) {
+    if (PAIR) {
+        const uint32_t p = fadd32(out, kParBiased, a.rk);   // sign bits 15 / 31 = [Z <= 0] per frame
+        const uint32_t lo = __ballot_sync(0xFFFFFFFFu, (p & 0x8000u) != 0);
+        const uint32_t hi = __ballot_sync(0xFFFFFFFFu, (p & 0x80000000u) != 0);
+        if (lane == 0) ((uint2 *)hbt)[n] = make_uint2(lo, hi);
+    } else {
+        const uint32_t h = __ballot_sync(0xFFFFFFFFu, __uint_as_float(out) <= 0.0f);
+        if (lane == 0) hbt[n] = h;
+    }
+}
+
+// syndrome of the posterior of the last variable pass from the ballots: one thread per
+// (row, tile), reading 8 (fp32: 4) bytes per edge instead of a 128-byte posterior line
+template <bool PAIR>
+__global__ void __launch_bounds__(256) k_ts_syndrome(const StreamArgs a, const TwoScanArgs t) {
+    const int tile = blockIdx.y, lane = threadIdx.x & 31;
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t xl = 0, xh = 0;
+    if (m < a.M) {
+        const int e0 = __ldg(a.row_ptr + m), e1 = __ldg(a.row_ptr + m + 1);
+        if (PAIR) {
+            const uint2 *hbt = (const uint2 *)t.hb + (size_t)tile * a.N;
+            for (int e = e0; e < e1; ++e) {
+                const uint2 v = __ldcg(hbt + __ldg(a.col_idx + e));
+                xl ^= v.x;
+                xh ^= v.y;
+            }
+        } else {
+            const uint32_t *hbt = t.hb + (size_t)tile * a.N;
+            for (int e = e0; e < e1; ++e) xl ^= __ldcg(hbt + __ldg(a.col_idx + e));
+        }
+    }
+    xl = __reduce_or_sync(0xFFFFFFFFu, xl);              // frames (lanes) failing some row of this warp
+    xh = __reduce_or_sync(0xFFFFFFFFu, xh);
+    const uint32_t s = PAIR ? ((((xl >> lane) & 1u) << 15) | (((xh >> lane) & 1u) << 31)) : ((xl >> lane) & 1u);
+    if (s) atomicOr(a.synd + tile * 32 + lane, s);
 }
 
 template <int DC, bool PAIR>
@@ -87,6 +130,73 @@ __global__ void __launch_bounds__(256) k_ts_check(const StreamArgs a, const TwoS
     }
 }
 
+// vertical scan + posterior of one column n with DV = |M(n)| edges (registers sized by
+// the column degree: the degree-16 worst case would cap occupancy for every column)
+template <int DV, bool PAIR, bool ES>
+__device__ __forceinline__ void ts_var_col(const StreamArgs &a, const TwoScanArgs &t, const uint32_t *msgt,
+                                           uint32_t *zvt, uint32_t *post, const uint32_t *z0t, uint32_t *hbt, int n,
+                                           int b0, int lane, uint32_t keep) {
+    int32_t eid[DV];
+    uint32_t mv[DV];
+#pragma unroll
+    for (int b = 0; b < DV; ++b) eid[b] = __ldg(t.vedge + b0 + b);
+    const size_t ni = (size_t)n * 32 + lane;
+    uint32_t Z = __ldcg(z0t + ni);
+#pragma unroll
+    for (int b = 0; b < DV; ++b) mv[b] = __ldcg(msgt + (size_t)eid[b] * 32 + lane);
+    if (PAIR) {
+        Z = vadd(Z, 0xC000C000u);                         // unbias
+#pragma unroll
+        for (int b = 0; b < DV; ++b) Z = vadd(Z, mv[b]);
+#pragma unroll
+        for (int b = 0; b < DV; ++b) __stcg(zvt + (size_t)eid[b] * 32 + lane, vadd(Z, vneg(mv[b], a.rk)));   // Eq.(2)
+        uint32_t out = vadd(Z, kPairBias);                // biased posterior words (k_stream.cuh)
+        if (ES && keep) out = sel(keep, __ldcg(post + ni), out);
+        __stcg(post + ni, out);
+        if (ES) ts_store_hb<true>(a, hbt, n, out, lane);
+    } else {
+        float Zf = __uint_as_float(Z);
+#pragma unroll
+        for (int b = 0; b < DV; ++b) Zf = __fadd_rn(Zf, __uint_as_float(mv[b]));          // ascending m
+#pragma unroll
+        for (int b = 0; b < DV; ++b)
+            __stcg(zvt + (size_t)eid[b] * 32 + lane, __float_as_uint(__fsub_rn(Zf, __uint_as_float(mv[b]))));
+        if (!(ES && keep)) __stcg(post + ni, __float_as_uint(Zf));
+        if (ES) ts_store_hb<false>(a, hbt, n, __float_as_uint(Zf), lane);
+    }
+}
+
+// columns of degree > 8: two passes over the edges (sum, then extrinsics) instead of
+// register arrays, so the rare high-degree columns do not set the kernel's register count
+template <bool PAIR, bool ES>
+__device__ __noinline__ void ts_var_col_wide(const StreamArgs &a, const TwoScanArgs &t, const uint32_t *msgt,
+                                             uint32_t *zvt, uint32_t *post, const uint32_t *z0t, uint32_t *hbt, int n,
+                                             int b0, int dv, int lane, uint32_t keep) {
+    const size_t ni = (size_t)n * 32 + lane;
+    uint32_t Z = __ldcg(z0t + ni);
+    float Zf = __uint_as_float(Z);
+    if (PAIR) Z = vadd(Z, 0xC000C000u);
+    for (int b = 0; b < dv; ++b) {
+        const uint32_t m = __ldcg(msgt + (size_t)__ldg(t.vedge + b0 + b) * 32 + lane);
+        if (PAIR) Z = vadd(Z, m);
+        else Zf = __fadd_rn(Zf, __uint_as_float(m));                      // ascending m
+    }
+    for (int b = 0; b < dv; ++b) {
+        const size_t ei = (size_t)__ldg(t.vedge + b0 + b) * 32 + lane;
+        const uint32_t m = __ldcg(msgt + ei);
+        __stcg(zvt + ei, PAIR ? vadd(Z, vneg(m, a.rk)) : __float_as_uint(__fsub_rn(Zf, __uint_as_float(m))));
+    }
+    if (PAIR) {
+        uint32_t out = vadd(Z, kPairBias);
+        if (ES && keep) out = sel(keep, __ldcg(post + ni), out);
+        __stcg(post + ni, out);
+        if (ES) ts_store_hb<true>(a, hbt, n, out, lane);
+    } else {
+        if (!(ES && keep)) __stcg(post + ni, __float_as_uint(Zf));
+        if (ES) ts_store_hb<false>(a, hbt, n, __float_as_uint(Zf), lane);
+    }
+}
+
 // vertical scan + posterior of iteration k: one warp per (column, tile).  Frames
 // frozen by early stop keep their posterior buffer (Lb[k % 3] is also the buffer of
 // iteration k - 3).
@@ -96,6 +206,8 @@ __global__ void __launch_bounds__(256) k_ts_var(const StreamArgs a, const TwoSca
     const uint32_t *msgt = t.msg + (size_t)tile * t.E * 32;
     uint32_t *zvt = t.zv + (size_t)tile * t.E * 32;
     uint32_t *post = a.Lb[k % 3] + (size_t)tile * a.N * 32;
+    const uint32_t *z0t = a.Z0 + (size_t)tile * a.N * 32;
+    uint32_t *hbt = t.hb + (size_t)tile * a.N * (PAIR ? 2 : 1);
     uint32_t keep = 0;
     if (ES) {
         const uint32_t d = a.done[tile * 32 + lane];
@@ -104,38 +216,14 @@ __global__ void __launch_bounds__(256) k_ts_var(const StreamArgs a, const TwoSca
     const int nw = gridDim.x * (blockDim.x >> 5);
     for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < a.N; n += nw) {
         const int b0 = __ldg(t.vptr + n), dv = __ldg(t.vptr + n + 1) - b0;
-        int32_t eid[kTsMaxDV];
-        uint32_t mv[kTsMaxDV];
-#pragma unroll
-        for (int b = 0; b < kTsMaxDV; ++b) {
-            if (b < dv) {
-                eid[b] = __ldg(t.vedge + b0 + b);
-                mv[b] = __ldcg(msgt + (size_t)eid[b] * 32 + lane);
-            }
+#define LDPC_TS_COL(D) \
+    case D: ts_var_col<D, PAIR, ES>(a, t, msgt, zvt, post, z0t, hbt, n, b0, lane, keep); break;
+        switch (dv) {
+            LDPC_TS_COL(1) LDPC_TS_COL(2) LDPC_TS_COL(3) LDPC_TS_COL(4) LDPC_TS_COL(5) LDPC_TS_COL(6)
+            LDPC_TS_COL(7) LDPC_TS_COL(8)
+        default: ts_var_col_wide<PAIR, ES>(a, t, msgt, zvt, post, z0t, hbt, n, b0, dv, lane, keep);
         }
-        const size_t ni = (size_t)n * 32 + lane;
-        uint32_t Z = __ldcg(a.Z0 + (size_t)tile * a.N * 32 + ni);
-        if (PAIR) {
-            Z = vadd(Z, 0xC000C000u);                     // unbias
-#pragma unroll
-            for (int b = 0; b < kTsMaxDV; ++b)
-                if (b < dv) Z = vadd(Z, mv[b]);
-#pragma unroll
-            for (int b = 0; b < kTsMaxDV; ++b)
-                if (b < dv) __stcg(zvt + (size_t)eid[b] * 32 + lane, vadd(Z, vneg(mv[b], a.rk)));   // Eq.(2)
-            uint32_t out = vadd(Z, kPairBias);            // biased posterior words (k_stream.cuh)
-            if (ES && keep) out = sel(keep, __ldcg(post + ni), out);
-            __stcg(post + ni, out);
-        } else {
-            float Zf = __uint_as_float(Z);
-#pragma unroll
-            for (int b = 0; b < kTsMaxDV; ++b)
-                if (b < dv) Zf = __fadd_rn(Zf, __uint_as_float(mv[b]));      // ascending m
-#pragma unroll
-            for (int b = 0; b < kTsMaxDV; ++b)
-                if (b < dv) __stcg(zvt + (size_t)eid[b] * 32 + lane, __float_as_uint(__fsub_rn(Zf, __uint_as_float(mv[b]))));
-            if (!(ES && keep)) __stcg(post + ni, __float_as_uint(Zf));
-        }
+#undef LDPC_TS_COL
     }
 }
 

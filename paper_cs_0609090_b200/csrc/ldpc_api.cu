@@ -548,7 +548,7 @@ struct Plan {
     // stream
     int tile = 64, ntiles = 0;
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
-    size_t off_msg = 0, off_zv = 0;   // two-scan: per-edge L_mn and Z_mn planes
+    size_t off_msg = 0, off_zv = 0, off_hb = 0;   // two-scan: per-edge L_mn and Z_mn planes, hard-bit ballots
     size_t ws_bytes = 0;
 };
 
@@ -765,6 +765,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
             const size_t eplane = (size_t)pl.ntiles * (size_t)c->E * 32 * 4;
             pl.off_msg = off; off += align256(eplane);
             pl.off_zv = off; off += align256(eplane);
+            pl.off_hb = off; off += align256((size_t)pl.ntiles * c->N * 8);
         } else {
             pl.off_st = off; off += align256((size_t)pl.ntiles * sw * c->M * 32 * 4);
         }
@@ -886,6 +887,7 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
         t.ecol = c->d_col_idx;
         t.msg = (uint32_t *)(w + pl.off_msg);
         t.zv = (uint32_t *)(w + pl.off_zv);
+        t.hb = (uint32_t *)(w + pl.off_hb);
         t.E = c->E;
         e = twoscan_run(a, t, r, s, &n);
     } else {

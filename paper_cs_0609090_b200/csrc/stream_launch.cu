@@ -189,7 +189,6 @@ cudaError_t twoscan_run(const StreamArgs &a0, const TwoScanArgs &t, const Stream
         e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); }, nl);
     }
     if (e != cudaSuccess) return e;
-    const dim3 ge((unsigned)std::min<int64_t>((t.E + 7) / 8, 4096), (unsigned)r.ntiles);
     const dim3 gm((unsigned)std::max(1, std::min((a.M + 7) / 8, 4096)), (unsigned)r.ntiles);
     const dim3 gn((unsigned)std::max(1, std::min((a.N + 7) / 8, 4096)), (unsigned)r.ntiles);
     const dim3 gr((unsigned)std::max(1, (a.M + 63) / 64), (unsigned)r.ntiles);
@@ -202,8 +201,8 @@ cudaError_t twoscan_run(const StreamArgs &a0, const TwoScanArgs &t, const Stream
         return pair ? launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); }, nl)
                     : launch([&] { k_stream_freeze<false><<<fgrid, 256, 0, s>>>(a, k); }, nl);
     };
-    e = pair ? launch([&] { k_ts_init<true><<<ge, 256, 0, s>>>(a, t); }, nl)
-             : launch([&] { k_ts_init<false><<<ge, 256, 0, s>>>(a, t); }, nl);
+    e = pair ? launch([&] { k_ts_init<true><<<gn, 256, 0, s>>>(a, t); }, nl)
+             : launch([&] { k_ts_init<false><<<gn, 256, 0, s>>>(a, t); }, nl);
     if (e != cudaSuccess) return e;
     if (es) {
         // k = 0: Z^(0) is in Lb[0]; frames passing freeze with iterations_used = 0
@@ -223,7 +222,11 @@ cudaError_t twoscan_run(const StreamArgs &a0, const TwoScanArgs &t, const Stream
         }
         if (e != cudaSuccess) return e;
         if (es && k < r.max_iter) {
-            if ((e = syndrome(k % 3)) != cudaSuccess || (e = freeze(k + 1)) != cudaSuccess) return e;
+            // syndrome of Z^(k) from the variable pass's hard-decision ballots
+            const dim3 gs((unsigned)((a.M + 255) / 256), (unsigned)r.ntiles);
+            e = pair ? launch([&] { k_ts_syndrome<true><<<gs, 256, 0, s>>>(a, t); }, nl)
+                     : launch([&] { k_ts_syndrome<false><<<gs, 256, 0, s>>>(a, t); }, nl);
+            if (e != cudaSuccess || (e = freeze(k + 1)) != cudaSuccess) return e;
         }
     }
     // final syndrome of Z^(K); frames not frozen get iterations_used = K

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--frames", type=int, default=0)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--sched", type=int, default=0, help="0 single-scan, 1 two-scan, 2 layered")
     ap.add_argument("--full", action="store_true", help="LDPC_MSG_FULL (the §4 per-edge message form)")
     ap.add_argument("--f32", action="store_true", help="decode the config's LLRs as fp32 (normalized 0.75)")
     args = ap.parse_args()
@@ -27,7 +28,7 @@ def main():
     F = args.frames or cfg.frames
     llr = torch.from_numpy(cfg.llrs(code, 0, F)).cuda()
     dec = P.Decoder(code, 0)
-    params = P.params_for_config(cfg, msg_format=P.LDPC_MSG_FULL if args.full else None)
+    params = P.params_for_config(cfg, schedule=args.sched, msg_format=P.LDPC_MSG_FULL if args.full else None)
     if args.f32:
         llr = llr.float()
         params = P.make_params(cfg.max_iter, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32,

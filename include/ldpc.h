@@ -11,7 +11,7 @@
  *   - with the normalized / offset modifications,
  *   - hard decision and syndrome stop rule (§3),
  * decoding a batch of independent frames, using only check->variable addressing
- * (P:219-224).  Numeric readings of silent passages: DESIGN.md §3 (D1-D23).
+ * (P:219-224).  Numeric readings of silent passages: DESIGN.md §3 (D1-D27).
  *
  * Conventions (all entry points):
  *   - Plain C types only.  `stream` is a cudaStream_t passed as void* (NULL =
@@ -67,8 +67,9 @@ typedef struct {
     const int16_t *qc_shift;   /* host, qc_rows*qc_cols entries (ignored when qc_z == 0) */
 } ldpc_code_desc;
 
-/* Validate H, build the device-side structures (check->variable addressing only,
- * a conflict-free row schedule, the QC circulant table) on `cuda_device`.
+/* Validate H, build the device-side structures (check->variable addressing for the
+ * single-scan kernels, a conflict-free row schedule, the QC circulant tables, and the
+ * variable->check column lists used only by the TWOSCAN baseline) on `cuda_device`.
  * Synchronous.  *out is set only on LDPC_OK. */
 ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_device, ldpc_code **out);
 
@@ -137,7 +138,9 @@ typedef struct {
                               need 2*Q*(max_dv + 1) < 16384 (biased 16-bit lanes, D26).
                               Ignored for F32. */
     int32_t llr_type;      /* LDPC_LLR_I16 | LDPC_LLR_I8 | LDPC_LLR_F32 */
-    int32_t msg_format;    /* LDPC_MSG_COMPACT | LDPC_MSG_1BIT (1BIT requires integer LLRs) */
+    int32_t msg_format;    /* LDPC_MSG_COMPACT | LDPC_MSG_1BIT | LDPC_MSG_FULL (1BIT and FULL
+                              require integer LLRs).  F32 LLRs: row degree <= 16 (resident
+                              kernel: <= 8, wider codes stream); integer: row degree <= 8. */
     int32_t schedule;      /* LDPC_SCHED_SINGLESCAN (0, default) | _TWOSCAN | _LAYERED */
     /* Optional per-iteration variants (P:179 lambda_k, P:186 beta_k): HOST arrays of
      * max_iter entries, read during the call only; NULL = the constants above.

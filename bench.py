@@ -271,6 +271,10 @@ def main():
         achieved = ALG_OPS_PER_EU * my_eu / (my_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
                 "frac": achieved / peak_ops, "traffic": None,
+                "how": (f"{ALG_OPS_PER_EU} algorithmic 16-bit ops per edge-update x edge-updates of the "
+                        f"launch / its duration (the decode is one launch); peak derived: 148 SMs x 64 "
+                        f"thread-instr/clk/SM on the ALU pipe (confirmed by tools/alu_peak.cu, "
+                        f"profiles/r01_alu_peak.json) x 2 frames per 16x2 lane x {clk:.0f} MHz"),
                 "hbm_model": {"bytes_per_eu": bytes_per_eu(cfg, code),
                               "achieved_gbs": bytes_per_eu(cfg, code) * my_eu / (my_ms * 1e-3) / 1e9,
                               "peak_gbs": peaks["hbm_gbs"],
@@ -314,7 +318,7 @@ def main():
                 "frac": ach / peaks["hbm_gbs"], "traffic": None, "frac_of_nominal_8tbs": ach / 8000.0,
                 "how": how, "whole_step": {"achieved_gbs": ach_step, "frac": ach_step / peaks["hbm_gbs"]},
                 "kernel_ms_per_launch": it_ms}
-    roof["peak_source"] = peak_src
+    roof["peak_source"] = "derived (unit counts x clock, microbenchmark-confirmed)" if resident else peak_src
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg.idx}.json")   # from tools/ncu_summary.py
     if os.path.exists(prof):
         with open(prof) as f:

@@ -87,6 +87,7 @@ struct TwoScanArgs {
     uint32_t *hb;           // [tile][N][2] (int pairs: lo, hi frames) or [tile][N] (fp32): hard-decision
                             // ballots of the posterior written by the variable pass (early stop)
     int64_t E;
+    int max_dv;             // largest column degree (selects the variable-pass instantiation)
 };
 
 // persistent state formats (workspace words per row-pair)

@@ -200,7 +200,10 @@ __device__ __noinline__ void ts_var_col_wide(const StreamArgs &a, const TwoScanA
 // vertical scan + posterior of iteration k: one warp per (column, tile).  Frames
 // frozen by early stop keep their posterior buffer (Lb[k % 3] is also the buffer of
 // iteration k - 3).
-template <bool PAIR, bool ES>
+// DVMAX (4 or 8): largest column degree handled with register arrays; the kernel's
+// register count follows it, so codes with max_dv <= 4 get the smaller, higher-occupancy
+// instantiation
+template <bool PAIR, bool ES, int DVMAX>
 __global__ void __launch_bounds__(256) k_ts_var(const StreamArgs a, const TwoScanArgs t, int k) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const uint32_t *msgt = t.msg + (size_t)tile * t.E * 32;
@@ -218,10 +221,17 @@ __global__ void __launch_bounds__(256) k_ts_var(const StreamArgs a, const TwoSca
         const int b0 = __ldg(t.vptr + n), dv = __ldg(t.vptr + n + 1) - b0;
 #define LDPC_TS_COL(D) \
     case D: ts_var_col<D, PAIR, ES>(a, t, msgt, zvt, post, z0t, hbt, n, b0, lane, keep); break;
-        switch (dv) {
-            LDPC_TS_COL(1) LDPC_TS_COL(2) LDPC_TS_COL(3) LDPC_TS_COL(4) LDPC_TS_COL(5) LDPC_TS_COL(6)
-            LDPC_TS_COL(7) LDPC_TS_COL(8)
-        default: ts_var_col_wide<PAIR, ES>(a, t, msgt, zvt, post, z0t, hbt, n, b0, dv, lane, keep);
+        if (DVMAX <= 4) {
+            switch (dv) {
+                LDPC_TS_COL(1) LDPC_TS_COL(2) LDPC_TS_COL(3) LDPC_TS_COL(4)
+            default: ts_var_col_wide<PAIR, ES>(a, t, msgt, zvt, post, z0t, hbt, n, b0, dv, lane, keep);
+            }
+        } else {
+            switch (dv) {
+                LDPC_TS_COL(1) LDPC_TS_COL(2) LDPC_TS_COL(3) LDPC_TS_COL(4) LDPC_TS_COL(5) LDPC_TS_COL(6)
+                LDPC_TS_COL(7) LDPC_TS_COL(8)
+            default: ts_var_col_wide<PAIR, ES>(a, t, msgt, zvt, post, z0t, hbt, n, b0, dv, lane, keep);
+            }
         }
 #undef LDPC_TS_COL
     }

@@ -889,6 +889,7 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
         t.zv = (uint32_t *)(w + pl.off_zv);
         t.hb = (uint32_t *)(w + pl.off_hb);
         t.E = c->E;
+        t.max_dv = c->max_dv;
         e = twoscan_run(a, t, r, s, &n);
     } else {
         e = stream_run(a, r, s, &n);

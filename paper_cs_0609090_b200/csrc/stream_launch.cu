@@ -213,13 +213,13 @@ cudaError_t twoscan_run(const StreamArgs &a0, const TwoScanArgs &t, const Stream
         e = pair ? launch([&] { k_ts_check<true><<<gm, 256, 0, s>>>(a, t); }, nl)
                  : launch([&] { k_ts_check<false><<<gm, 256, 0, s>>>(a, t); }, nl);
         if (e != cudaSuccess) return e;
-        if (pair) {
-            if (es) e = launch([&] { k_ts_var<true, true><<<gn, 256, 0, s>>>(a, t, k); }, nl);
-            else e = launch([&] { k_ts_var<true, false><<<gn, 256, 0, s>>>(a, t, k); }, nl);
-        } else {
-            if (es) e = launch([&] { k_ts_var<false, true><<<gn, 256, 0, s>>>(a, t, k); }, nl);
-            else e = launch([&] { k_ts_var<false, false><<<gn, 256, 0, s>>>(a, t, k); }, nl);
-        }
+        const bool d4 = t.max_dv <= 4;
+#define LDPC_TS_VAR(P_, E_)                                                                      \
+    (d4 ? launch([&] { k_ts_var<P_, E_, 4><<<gn, 256, 0, s>>>(a, t, k); }, nl)                   \
+        : launch([&] { k_ts_var<P_, E_, 8><<<gn, 256, 0, s>>>(a, t, k); }, nl))
+        if (pair) e = es ? LDPC_TS_VAR(true, true) : LDPC_TS_VAR(true, false);
+        else e = es ? LDPC_TS_VAR(false, true) : LDPC_TS_VAR(false, false);
+#undef LDPC_TS_VAR
         if (e != cudaSuccess) return e;
         if (es && k < r.max_iter) {
             // syndrome of Z^(k) from the variable pass's hard-decision ballots

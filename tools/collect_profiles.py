@@ -16,6 +16,30 @@ MEAS = os.path.join(ROOT, "gpurun_out", "meas")
 PROF = os.path.join(ROOT, "profiles")
 
 
+def summarize_launches(csv_path, out_path, workload):
+    """Per-kernel totals of an ncu --csv launch list with time and DRAM byte metrics."""
+    import collections
+    import csv
+    rows = [r for r in csv.reader(open(csv_path)) if len(r) > 14 and r[0] != "ID"]
+    agg = collections.defaultdict(lambda: collections.defaultdict(float))
+    cnt = collections.Counter()
+    for r in rows:
+        k, m, v = r[4].split("(")[0], r[12], float(r[14].replace(",", ""))
+        agg[k][m] += v
+        cnt[k] += m == "gpu__time_duration.sum"
+    out = []
+    for k, d in agg.items():
+        t_us = d["gpu__time_duration.sum"] / 1e3
+        b = d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]
+        out.append({"kernel": k, "launches": cnt[k], "total_us": round(t_us, 1),
+                    "us_per_launch": round(t_us / max(cnt[k], 1), 1),
+                    "dram_MB_per_launch": round(b / max(cnt[k], 1) / 1e6, 1),
+                    "dram_GBs": round(b / (t_us * 1e-6) / 1e9, 1) if t_us else None})
+    out.sort(key=lambda x: -x["total_us"])
+    with open(out_path, "w") as f:
+        json.dump({"workload": workload, "kernels": out}, f, indent=1)
+
+
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
@@ -31,6 +55,13 @@ def main():
         shutil.copy(lc, os.path.join(PROF, f"{tag}_launches_bench_cfg2.csv"))
         subprocess.check_call([sys.executable, summ, "launches", lc, os.path.join(PROF, f"{tag}_launches_bench_cfg2.json")],
                               stdout=subprocess.DEVNULL)
+    ts = os.path.join(MEAS, "twoscan_cfg2.csv")
+    if os.path.exists(ts):
+        shutil.copy(ts, os.path.join(PROF, f"{tag}_twoscan_cfg2_launches.csv"))
+        summarize_launches(ts, os.path.join(PROF, f"{tag}_twoscan_cfg2_launches.json"),
+                           "cfg2 two-scan (LDPC_SCHED_TWOSCAN), 8192 frames, 15 iterations, early stop; ncu --metrics "
+                           "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
+                           "(cold-cache, serialised)")
     for c in (2, 4, 5):
         rep = os.path.join(MEAS, f"prof_cfg{c}.ncu-rep")
         if not os.path.exists(rep):

@@ -17,3 +17,8 @@ for c in 2 4 5; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K -s 1 -c 1 -o $OUT/prof_cfg$c \
     python tools/prof_decode.py --config $c --reps 2 > $OUT/ncu_cfg$c.log 2>&1; echo "ncu cfg$c rc=$?"
 done
+# two-scan baseline launch list (cfg2): per-kernel time and DRAM bytes
+timeout 300 python tools/prof_decode.py --config 2 --sched 1 --reps 1 > /dev/null 2>&1 && \
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 80 \
+  --csv --log-file $OUT/twoscan_cfg2.csv python tools/prof_decode.py --config 2 --sched 1 --reps 1 > /dev/null 2>&1
+echo "twoscan launches rc=$?"

@@ -175,7 +175,8 @@ ldpc_status ldpc_decode_workspace_size(const ldpc_code *code, int64_t n_frames,
  * order that can vary run to run (fp32 sums), see DESIGN.md §3 D11.
  * Kernel choice (automatic): codes whose posterior double buffer fits in shared memory
  * decode resident (one launch; integer: a frame pair per CTA, F32: a frame per CTA, row
- * degree <= 8); longer codes use the streaming kernels (one launch per iteration). */
+ * degree <= 8) when the compact state of a CTA's rows fits in the SM's Tensor Memory;
+ * other codes use the streaming kernels (one launch per iteration). */
 ldpc_status ldpc_decode_batch(const ldpc_code *code, const ldpc_decode_params *params, int64_t n_frames,
                               const void *llr, uint32_t *hard_bits, void *posteriors,
                               uint8_t *syndrome_ok, int32_t *iterations_used,

@@ -543,7 +543,7 @@ struct Plan {
     size_t smem = 0;
     int grid = 0;
     size_t slot_words = 0;
-    uint32_t tmem_cols = 0;
+    uint32_t tmem_cols = 0, tmem_cols_needed = 0;
     int cols_per_group = 0;
     // stream
     int tile = 64, ntiles = 0;
@@ -731,7 +731,24 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         const int groups = (pl.threads + 127) / 128;   // 128-thread TMEM lane slices
         uint32_t need = (uint32_t)(pl.cols_per_group * groups), cols = 32;
         while (cols < need) cols <<= 1;
-        if (cols > 512) return fail(LDPC_ERR_UNSUPPORTED, "compact state needs %u TMEM columns (> 512)", need);
+        pl.tmem_cols_needed = cols;
+        if (cols > 512) {
+            // more check rows per thread than an SM's 512 TMEM columns can hold state for:
+            // the streaming kernels (state in HBM) take the decode where they apply
+            if (pl.lay || pl.fmt == FMT_FULL)
+                return fail(LDPC_ERR_UNSUPPORTED, "%s needs %u TMEM columns (> 512)",
+                            pl.lay ? "layered schedule" : "full per-edge messages", need);
+            const bool f32 = p->llr_type == LDPC_LLR_F32;
+            if (!f32 && (int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
+                return fail(LDPC_ERR_UNSUPPORTED, "compact state needs %u TMEM columns (> 512) and the streaming "
+                                                  "kernels need 2*Q*(max_dv+1) < 16384", need);
+            pl.path = f32 ? PATH_STREAM_F : PATH_STREAM_I;
+            pl.kind = RES_BATCHED;
+            pl.tile = f32 ? 32 : 64;
+        }
+    }
+    if (pl.path == PATH_RESIDENT) {
+        const uint32_t cols = pl.tmem_cols_needed;
         pl.tmem_cols = cols;
         int blocks = 0;
         cudaError_t e = res_occupancy_any(c, p, pl, &blocks);
@@ -751,10 +768,11 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                                              (int64_t)blocks * c->sm_count * std::max(1, atoi(ge)));
         pl.slot_words = ((size_t)c->N + 63) & ~(size_t)63;
         if (getenv("LDPC_DEBUG"))
-            fprintf(stderr, "[ldpc] resident: threads=%d smem=%zu tmem_cols=%u need=%u occ_blocks=%d grid=%d batches=%d\n",
-                    pl.threads, pl.smem, cols, need, blocks, pl.grid, pl.nbatch);
+            fprintf(stderr, "[ldpc] resident: threads=%d smem=%zu tmem_cols=%u (%d per group) occ_blocks=%d grid=%d batches=%d\n",
+                    pl.threads, pl.smem, cols, pl.cols_per_group, blocks, pl.grid, pl.nbatch);
         pl.ws_bytes = align256((size_t)pl.grid * pl.slot_words * 4);
     } else {
+        // streaming layout (also the fallback of a resident plan that does not fit in TMEM)
         pl.ntiles = (int)((F + pl.tile - 1) / pl.tile);
         const size_t plane = (size_t)pl.ntiles * c->N * 32 * 4;
         const int sw = pl.path == PATH_STREAM_F ? 3 : (pl.fmt == FMT_C16 ? 3 : 2);

@@ -378,6 +378,31 @@ def test_resident_size_boundary():
             assert_int_parity(code, llr, params, 6, es, 1, 511)
 
 
+def test_tmem_capacity_falls_back_to_streaming():
+    """N = M = 24000 (4,4)-regular: the posteriors fit in shared memory but 94 rows per
+    thread need 564 TMEM columns of compact state (> 512), so the planner streams the
+    decode (int16 and fp32); the per-edge and layered forms, which need TMEM / the resident
+    kernel, are rejected."""
+    code = g.regular(24000, 4, 4, seed=3, remove_4cycles=False)
+    s2 = g.ebn0_to_sigma2(4.0, 0.5)
+    llr = g.llr(8, 0, 3, code.n_vars, s2, g.LLR_I16, 3, 511)
+    params = P.make_params(5, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+    assert_int_parity(code, llr, params, 5, 1, 1, 511)
+    assert P.ldpc_last_launch_count() > 1                       # streamed
+    z = g.llr(9, 0, 3, code.n_vars, s2, g.LLR_F32)
+    pf = P.make_params(5, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+    post, hb, ok, it = gpu_decode(code, z, pf)
+    assert P.ldpc_last_launch_count() > 1
+    ref = oracle.decode(code, z, "compact", "f32", 5, 0, alpha=0.75, nthreads=NT)
+    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    dec = decoder(code)
+    for fmt, sched in ((P.LDPC_MSG_FULL, P.LDPC_SCHED_SINGLESCAN), (P.LDPC_MSG_COMPACT, P.LDPC_SCHED_LAYERED)):
+        bad = P.make_params(5, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, fmt, sched)
+        with pytest.raises(P.LdpcError) as e:
+            dec.workspace(3, bad)
+        assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+
+
 def test_high_column_degree_batched_kernel():
     """Column degree 20 at Q = 511: 2Q(dv+1) >= 0x4000, so the (unbiased) batched resident
     kernel runs; the streaming integer path rejects it (biased lanes would overflow)."""

@@ -7,7 +7,7 @@
 // own rows back to back.
 //
 // Exactness of a 32-bit add on two 16-bit lanes: every posterior word holds
-// 2 Z_n + 0x4000 in each lane (BIAS).  |2 Z_n| <= 2 Q (dv + 1) < 0x4000 (checked by the
+// 2 Z_n + 0x3FFF in each lane (kAtomBias).  |2 Z_n| <= 2 Q (dv + 1) < 0x4000 (checked by the
 // planner), and so does every partial sum in any order, so both lanes stay in
 // [0, 0x8000): non-negative lanes never carry or borrow across the lane boundary.  The
 // message is added in "V form" (hi * 65536 + lo as a signed 32-bit integer), which is
@@ -24,7 +24,23 @@
 
 namespace ldpc {
 
-constexpr int kAtomBias = 0x4000;
+// Posterior words hold 2Z + 0x3FFF per lane.  With |2Z| <= 2Q(dv+1) < 0x4000 (planner) every
+// lane stays in [1, 0x7FFF] and the hard decision [Z <= 0] is the complement of bit 14, so
+// a row's syndrome bit is an XOR of its gathered words (no per-edge subtraction).  Being
+// odd, the words never equal 0x4000, which keeps the subtract-based final-pass parity
+// (cpar = -0x40004000, rowcore.cuh row_parity) exact despite the lane borrow.
+constexpr int kAtomBias = 0x3FFF;
+constexpr uint32_t kAtomQ0 = 0x40014001u;    // (0x8000 - bias) per lane: q + 0x8000 = word + Q0 - 2 L_old
+
+// Hard-decision parity of a row from its biased words: bit 15 / 31 set iff odd.
+template <int DC>
+__device__ __forceinline__ uint32_t atom_row_parity(const uint32_t (&L)[DC]) {
+    uint32_t x = L[0];
+#pragma unroll
+    for (int j = 1; j < DC; ++j) x ^= L[j];
+    x = (x << 1) & 0x80008000u;                         // XOR of bit 14 -> bit 15 (and 30 -> 31)
+    return (DC & 1) ? (x ^ 0x80008000u) : x;            // [Z <= 0] = NOT bit 14
+}
 
 template <int DC, bool QC, bool ES>
 __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba, int e0,
@@ -43,13 +59,13 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
     uint32_t L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
-    if (ES) synd |= row_parity<DC>(L, a.rk, a.cpar);
+    if (ES) synd |= atom_row_parity<DC>(L);
     uint32_t q[DC];                                                      // q_mn + 0x8000 per lane
     if (first_iter) {
 #pragma unroll
-        for (int j = 0; j < DC; ++j) q[j] = fadd32(L[j], 0x40004000u, a.rk);   // L^(0)_mn = 0
+        for (int j = 0; j < DC; ++j) q[j] = fadd32(L[j], kAtomQ0, a.rk);    // L^(0)_mn = 0
     } else {
-        rebuild_q_b8<DC>(L, st, q, a.rk);                                  // Z_n - L^(k-1)_mn
+        rebuild_q_b8<DC, kAtomQ0>(L, st, q, a.rk);                         // Z_n - L^(k-1)_mn
     }
     uint32_t rn[DC];                                                     // V(L^(k)_mn) + 0x8000
     new_state<DC, true>(q, vk, st, rn, a.rk);
@@ -60,9 +76,9 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
 
 // ---------------------------------------------------------------- FMT_FULL (§4)
 // The single-scan of PAPER.md §4 keeps every check message L_mn: here one
-// TMEM word per edge per frame pair, stored as c = 0x40004000 - V(L) (= 0x4000C000 minus the
-// RED value V(L) + 0x8000), so the next iteration's q_mn + 0x8000 per lane = (2Z_n + 0x4000)
-// + c is one IMAD (no rebuild from a compact state).  Same messages, posteriors and stopping as the compact form.
+// TMEM word per edge per frame pair, stored as c = kAtomQ0 - V(L) (= kAtomQ0 + 0x8000 minus
+// the RED value V(L) + 0x8000), so the next iteration's q_mn + 0x8000 per lane =
+// (2Z_n + 0x3FFF) + c is one IMAD (no rebuild from a compact state).  Same messages, posteriors and stopping as the compact form.
 template <int DC>
 __device__ __forceinline__ void full_tmem_load(uint32_t taddr, uint32_t (&c)[8]) {
     if constexpr (DC == 8) {
@@ -109,17 +125,17 @@ __device__ __forceinline__ void atom_row_full(const ResArgs &a, const QcTab &t, 
     uint32_t L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
-    if (ES) synd |= row_parity<DC>(L, a.rk, a.cpar);
+    if (ES) synd |= atom_row_parity<DC>(L);
     uint32_t q[DC];                                                      // q_mn + 0x8000 per lane
 #pragma unroll
-    for (int j = 0; j < DC; ++j) q[j] = fadd32(L[j], first_iter ? 0x40004000u : c[j], a.rk);   // Z - L_old
+    for (int j = 0; j < DC; ++j) q[j] = fadd32(L[j], first_iter ? kAtomQ0 : c[j], a.rk);   // Z - L_old
     uint32_t rn[DC];
     RowState st;                                                         // unused: no compact state
     new_state<DC, true>(q, vk, st, rn, a.rk);                           // Eq.(3)
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");   // Z += L
-        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c[j]) : "r"(rn[j]), "r"(a.rk.m1), "r"(0x4000C000u));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c[j]) : "r"(rn[j]), "r"(a.rk.m1), "r"(kAtomQ0 + 0x8000u));
     }
 }
 
@@ -146,12 +162,12 @@ __device__ __forceinline__ void atom_row_full_x2(const ResArgs &a, const QcTab &
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L0[j]) : "r"(d0[j] + bp));
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L1[j]) : "r"(d1[j] + bp));
     }
-    if (ES) synd |= row_parity<DC>(L0, a.rk, a.cpar) | row_parity<DC>(L1, a.rk, a.cpar);
+    if (ES) synd |= atom_row_parity<DC>(L0) | atom_row_parity<DC>(L1);
     uint32_t q0[DC], q1[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        q0[j] = fadd32(L0[j], first_iter ? 0x40004000u : c0[j], a.rk);
-        q1[j] = fadd32(L1[j], first_iter ? 0x40004000u : c1[j], a.rk);
+        q0[j] = fadd32(L0[j], first_iter ? kAtomQ0 : c0[j], a.rk);
+        q1[j] = fadd32(L1[j], first_iter ? kAtomQ0 : c1[j], a.rk);
     }
     uint32_t rn0[DC], rn1[DC];
     RowState st;
@@ -161,8 +177,8 @@ __device__ __forceinline__ void atom_row_full_x2(const ResArgs &a, const QcTab &
     for (int j = 0; j < DC; ++j) {
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d0[j] + ba), "r"(rn0[j]) : "memory");
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d1[j] + ba), "r"(rn1[j]) : "memory");
-        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c0[j]) : "r"(rn0[j]), "r"(a.rk.m1), "r"(0x4000C000u));
-        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c1[j]) : "r"(rn1[j]), "r"(a.rk.m1), "r"(0x4000C000u));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c0[j]) : "r"(rn0[j]), "r"(a.rk.m1), "r"(kAtomQ0 + 0x8000u));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(c1[j]) : "r"(rn1[j]), "r"(a.rk.m1), "r"(kAtomQ0 + 0x8000u));
     }
 }
 

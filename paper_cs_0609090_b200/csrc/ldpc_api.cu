@@ -823,7 +823,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.bptr = pl.lay ? c->d_bptr_lay : c->d_bptr;
     a.colT = natural ? c->d_colT_lay : c->d_colT;
     a.dcT = natural ? c->d_dcT_lay : c->d_dcT;
-    a.cpar = pl.kind == RES_ATOM ? 0xBFFEBFFFu : 0xFFFEFFFFu;
+    a.cpar = pl.kind == RES_ATOM ? 0xBFFFC000u : 0xFFFEFFFFu;   // -(bias + 1) per lane (atom: bias 0x3FFF)
     a.alpha = pl.alpha;
     a.beta = pl.betaf;
     if (pl.kind == RES_F32 && !pl.alphas.empty()) {

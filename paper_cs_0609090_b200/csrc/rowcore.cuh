@@ -64,14 +64,16 @@ __device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowStat
 // B8 rebuild for the barrier-free resident kernel: L holds 2Z + 0x4000 per lane; the four
 // candidates 0x4000 -/+ A, B are formed by IMAD (lanes stay non-negative, no carries) and
 // q + 0x8000 = L + candidate is one 32-bit IMAD per edge (FMA pipe).
-template <int DC>
+// Q0 = (0x8000 - bias) per lane: 0x40004000 for words biased by 0x4000 (streaming kernels),
+// 0x40014001 for words biased by 0x3FFF (barrier-free resident kernel, k_resident_atom.cuh).
+template <int DC, uint32_t Q0 = 0x40004000u>
 __device__ __forceinline__ void rebuild_q_b8(const uint32_t (&L)[DC], const RowState &st, uint32_t (&q)[DC],
                                              const RegK &k) {
-    uint32_t A, B, nA, nB;                                      // -L_old + 0x4000 for L_old = +A, +B, -A, -B
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(A) : "r"(st.A), "r"(k.m1), "r"(0x40004000u));
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(B) : "r"(st.B), "r"(k.m1), "r"(0x40004000u));
-    nA = fadd32(st.A, 0x40004000u, k);
-    nB = fadd32(st.B, 0x40004000u, k);
+    uint32_t A, B, nA, nB;                                      // -L_old + Q0 for L_old = +A, +B, -A, -B
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(A) : "r"(st.A), "r"(k.m1), "r"(Q0));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(B) : "r"(st.B), "r"(k.m1), "r"(Q0));
+    nA = fadd32(st.A, Q0, k);
+    nB = fadd32(st.B, Q0, k);
 #pragma unroll
     for (int i = 0; i < (DC + 1) / 2; ++i) {
         const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte

@@ -115,9 +115,10 @@ enum { LDPC_MSG_COMPACT = 0, LDPC_MSG_1BIT = 1,
  *               before it (layered / Gauss-Seidel schedule, reading D25).  Not
  *               equivalent to two-scan; usually converges in fewer iterations.  The row
  *               order of H defines the schedule (QC codes: base row by base row).
- *               Requires the resident kernel (a frame pair's N posteriors in shared
- *               memory, e.g. N <= ~27000) and at most 256 consecutive variable-disjoint
- *               rows per batch, else LDPC_ERR_UNSUPPORTED. */
+ *               Requires the resident kernel (a frame's N posteriors in shared
+ *               memory, e.g. N <= ~27000), row degree <= 8 and at most 256 consecutive
+ *               variable-disjoint rows per batch, else LDPC_ERR_UNSUPPORTED.  Integer and
+ *               F32 LLRs (F32 layered is bit-exact with a sequential implementation). */
 enum { LDPC_SCHED_SINGLESCAN = 0, LDPC_SCHED_TWOSCAN = 1, LDPC_SCHED_LAYERED = 2 };
 
 typedef struct {

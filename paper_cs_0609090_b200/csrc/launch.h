@@ -9,8 +9,9 @@ namespace ldpc {
 // Resident kernels.  i8 selects int8 channel LLRs (else int16).  kind: RES_BATCHED
 // (k_resident.cuh, flooding in conflict-free batches), RES_LAYERED (k_resident.cuh,
 // in-place schedule), RES_ATOM (k_resident_atom.cuh, flooding with shared atomics),
-// RES_F32 (k_resident_f32.cuh, fp32 LLRs, one frame per CTA).
-enum { RES_BATCHED = 0, RES_LAYERED = 1, RES_ATOM = 2, RES_F32 = 3 };
+// RES_F32 (k_resident_f32.cuh, fp32 LLRs, one frame per CTA), RES_F32_LAY (the same with the
+// layered schedule).
+enum { RES_BATCHED = 0, RES_LAYERED = 1, RES_ATOM = 2, RES_F32 = 3, RES_F32_LAY = 4 };
 cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,
                           int threads, int *blocks);
 cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,

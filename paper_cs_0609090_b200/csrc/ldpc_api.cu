@@ -613,8 +613,6 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (p->llr_type == LDPC_LLR_F32) {
         if (p->msg_format != LDPC_MSG_COMPACT)
             return fail(LDPC_ERR_UNSUPPORTED, "1-bit and full per-edge message formats need integer LLRs");
-        if (pl.sched == LDPC_SCHED_LAYERED)
-            return fail(LDPC_ERR_UNSUPPORTED, "layered schedule is implemented for integer LLRs only");
         if (c->max_dc > 16) return fail(LDPC_ERR_UNSUPPORTED, "F32 path supports row degree <= 16 (max %d)", c->max_dc);
         if (p->variant == LDPC_MINSUM_OFFSET && !(p->offset_f >= 0.f))
             return fail(LDPC_ERR_INVALID_ARG, "offset_f must be >= 0");
@@ -636,6 +634,18 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                           !(force && force[0] == '1') && (pl.alphas.empty() || p->max_iter <= kMaxSched);
         pl.path = fres ? PATH_RESIDENT : PATH_STREAM_F;
         if (fres) pl.kind = RES_F32;
+        if (pl.sched == LDPC_SCHED_LAYERED) {
+            // layered schedule (D25): resident only (k_resident_f32_lay, one posterior array)
+            if (!c->res_ok || c->max_dc > kMaxDC)
+                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule needs a code whose posteriors fit in shared memory "
+                                                  "(the resident kernel) and row degree <= %d", kMaxDC);
+            if (c->res_threads_lay > 256) return fail(LDPC_ERR_UNSUPPORTED, "layered batches wider than 256 rows");
+            if (!pl.alphas.empty() && p->max_iter > kMaxSched)
+                return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
+            pl.path = PATH_RESIDENT;
+            pl.lay = true;
+            pl.kind = RES_F32_LAY;
+        }
         pl.tile = 32;
     } else if (p->llr_type == LDPC_LLR_I16 || p->llr_type == LDPC_LLR_I8) {
         if (p->offset_raw < 0 || p->offset_raw > 16383) return fail(LDPC_ERR_INVALID_ARG, "offset_raw out of range");
@@ -694,7 +704,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     } else {
         return fail(LDPC_ERR_INVALID_ARG, "bad llr_type %d", p->llr_type);
     }
-    const int64_t npairs = pl.kind == RES_F32 ? F : (F + 1) / 2;   // CTA work units: frame pairs (fp32: frames)
+    const bool f32res = pl.kind == RES_F32 || pl.kind == RES_F32_LAY;
+    const int64_t npairs = f32res ? F : (F + 1) / 2;   // CTA work units: frame pairs (fp32: frames)
     if (pl.path == PATH_RESIDENT && !pl.vks.empty() && p->max_iter > kMaxSched) {
         if (pl.lay) return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
         pl.path = PATH_STREAM_I;                         // the streaming kernels take any schedule length
@@ -708,8 +719,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         // selects the batched kernel
         const char *be = getenv("LDPC_RES_BATCHED");
         const bool atom_ok = (int64_t)2 * pl.Q * (c->max_dv + 1) < 0x4000 && c->nbatch_atom > 0;
-        if (pl.kind != RES_F32)
-            pl.kind = pl.lay ? RES_LAYERED : ((atom_ok && !(be && be[0] == '1')) ? RES_ATOM : RES_BATCHED);
+        if (!f32res) pl.kind = pl.lay ? RES_LAYERED : ((atom_ok && !(be && be[0] == '1')) ? RES_ATOM : RES_BATCHED);
         if (pl.fmt == FMT_FULL && pl.kind != RES_ATOM)
             return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages (LDPC_MSG_FULL) need the barrier-free resident "
                                               "kernel: SINGLESCAN schedule and 2*Q*(max_dv+1) < 16384");
@@ -826,7 +836,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.cpar = pl.kind == RES_ATOM ? 0xBFFFC000u : 0xFFFEFFFFu;   // -(bias + 1) per lane (atom: bias 0x3FFF)
     a.alpha = pl.alpha;
     a.beta = pl.betaf;
-    if (pl.kind == RES_F32 && !pl.alphas.empty()) {
+    if ((pl.kind == RES_F32 || pl.kind == RES_F32_LAY) && !pl.alphas.empty()) {
         a.nsched = (int)pl.alphas.size();
         for (size_t k = 0; k < pl.alphas.size(); ++k) {
             a.alpha_sched[k] = pl.alphas[k];
@@ -840,7 +850,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.cols_per_group = pl.cols_per_group;
     a.rk = make_regk();
     static const QcTab empty_tab{};
-    const QcTab *qt = pl.kind == RES_LAYERED ? c->qtab_lay
+    const QcTab *qt = (pl.kind == RES_LAYERED || pl.kind == RES_F32_LAY) ? c->qtab_lay
                                              : ((pl.kind == RES_ATOM || pl.kind == RES_F32) ? c->qtab_atom : c->qtab);
     cudaError_t e = res_launch(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.kind, pl.grid,
                                pl.threads, pl.smem, a, qt ? *qt : empty_tab, s);

@@ -12,7 +12,8 @@ namespace {
 template <bool QC, bool ES, int FMT, typename TIN, int KIND>
 struct Kern {
     static auto get() {
-        if constexpr (KIND == 3) return k_resident_f32<QC, ES>;
+        if constexpr (KIND == 4) return k_resident_f32_lay<QC, ES>;
+        else if constexpr (KIND == 3) return k_resident_f32<QC, ES>;
         else if constexpr (KIND == 2) return k_resident_atom<QC, ES, FMT, TIN>;
         else return k_resident<QC, ES, FMT, TIN, KIND == 1>;
     }
@@ -65,9 +66,10 @@ cudaError_t dispatch(bool qc, bool es, int fmt, bool i8, int kind, Args... args)
         return i8 ? K<Q, E, FMT_FULL, int8_t, 2>::run(args...) : K<Q, E, FMT_FULL, int16_t, 2>::run(args...);
     LDPC_RES_FULL(true, true) LDPC_RES_FULL(true, false) LDPC_RES_FULL(false, true) LDPC_RES_FULL(false, false)
 #undef LDPC_RES_FULL
-    // fp32 LLRs: one frame per CTA (k_resident_f32.cuh)
+    // fp32 LLRs: one frame per CTA (k_resident_f32.cuh; kind 4: layered schedule)
 #define LDPC_RES_F32(Q, E) \
-    if (qc == Q && es == E && kind == 3) return K<Q, E, FMT_C16, float, 3>::run(args...);
+    if (qc == Q && es == E && kind == 3) return K<Q, E, FMT_C16, float, 3>::run(args...); \
+    if (qc == Q && es == E && kind == 4) return K<Q, E, FMT_C16, float, 4>::run(args...);
     LDPC_RES_F32(true, true) LDPC_RES_F32(true, false) LDPC_RES_F32(false, true) LDPC_RES_F32(false, false)
 #undef LDPC_RES_F32
 #undef LDPC_RES_CASE

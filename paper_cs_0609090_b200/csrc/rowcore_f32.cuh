@@ -11,11 +11,12 @@ namespace ldpc {
 // State word W: bit j = sign of L_mn (1 = negative), bit 16 + ñ set (one-hot position).
 // Selections work on the IEEE bit patterns: |L| = A or B is A + [j == ñ] (B - A) as a
 // 32-bit integer (exact; IMAD on the FMA pipe), the sign is an XOR of bit 31.
+// f32_row_q also returns q_mn = Z_n - L^(k-1)_mn (the layered update writes q + L^(k)_mn).
 template <int DC>
-__device__ __forceinline__ void f32_row(const float (&L)[DC], bool first_iter, float A0, float B0, uint32_t W0,
-                                        float alpha, float beta, float &A, float &B, uint32_t &Wn, float (&r)[DC]) {
+__device__ __forceinline__ void f32_row_q(const float (&L)[DC], bool first_iter, float A0, float B0, uint32_t W0,
+                                          float alpha, float beta, float &A, float &B, uint32_t &Wn, float (&r)[DC],
+                                          float (&q)[DC]) {
     static_assert(DC <= 16, "one-hot position bits 16..31");
-    float q[DC];
     if (first_iter) {
 #pragma unroll
         for (int j = 0; j < DC; ++j) q[j] = L[j];                    // L^(0)_mn = 0
@@ -53,6 +54,13 @@ __device__ __forceinline__ void f32_row(const float (&L)[DC], bool first_iter, f
         const uint32_t mag = isel * db1 + a1;
         r[j] = __uint_as_float(mag ^ ((sg << (31 - j)) & 0x80000000u));
     }
+}
+
+template <int DC>
+__device__ __forceinline__ void f32_row(const float (&L)[DC], bool first_iter, float A0, float B0, uint32_t W0,
+                                        float alpha, float beta, float &A, float &B, uint32_t &Wn, float (&r)[DC]) {
+    float q[DC];
+    f32_row_q<DC>(L, first_iter, A0, B0, W0, alpha, beta, A, B, Wn, r, q);
 }
 
 }  // namespace ldpc

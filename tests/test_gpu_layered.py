@@ -1,6 +1,7 @@
 """GPU layered schedule (LDPC_SCHED_LAYERED, reading D25) against the
 CPU oracle's layered engine: bit-exact posteriors, hard bits, syndrome flags and
-iteration counts (integer LLRs, compact and 1-bit formats, early stop on and off)."""
+iteration counts (integer LLRs, compact and 1-bit formats, early stop on and off; fp32
+LLRs, where the in-place schedule makes the order of operations the oracle's)."""
 import numpy as np
 import pytest
 
@@ -72,10 +73,47 @@ def test_layered_unsupported_for_streaming_sizes():
     assert e.value.status == P.LDPC_ERR_UNSUPPORTED
 
 
-def test_layered_f32_unsupported():
-    code = g.CONFIGS[1].code()
-    dec = decoder(code)
-    params = P.make_params(5, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY)
+def assert_lay_f32(code, llr, params, K, es, alpha=1.0, beta=0.0, **kw):
+    """fp32 layered: every variable is updated by one row at a time in ascending m with the
+    oracle's operations (D11: one rounding each), so the GPU is bit-exact with the oracle."""
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    assert P.ldpc_last_launch_count() == 1                      # resident layered kernel
+    ref = oracle.decode(code, llr, "layered", "f32", K, es, beta=beta, alpha=alpha, nthreads=NT, **kw)
+    np.testing.assert_array_equal(it, ref.iters)
+    np.testing.assert_array_equal(ok, ref.ok)
+    np.testing.assert_array_equal(post.view(np.uint32), ref.post.astype(np.float32).view(np.uint32))
+    np.testing.assert_array_equal(hb, oracle.pack_bits((ref.post <= 0).astype(np.uint8)))
+
+
+@pytest.mark.parametrize("code", small_codes(), ids=lambda c: c.name)
+def test_layered_f32_small_codes(code):
+    if int(np.max(np.diff(code.row_ptr))) > 8:
+        pytest.skip("resident kernels: row degree <= 8")
+    for F in (1, 33, 130):
+        for ebn0 in (1.0, 3.0):
+            llr = g.llr(500 + F, 0, F, code.n_vars, g.ebn0_to_sigma2(ebn0, max(code.rate, 0.3)), g.LLR_F32)
+            for variant, alpha, beta, es, K in ((P.LDPC_MINSUM_NORMALIZED, 0.75, 0.0, 0, 10),
+                                                (P.LDPC_MINSUM_OFFSET, 1.0, 0.25, 1, 12),
+                                                (P.LDPC_MINSUM_NORMALIZED, 0.8125, 0.0, 1, 25)):
+                params = P.make_params(K, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY)
+                assert_lay_f32(code, llr, params, K, es, alpha, beta)
+
+
+@pytest.mark.parametrize("es", [0, 1])
+def test_layered_f32_cfg2_code(es):
+    code = g.CONFIGS[2].code()
+    llr = g.llr(61 + es, 0, 64, code.n_vars, g.ebn0_to_sigma2(2.0, code.rate), g.LLR_F32)
+    params = P.make_params(15, es, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY)
+    assert_lay_f32(code, llr, params, 15, es, 0.75)
+    al = np.linspace(0.6, 0.95, 15).astype(np.float32)                 # lambda_k per iteration (P:179)
+    params = P.make_params(15, es, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY,
+                           alpha_per_iter=al)
+    assert_lay_f32(code, llr, params, 15, es, 0.75, alpha_sched=al.astype(np.float64))
+
+
+def test_layered_f32_unsupported_for_streaming_sizes():
+    cfg = g.CONFIGS[5]
+    dec = decoder(cfg.code())
     with pytest.raises(P.LdpcError) as e:
-        dec.workspace(8, params)
+        dec.workspace(64, P.params_for_config(cfg, LAY))
     assert e.value.status == P.LDPC_ERR_UNSUPPORTED

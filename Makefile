@@ -11,7 +11,7 @@ SRCS := $(wildcard $(CSRC)/*.cu)
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/ldpc.h
 
-all: $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so
+all: $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so examples/decode_c
 
 build/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
@@ -25,8 +25,14 @@ oracle/liboracle.so: oracle/oracle.c oracle/engine.inc
 ldpcgen/libldpcgen.so: ldpcgen/ldpcgen.c
 	gcc -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -o $@ ldpcgen/ldpcgen.c -lm -lpthread
 
+# plain-C consumer of the C ABI (examples/decode_c.c)
+CUDA_HOME ?= /usr/local/cuda
+examples/decode_c: examples/decode_c.c include/ldpc.h $(LIB)
+	gcc -O2 -std=c11 -Wall -Iinclude -I$(CUDA_HOME)/include -o $@ $< -Lpaper_cs_0609090_b200 -lldpc \
+	  -L$(CUDA_HOME)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../paper_cs_0609090_b200' -Wl,-rpath,$(CUDA_HOME)/lib64
+
 clean:
-	rm -f build/*.o $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so
+	rm -f build/*.o $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so examples/decode_c
 
 .PHONY: all clean
 $(shell mkdir -p build)

@@ -469,3 +469,15 @@ def test_concurrent_host_api_calls_on_one_code():
         np.testing.assert_array_equal(hb, oracle.pack_bits(ref.bits))
         np.testing.assert_array_equal(ok, ref.ok)
         np.testing.assert_array_equal(it, ref.iters)
+
+
+def test_plain_c_consumer():
+    """examples/decode_c.c: the C ABI used from plain C (no Python, no PyTorch) -- code
+    creation from a QC shift table, both decode entry points, error counters."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "decode_c")
+    if not os.path.exists(exe):
+        pytest.skip("examples/decode_c not built (make examples/decode_c)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout

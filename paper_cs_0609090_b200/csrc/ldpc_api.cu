@@ -560,6 +560,8 @@ bool make_vark(double lambda, int beta, int Q, VarK &v) {
         v.norm = 0;
         v.nbeta2p1 = pack2(1 - 2 * beta, 1 - 2 * beta);
         v.q2p1 = pack2(2 * Q + 1, 2 * Q + 1);
+        v.nb8 = pack2(0x8000 - 2 * beta, 0x8000 - 2 * beta);
+        v.q2 = pack2(2 * Q, 2 * Q);
         return true;
     }
     for (int ns = 0; ns <= 8; ++ns) {

@@ -128,7 +128,7 @@ __device__ __forceinline__ void two_min(const uint32_t (&v)[DC], uint32_t &m1, u
     m2 = a2[0];
 }
 
-// doubled magnitude of the variant from m~ = 2|q| - [q < 0] (B8: m = m~ + 0x8000 per lane)
+// doubled magnitude of the variant from m~ = 2|q| - [q < 0] (B8: m = 2|q| + 0x8000 per lane, exact)
 // Normalized path out of line: a call cannot be if-converted, so the offset path (every
 // BASELINE integer config) does not execute the normalized instructions speculatively.
 static __device__ __noinline__ uint32_t variant_mag_norm(uint32_t m, uint32_t na, uint32_t ns, uint32_t nmask, uint32_t nb2,
@@ -140,7 +140,13 @@ static __device__ __noinline__ uint32_t variant_mag_norm(uint32_t m, uint32_t na
 
 template <bool B8 = false>
 __device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const RegK &k) {
-    if (B8) m ^= 0x80008000u;                                     // unbias (the DPX add must not wrap)
+    if (B8) {
+        // m = 0x8000 + 2|q| exactly (new_state<B8>); as a signed half that is 2|q| - 0x8000, so
+        // relu(min(2|q| - 2 beta, 2Q)) is one VIADDMNMX with the unbias folded into the added
+        // constant 0x8000 - 2 beta (16-bit wrap-around add)
+        if (__builtin_expect(v.norm != 0, 0)) return variant_mag_norm(m ^ 0x80008000u, v.na, v.ns, v.nmask, v.nb2, v.q2);
+        return vaddmin_relu(m, v.nb8, v.q2);
+    }
     if (__builtin_expect(v.norm != 0, 0)) return variant_mag_norm(m, v.na, v.ns, v.nmask, v.nb2, v.q2);
     // relu(min(m~ + 1 - 2 beta, 2Q + 1)) with the low bit cleared is exact (m~ in {2|q|-1, 2|q|})
     return vaddmin_relu(m, v.nbeta2p1, v.q2p1) & 0xFFFEFFFEu;
@@ -162,8 +168,8 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
                                           const RegK &k) {
     uint32_t mt[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j)                                 // 2|q| - [q<0]  (B8: + 0x8000)
-        mt[j] = B8 ? __vmaxu2(q[j], fnot(q[j], k)) : vmax(q[j], fnot(q[j], k));
+    for (int j = 0; j < DC; ++j)                                 // 2|q| - [q<0]  (B8: 2|q| + 0x8000, exact)
+        mt[j] = B8 ? __vmaxu2(q[j], negb(q[j], k)) : vmax(q[j], fnot(q[j], k));
     uint32_t m1, m2;
     two_min<DC, B8>(mt, m1, m2);
     uint32_t par = q[0];

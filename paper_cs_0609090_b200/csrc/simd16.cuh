@@ -43,6 +43,13 @@ __device__ __forceinline__ uint32_t vform(uint32_t p, const RegK &k) {
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(p & 0x8000u), "r"(k.m2), "r"(p));
     return d;
 }
+// 0x10000 - a per half for halves in (0, 0x10000): one IMAD (the 0x8000-biased negation:
+// (q + 0x8000) -> (-q + 0x8000))
+__device__ __forceinline__ uint32_t negb(uint32_t a, const RegK &k) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(k.m1), "r"(0x00010000u));
+    return d;
+}
 // -a per half (IMAD NOT + VIADD)
 __device__ __forceinline__ uint32_t vneg(uint32_t a, const RegK &k) { return __vadd2(fnot(a, k), 0x00010001u); }
 // min(a + b, c) per half, then max(., 0)   (VIADDMNMX.S16x2.RELU)

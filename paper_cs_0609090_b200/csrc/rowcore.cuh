@@ -181,12 +181,17 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
     const uint32_t Pm = signmask(par);                          // product of all signs < 0
     const uint32_t A = variant_mag<B8>(m1, vk, k);
     const uint32_t B = variant_mag<B8>(m2, vk, k);
-    uint32_t nA = vneg(A, k), nB = vneg(B, k), Ac = A, Bc = B;
-    if (B8) {                                                    // message candidates ^ 0x8000 (low lane)
-        nA = __vadd2(fnot(A, k), 0x00018001u);
-        nB = __vadd2(fnot(B, k), 0x00018001u);
+    uint32_t nA, nB, Ac = A, Bc = B;
+    if (B8) {
+        // message candidates V(+-A) + 0x8000 (the RED operand): V is linear and the lanes of
+        // A are in [0, 2Q], so V(-A) + 0x8000 = 0x8000 - A is one IMAD (no lane borrow)
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(nA) : "r"(A), "r"(k.m1), "r"(0x00008000u));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(nB) : "r"(B), "r"(k.m1), "r"(0x00008000u));
         Ac = fadd32(A, 0x00008000u, k);
         Bc = fadd32(B, 0x00008000u, k);
+    } else {
+        nA = vneg(A, k);
+        nB = vneg(B, k);
     }
     // message for an edge whose own q is >= 0 carries the sign of the full product
     const uint32_t Apos = sel(Pm, nA, Ac), Aneg = sel(Pm, Ac, nA);

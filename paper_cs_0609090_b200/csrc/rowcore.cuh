@@ -69,22 +69,24 @@ __device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowStat
 template <int DC, uint32_t Q0 = 0x40004000u>
 __device__ __forceinline__ void rebuild_q_b8(const uint32_t (&L)[DC], const RowState &st, uint32_t (&q)[DC],
                                              const RegK &k) {
-    uint32_t A, B, nA, nB;                                      // -L_old + Q0 for L_old = +A, +B, -A, -B
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(A) : "r"(st.A), "r"(k.m1), "r"(Q0));
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(B) : "r"(st.B), "r"(k.m1), "r"(Q0));
-    nA = fadd32(st.A, Q0, k);
-    nB = fadd32(st.B, Q0, k);
+    // -L_old + Q0 is Q0 + mag for a negative L_old and Q0 - mag for a positive one; per lane
+    // the two sum to 2 Q0 (< 0x10000, no carries), so once the magnitude is selected by the
+    // argmin mask the other sign is one IMAD: 2 Q0 - (Q0 + mag)
+    const uint32_t nA = fadd32(st.A, Q0, k), nB = fadd32(st.B, Q0, k);
 #pragma unroll
     for (int i = 0; i < (DC + 1) / 2; ++i) {
         const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte
         const uint32_t wo = st.W << (3 - i);       // idx bits of pair i -> bit 7 of each byte
-        {
-            const uint32_t sm = prmt(ws, 0u, 0xAA88u), ix = prmt(wo, 0u, 0xAA88u);
-            q[2 * i] = fadd32(L[2 * i], sel(sm, sel(ix, nB, nA), sel(ix, B, A)), k);
-        }
-        if (2 * i + 1 < DC) {
-            const uint32_t sm = prmt(ws, 0u, 0xBB99u), ix = prmt(wo, 0u, 0xBB99u);
-            q[2 * i + 1] = fadd32(L[2 * i + 1], sel(sm, sel(ix, nB, nA), sel(ix, B, A)), k);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = 2 * i + h;
+            if (j >= DC) break;
+            const uint32_t s8 = h ? 0xBB99u : 0xAA88u;
+            const uint32_t sm = prmt(ws, 0u, s8), ix = prmt(wo, 0u, s8);
+            const uint32_t neg = sel(ix, nB, nA);                               // Q0 + mag
+            uint32_t pos;                                                       // Q0 - mag
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(pos) : "r"(neg), "r"(k.m1), "r"(Q0 + Q0));
+            q[j] = fadd32(L[j], sel(sm, neg, pos), k);
         }
     }
 }
@@ -194,16 +196,28 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
         nB = vneg(B, k);
     }
     // message for an edge whose own q is >= 0 carries the sign of the full product
-    const uint32_t Apos = sel(Pm, nA, Ac), Aneg = sel(Pm, Ac, nA);
-    const uint32_t Bpos = sel(Pm, nB, Bc), Bneg = sel(Pm, Bc, nB);
+    const uint32_t Apos = sel(Pm, nA, Ac), Bpos = sel(Pm, nB, Bc);
+    uint32_t Aneg = 0, Bneg = 0;
+    if (!B8) {
+        Aneg = sel(Pm, Ac, nA);
+        Bneg = sel(Pm, Bc, nB);
+    }
     const uint32_t cm1 = fnot(m1, k);                           // -m1 - 1
     uint32_t W = 0, sqp = 0, ixp = 0;
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         const uint32_t ix = vaddmin(mt[j], cm1, k.zero);          // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
         const uint32_t sq = signmask(q[j]);                     // 0xFFFF: q < 0  (B8: q >= 0)
-        if (B8) r[j] = sel(sq, sel(ix, Bpos, Apos), sel(ix, Bneg, Aneg));
-        else r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
+        if (B8) {
+            // per lane the two candidates of one magnitude sum to 0x10000 (0x8000 -+ A ...,
+            // lanes never zero), so the opposite-sign message is one IMAD: 0x10000 - x
+            const uint32_t x = sel(ix, Bpos, Apos);
+            uint32_t y;
+            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(y) : "r"(x), "r"(k.m1), "r"(0x00010000u));
+            r[j] = sel(sq, x, y);
+        } else {
+            r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
+        }
         if ((j & 1) == 0) {
             sqp = sq;
             ixp = ix;

@@ -20,6 +20,8 @@
 // degree); other codes -- thread t owns rows t, t + T, t + 2T, ...  The TMEM column of
 // a row's state is its slot b.
 #pragma once
+#include <type_traits>
+
 #include "k_resident.cuh"
 
 namespace ldpc {
@@ -42,7 +44,7 @@ __device__ __forceinline__ uint32_t atom_row_parity(const uint32_t (&L)[DC]) {
     return (DC & 1) ? (x ^ 0x80008000u) : x;            // [Z <= 0] = NOT bit 14
 }
 
-template <int DC, bool QC, bool ES>
+template <int DC, bool QC, bool ES, int VM>
 __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba, int e0,
                                          uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
     uint32_t d[DC];
@@ -68,7 +70,7 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
         rebuild_q_b8<DC, kAtomQ0>(L, st, q, a.rk);                         // Z_n - L^(k-1)_mn
     }
     uint32_t rn[DC];                                                     // V(L^(k)_mn) + 0x8000
-    new_state<DC, true>(q, vk, st, rn, a.rk);
+    new_state<DC, true, VM>(q, vk, st, rn, a.rk);
 #pragma unroll
     for (int j = 0; j < DC; ++j)                                          // Z^(k)_n += L^(k)_mn
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");
@@ -107,7 +109,7 @@ __device__ __forceinline__ void full_tmem_store(uint32_t taddr, const uint32_t (
     }
 }
 
-template <int DC, bool QC, bool ES>
+template <int DC, bool QC, bool ES, int VM>
 __device__ __forceinline__ void atom_row_full(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp,
                                               uint32_t ba, int e0, uint32_t r4, int p, bool first_iter,
                                               uint32_t (&c)[8], uint32_t &synd) {
@@ -131,7 +133,7 @@ __device__ __forceinline__ void atom_row_full(const ResArgs &a, const QcTab &t, 
     for (int j = 0; j < DC; ++j) q[j] = fadd32(L[j], first_iter ? kAtomQ0 : c[j], a.rk);   // Z - L_old
     uint32_t rn[DC];
     RowState st;                                                         // unused: no compact state
-    new_state<DC, true>(q, vk, st, rn, a.rk);                           // Eq.(3)
+    new_state<DC, true, VM>(q, vk, st, rn, a.rk);                           // Eq.(3)
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");   // Z += L
@@ -144,7 +146,7 @@ __device__ __forceinline__ void atom_row_full(const ResArgs &a, const QcTab &t, 
 // with the other's work.  The full-message kernel is held to 2 CTAs/SM by TMEM, so the
 // 4 warps per scheduler alone cannot hide that latency.  Flooding reads Z^(k-1) and
 // accumulates into Z^(k) (different buffers), so the order of the two rows is free.
-template <int DC, bool ES>
+template <int DC, bool ES, int VM>
 __device__ __forceinline__ void atom_row_full_x2(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp,
                                                  uint32_t ba, int e0, int e1, uint32_t r4, bool first_iter,
                                                  uint32_t (&c0)[8], uint32_t (&c1)[8], uint32_t &synd) {
@@ -171,8 +173,8 @@ __device__ __forceinline__ void atom_row_full_x2(const ResArgs &a, const QcTab &
     }
     uint32_t rn0[DC], rn1[DC];
     RowState st;
-    new_state<DC, true>(q0, vk, st, rn0, a.rk);
-    new_state<DC, true>(q1, vk, st, rn1, a.rk);
+    new_state<DC, true, VM>(q0, vk, st, rn0, a.rk);
+    new_state<DC, true, VM>(q1, vk, st, rn1, a.rk);
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d0[j] + ba), "r"(rn0[j]) : "memory");
@@ -182,7 +184,7 @@ __device__ __forceinline__ void atom_row_full_x2(const ResArgs &a, const QcTab &
     }
 }
 
-template <int DC, bool ES, int FMT>
+template <int DC, bool ES, int FMT, int VM>
 __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t tw,
                                            int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba, bool first_iter,
                                            uint32_t &synd) {
@@ -200,7 +202,7 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
                 full_tmem_load<DC>(col1, c1);
             }
             if (rloc < a.Z)
-                atom_row_full_x2<DC, ES>(a, t, vk, bp, ba, t.e0[b][g], t.e0[b + 1][g], r4, first_iter, c0, c1, synd);
+                atom_row_full_x2<DC, ES, VM>(a, t, vk, bp, ba, t.e0[b][g], t.e0[b + 1][g], r4, first_iter, c0, c1, synd);
             full_tmem_store<DC>(col0, c0);
             full_tmem_store<DC>(col1, c1);
         }
@@ -210,7 +212,7 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
             uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
             const uint32_t col = tw + (uint32_t)t.tcol[b][g];
             if (!first_iter) full_tmem_load<DC>(col, c);
-            if (rloc < a.Z) atom_row_full<DC, true, ES>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, c, synd);
+            if (rloc < a.Z) atom_row_full<DC, true, ES, VM>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, c, synd);
             full_tmem_store<DC>(col, c);
         }
         return b;
@@ -219,55 +221,55 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
         for (; b < bend; ++b) {
             RowState st = {0u, 0u, 0u};
             if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-            if (rloc < a.Z) atom_row<DC, true, ES>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
+            if (rloc < a.Z) atom_row<DC, true, ES, VM>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
             state_tmem_store<FMT>(tw, b, nb, st);
         }
         return b;
     }
 }
 
-template <bool ES, int FMT>
+template <bool ES, int FMT, int VM>
 __device__ __forceinline__ int atom_qc_dispatch(int dc, int b, int bend, int g, const ResArgs &a, const QcTab &t,
                                                 const VarK &vk, uint32_t tw, int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba,
                                                 bool first_iter, uint32_t &synd) {
     switch (dc) {
-    case 2: return atom_qc_run<2, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 3: return atom_qc_run<3, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 4: return atom_qc_run<4, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 5: return atom_qc_run<5, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 6: return atom_qc_run<6, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 7: return atom_qc_run<7, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 8: return atom_qc_run<8, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    default: return atom_qc_run<0, ES, FMT>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 2: return atom_qc_run<2, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 3: return atom_qc_run<3, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 4: return atom_qc_run<4, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 5: return atom_qc_run<5, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 6: return atom_qc_run<6, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 7: return atom_qc_run<7, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 8: return atom_qc_run<8, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    default: return atom_qc_run<0, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
     }
 }
 
-template <bool ES>
+template <bool ES, int VM>
 __device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba,
                                                   int p, bool first_iter, RowState &st, uint32_t &synd) {
     switch (dc) {
-    case 2: atom_row<2, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 3: atom_row<3, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 4: atom_row<4, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 5: atom_row<5, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 6: atom_row<6, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 7: atom_row<7, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 8: atom_row<8, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 2: atom_row<2, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 3: atom_row<3, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 4: atom_row<4, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 5: atom_row<5, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 6: atom_row<6, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 7: atom_row<7, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 8: atom_row<8, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
     }
 }
 
-template <bool ES>
+template <bool ES, int VM>
 __device__ __forceinline__ void atom_csr_dispatch_full(int dc, const ResArgs &a, const QcTab &t, const VarK &vk,
                                                        uint32_t bp, uint32_t ba, int p, bool first_iter,
                                                        uint32_t (&c)[8], uint32_t &synd) {
     switch (dc) {
-    case 2: atom_row_full<2, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
-    case 3: atom_row_full<3, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
-    case 4: atom_row_full<4, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
-    case 5: atom_row_full<5, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
-    case 6: atom_row_full<6, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
-    case 7: atom_row_full<7, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
-    case 8: atom_row_full<8, false, ES>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 2: atom_row_full<2, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 3: atom_row_full<3, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 4: atom_row_full<4, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 5: atom_row_full<5, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 6: atom_row_full<6, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 7: atom_row_full<7, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
+    case 8: atom_row_full<8, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, c, synd); break;
     }
 }
 
@@ -341,30 +343,37 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             uint32_t synd = 0;
             const bool first_iter = (k == 1);
             const VarK vk = a.nsched ? a.vk_sched[k - 1] : a.vk;   // lambda_k / beta_k
-            if (QC) {
+            // one scan over this thread's rows; the check-node variant (offset / normalized)
+            // is fixed per iteration, so it is a template parameter of the row code
+            auto scan = [&](auto vm_tag) {
+                constexpr int VM = decltype(vm_tag)::value;
+                if (QC) {
 #pragma unroll 1
-                for (int b = 0; b < nb;) {
-                    if (grp == 0) b = atom_qc_dispatch<ES, FMT>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-                    else b = atom_qc_dispatch<ES, FMT>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-                }
-            } else {
+                    for (int b = 0; b < nb;) {
+                        if (grp == 0) b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+                        else b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+                    }
+                } else {
 #pragma unroll 1
-                for (int b = 0; b < nb; ++b) {
-                    const int p = b * nth + tid;
-                    if constexpr (FMT == FMT_FULL) {
-                        // rows of one slot differ in degree across the warp: 8 columns per slot
-                        uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-                        if (!first_iter) full_tmem_load<8>(tw + 8u * b, c);
-                        if (p < a.M) atom_csr_dispatch_full<ES>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, c, synd);
-                        full_tmem_store<8>(tw + 8u * b, c);
-                    } else {
-                        RowState st = {0u, 0u, 0u};
-                        if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-                        if (p < a.M) atom_csr_dispatch<ES>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, st, synd);
-                        state_tmem_store<FMT>(tw, b, nb, st);
+                    for (int b = 0; b < nb; ++b) {
+                        const int p = b * nth + tid;
+                        if constexpr (FMT == FMT_FULL) {
+                            // rows of one slot differ in degree across the warp: 8 columns per slot
+                            uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                            if (!first_iter) full_tmem_load<8>(tw + 8u * b, c);
+                            if (p < a.M) atom_csr_dispatch_full<ES, VM>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, c, synd);
+                            full_tmem_store<8>(tw + 8u * b, c);
+                        } else {
+                            RowState st = {0u, 0u, 0u};
+                            if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
+                            if (p < a.M) atom_csr_dispatch<ES, VM>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, st, synd);
+                            state_tmem_store<FMT>(tw, b, nb, st);
+                        }
                     }
                 }
-            }
+            };
+            if (vk.norm) scan(std::integral_constant<int, 1>{});
+            else scan(std::integral_constant<int, 0>{});
             tmem_wait_st();
             const char *Lpb = (const char *)((k & 1) ? buf0 : buf1);
             if (ES) {

@@ -140,13 +140,16 @@ static __device__ __noinline__ uint32_t variant_mag_norm(uint32_t m, uint32_t na
     return vaddmin_relu(x, nb2, q2);
 }
 
-template <bool B8 = false>
+// VM: -1 = decide offset / normalized at run time (v.norm); 0 / 1 = the caller already did
+// (the barrier-free kernel dispatches once per iteration, keeping the branch out of its rows)
+template <bool B8 = false, int VM = -1>
 __device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const RegK &k) {
     if (B8) {
         // m = 0x8000 + 2|q| exactly (new_state<B8>); as a signed half that is 2|q| - 0x8000, so
         // relu(min(2|q| - 2 beta, 2Q)) is one VIADDMNMX with the unbias folded into the added
         // constant 0x8000 - 2 beta (16-bit wrap-around add)
-        if (__builtin_expect(v.norm != 0, 0)) return variant_mag_norm(m ^ 0x80008000u, v.na, v.ns, v.nmask, v.nb2, v.q2);
+        if (VM == 1 || (VM < 0 && __builtin_expect(v.norm != 0, 0)))
+            return variant_mag_norm(m ^ 0x80008000u, v.na, v.ns, v.nmask, v.nb2, v.q2);
         return vaddmin_relu(m, v.nb8, v.q2);
     }
     if (__builtin_expect(v.norm != 0, 0)) return variant_mag_norm(m, v.na, v.ns, v.nmask, v.nb2, v.q2);
@@ -165,7 +168,7 @@ __device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const
 // unsigned, the per-lane sign mask is [q >= 0] (bit 15), and the returned messages are
 // "V form + 0x8000": r ^ 0x8000 in the low lane == V(r) + 0x8000 as a 32-bit integer, so a
 // 32-bit RED adds them exactly (the accumulator start value is lowered by dv_n 0x8000).
-template <int DC, bool B8 = false>
+template <int DC, bool B8 = false, int VM = -1>
 __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &vk, RowState &st, uint32_t (&r)[DC],
                                           const RegK &k) {
     uint32_t mt[DC];
@@ -181,8 +184,8 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
     // negative iff the count of negative ones, DC - that, is odd
     if (B8 && (DC & 1)) par ^= 0x80008000u;
     const uint32_t Pm = signmask(par);                          // product of all signs < 0
-    const uint32_t A = variant_mag<B8>(m1, vk, k);
-    const uint32_t B = variant_mag<B8>(m2, vk, k);
+    const uint32_t A = variant_mag<B8, VM>(m1, vk, k);
+    const uint32_t B = variant_mag<B8, VM>(m2, vk, k);
     uint32_t nA, nB, Ac = A, Bc = B;
     if (B8) {
         // message candidates V(+-A) + 0x8000 (the RED operand): V is linear and the lanes of

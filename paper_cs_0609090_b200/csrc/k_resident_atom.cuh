@@ -345,13 +345,14 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             const VarK vk = a.nsched ? a.vk_sched[k - 1] : a.vk;   // lambda_k / beta_k
             // one scan over this thread's rows; the check-node variant (offset / normalized)
             // is fixed per iteration, so it is a template parameter of the row code
-            auto scan = [&](auto vm_tag) {
+            auto scan = [&](auto vm_tag, auto fi_tag) {
                 constexpr int VM = decltype(vm_tag)::value;
+                constexpr bool FI = decltype(fi_tag)::value;   // first iteration: no rebuild, no state load
                 if (QC) {
 #pragma unroll 1
                     for (int b = 0; b < nb;) {
-                        if (grp == 0) b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-                        else b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+                        if (grp == 0) b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, bp, ba, FI, synd);
+                        else b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, bp, ba, FI, synd);
                     }
                 } else {
 #pragma unroll 1
@@ -360,20 +361,27 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
                         if constexpr (FMT == FMT_FULL) {
                             // rows of one slot differ in degree across the warp: 8 columns per slot
                             uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-                            if (!first_iter) full_tmem_load<8>(tw + 8u * b, c);
-                            if (p < a.M) atom_csr_dispatch_full<ES, VM>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, c, synd);
+                            if (!FI) full_tmem_load<8>(tw + 8u * b, c);
+                            if (p < a.M) atom_csr_dispatch_full<ES, VM>(a.dcT[p], a, t, vk, bp, ba, p, FI, c, synd);
                             full_tmem_store<8>(tw + 8u * b, c);
                         } else {
                             RowState st = {0u, 0u, 0u};
-                            if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-                            if (p < a.M) atom_csr_dispatch<ES, VM>(a.dcT[p], a, t, vk, bp, ba, p, first_iter, st, synd);
+                            if (!FI) state_tmem_load<FMT>(tw, b, nb, st);
+                            if (p < a.M) atom_csr_dispatch<ES, VM>(a.dcT[p], a, t, vk, bp, ba, p, FI, st, synd);
                             state_tmem_store<FMT>(tw, b, nb, st);
                         }
                     }
                 }
             };
-            if (vk.norm) scan(std::integral_constant<int, 1>{});
-            else scan(std::integral_constant<int, 0>{});
+            using F1 = std::integral_constant<bool, true>;
+            using F0 = std::integral_constant<bool, false>;
+            if (vk.norm) {
+                if (first_iter) scan(std::integral_constant<int, 1>{}, F1{});
+                else scan(std::integral_constant<int, 1>{}, F0{});
+            } else {
+                if (first_iter) scan(std::integral_constant<int, 0>{}, F1{});
+                else scan(std::integral_constant<int, 0>{}, F0{});
+            }
             tmem_wait_st();
             const char *Lpb = (const char *)((k & 1) ? buf0 : buf1);
             if (ES) {

@@ -124,9 +124,8 @@ __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *
     }
 }
 
-// PAIR = true: int16 pairs (V-form accumulators); false: fp32.
-template <bool PAIR, int FMT, bool ES>
-__global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe(const StreamArgs a, int k) {
+template <bool PAIR, int FMT, bool ES, bool FI>
+__device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
     extern __shared__ __align__(128) uint32_t psm[];
     uint32_t *coltab = psm;                                       // [RB][8]
     uint8_t *dctab = (uint8_t *)(psm + kPipeRB * 8);              // [RB]
@@ -182,7 +181,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe
         }
     }
     __syncwarp();
-    const bool first_iter = (k == 1);
+    constexpr bool first_iter = FI;                   // compile-time: no rebuild / state copy in iteration 1
     const int nst_copy = first_iter ? 0 : nst;
     uint32_t *wring = ring + (size_t)warp * kPipeD * kPipeLines * 32;
     const uint32_t wring_s = (uint32_t)__cvta_generic_to_shared(wring);
@@ -241,6 +240,15 @@ __global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe
     }
     cp_async_wait<0>();
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
+}
+
+// PAIR = true: int16 pairs (V-form accumulators); false: fp32.  The first iteration (no
+// previous messages to rebuild, no state to read) is a separate instantiation of the body,
+// so rows carry no per-row branch (or if-converted both paths) for it.
+template <bool PAIR, int FMT, bool ES>
+__global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe(const StreamArgs a, int k) {
+    if (k == 1) pipe_body<PAIR, FMT, ES, true>(a, k);
+    else pipe_body<PAIR, FMT, ES, false>(a, k);
 }
 
 inline size_t pipe_smem_bytes() {

@@ -22,6 +22,7 @@
 // codes: the host builds batches by greedy row colouring and per-edge byte
 // offsets come from a [DC][M] table.
 #pragma once
+#include <type_traits>
 #include "args.cuh"
 #include "rowcore.cuh"
 #include "tmem.cuh"
@@ -342,35 +343,41 @@ __global__ void __launch_bounds__(256, 3) k_resident(const __grid_constant__ Res
                 if (done == 3) { finished = true; break; }
             }
             constexpr bool RES = ES && !LAY;         // flooding: syndrome fused into the gather
-            if (QC) {
-                // warp-uniform group branch: uniform table indices
+            // the first iteration (no rebuild, no state load) is a compile-time variant of the scan
+            auto scan = [&](auto fi_tag) {
+                constexpr bool FI = decltype(fi_tag)::value;
+                if (QC) {
+                    // warp-uniform group branch: uniform table indices
 #pragma unroll 1
-                for (int b = 0; b < nb;) {
-                    if (grp == 0) b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-                    else b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, first_iter, synd);
-                }
-            } else {
+                    for (int b = 0; b < nb;) {
+                        if (grp == 0) b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, FI, synd);
+                        else b = qc_run_dispatch<RES, FMT, LAY>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, Lpb, Lab, FI, synd);
+                    }
+                } else {
 #pragma unroll 1
-                for (int b = 0; b < nb; ++b) {
-                    RowState st = {0u, 0u, 0u};
-                    const int p = a.bptr[b] + tid;
-                    const bool valid = p < a.bptr[b + 1];
-                    if (LAY) {
-                        // layered general codes: batches can be single rows (e.g. a staircase),
-                        // so the state lives in shared memory indexed by row, [3][M] words
-                        if (!first_iter && valid) { st.A = sst[p]; st.B = sst[a.M + p]; st.W = sst[2 * a.M + p]; }
-                    } else if (!first_iter) {
-                        state_tmem_load<FMT>(tw, b, nb, st);
+                    for (int b = 0; b < nb; ++b) {
+                        RowState st = {0u, 0u, 0u};
+                        const int p = a.bptr[b] + tid;
+                        const bool valid = p < a.bptr[b + 1];
+                        if (LAY) {
+                            // layered general codes: batches can be single rows (e.g. a staircase),
+                            // so the state lives in shared memory indexed by row, [3][M] words
+                            if (!FI && valid) { st.A = sst[p]; st.B = sst[a.M + p]; st.W = sst[2 * a.M + p]; }
+                        } else if (!FI) {
+                            state_tmem_load<FMT>(tw, b, nb, st);
+                        }
+                        if (valid) res_dispatch<QC, RES, LAY>(a.dcT[p], a, t, vk, Lpb, Lab, 0, 0, p, FI, st, synd);
+                        if (LAY) {
+                            if (valid) { sst[p] = st.A; sst[a.M + p] = st.B; sst[2 * a.M + p] = st.W; }
+                        } else {
+                            state_tmem_store<FMT>(tw, b, nb, st);
+                        }
+                        __syncthreads();                     // batch b's accumulations complete
                     }
-                    if (valid) res_dispatch<QC, RES, LAY>(a.dcT[p], a, t, vk, Lpb, Lab, 0, 0, p, first_iter, st, synd);
-                    if (LAY) {
-                        if (valid) { sst[p] = st.A; sst[a.M + p] = st.B; sst[2 * a.M + p] = st.W; }
-                    } else {
-                        state_tmem_store<FMT>(tw, b, nb, st);
-                    }
-                    __syncthreads();                     // batch b's accumulations complete
                 }
-            }
+            };
+            if (first_iter) scan(std::integral_constant<bool, true>{});
+            else scan(std::integral_constant<bool, false>{});
             tmem_wait_st();
             if (RES) {
                 // syndrome of Z^(k-1), gathered during this scan (1-iteration lag)

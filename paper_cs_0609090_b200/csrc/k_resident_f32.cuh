@@ -196,22 +196,28 @@ __global__ void __launch_bounds__(256, 3) k_resident_f32(const __grid_constant__
             const bool first_iter = (k == 1);
             const float alpha = a.nsched ? a.alpha_sched[k - 1] : a.alpha;   // lambda_k / beta_k
             const float beta = a.nsched ? a.beta_sched[k - 1] : a.beta;
-            if (QC) {
+            // the first iteration (no rebuild, no state load) is a compile-time variant of the scan
+            auto scan = [&](auto fi_tag) {
+                constexpr bool FI = decltype(fi_tag)::value;
+                if (QC) {
 #pragma unroll 1
-                for (int b = 0; b < nb;) {
-                    if (grp == 0) b = f32res_qc_dispatch<ES>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, alpha, beta, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-                    else b = f32res_qc_dispatch<ES>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, alpha, beta, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-                }
-            } else {
+                    for (int b = 0; b < nb;) {
+                        if (grp == 0) b = f32res_qc_dispatch<ES>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, alpha, beta, tw, nb, rloc, r4, bp, ba, FI, synd);
+                        else b = f32res_qc_dispatch<ES>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, alpha, beta, tw, nb, rloc, r4, bp, ba, FI, synd);
+                    }
+                } else {
 #pragma unroll 1
-                for (int b = 0; b < nb; ++b) {
-                    const int p = b * nth + tid;
-                    RowState st = {0u, 0u, 0u};
-                    if (!first_iter) state_tmem_load<FMT_C16>(tw, b, nb, st);
-                    if (p < a.M) f32res_csr_dispatch<ES>(a.dcT[p], a, t, alpha, beta, bp, ba, p, first_iter, st, synd);
-                    state_tmem_store<FMT_C16>(tw, b, nb, st);
+                    for (int b = 0; b < nb; ++b) {
+                        const int p = b * nth + tid;
+                        RowState st = {0u, 0u, 0u};
+                        if (!FI) state_tmem_load<FMT_C16>(tw, b, nb, st);
+                        if (p < a.M) f32res_csr_dispatch<ES>(a.dcT[p], a, t, alpha, beta, bp, ba, p, FI, st, synd);
+                        state_tmem_store<FMT_C16>(tw, b, nb, st);
+                    }
                 }
-            }
+            };
+            if (first_iter) scan(std::integral_constant<bool, true>{});
+            else scan(std::integral_constant<bool, false>{});
             tmem_wait_st();
             const float *Lp = (k & 1) ? buf0 : buf1;
             if (ES) {

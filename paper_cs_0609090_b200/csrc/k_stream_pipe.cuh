@@ -58,7 +58,7 @@ __device__ __forceinline__ void pipe_issue_row(uint32_t slot, const uint32_t *Lp
     }
 }
 
-template <int DC, int FMT, bool ES>
+template <int DC, int FMT, bool ES, int VM>
 __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *sl, const uint32_t *cols, int m,
                                            int lane, uint32_t *Lat, uint32_t *stt, size_t sstride, bool first_iter,
                                            uint32_t keep, uint32_t &synd) {
@@ -85,7 +85,7 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
         rebuild_q_b8<DC>(L, st, q, a.rk);
     }
     uint32_t rn[DC];                                      // V(L^(k)_mn) + 0x8000
-    new_state<DC, true>(q, a.vk, st, rn, a.rk);
+    new_state<DC, true, VM>(q, a.vk, st, rn, a.rk);
     StateIO<FMT>::store(stt + lane, sstride, (size_t)m * 32, st);
 #pragma unroll
     for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, red_value(rn[j], keep));
@@ -124,7 +124,7 @@ __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *
     }
 }
 
-template <bool PAIR, int FMT, bool ES, bool FI>
+template <bool PAIR, int FMT, bool ES, bool FI, int VM>
 __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
     extern __shared__ __align__(128) uint32_t psm[];
     uint32_t *coltab = psm;                                       // [RB][8]
@@ -210,13 +210,13 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
         const int dc = dctab[r];
         if (PAIR) {
             switch (dc) {
-            case 2: pipe_row_i<2, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 3: pipe_row_i<3, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 4: pipe_row_i<4, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 5: pipe_row_i<5, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 6: pipe_row_i<6, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 7: pipe_row_i<7, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 8: pipe_row_i<8, FMT, ES>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 2: pipe_row_i<2, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 3: pipe_row_i<3, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 4: pipe_row_i<4, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 5: pipe_row_i<5, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 6: pipe_row_i<6, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 7: pipe_row_i<7, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            case 8: pipe_row_i<8, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
             }
         } else {
             switch (dc) {
@@ -244,11 +244,22 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
 
 // PAIR = true: int16 pairs (V-form accumulators); false: fp32.  The first iteration (no
 // previous messages to rebuild, no state to read) is a separate instantiation of the body,
-// so rows carry no per-row branch (or if-converted both paths) for it.
+// so rows carry no per-row branch (or if-converted both paths) for it; likewise the
+// check-node variant.
 template <bool PAIR, int FMT, bool ES>
 __global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe(const StreamArgs a, int k) {
-    if (k == 1) pipe_body<PAIR, FMT, ES, true>(a, k);
-    else pipe_body<PAIR, FMT, ES, false>(a, k);
+    // the integer check-node variant (offset / normalized) of this launch's iteration is a
+    // template parameter of the rows as well (fp32 rows take alpha / beta directly)
+    if constexpr (!PAIR) {
+        if (k == 1) pipe_body<PAIR, FMT, ES, true, 0>(a, k);
+        else pipe_body<PAIR, FMT, ES, false, 0>(a, k);
+    } else if (a.vk.norm == 0) {
+        if (k == 1) pipe_body<PAIR, FMT, ES, true, 0>(a, k);
+        else pipe_body<PAIR, FMT, ES, false, 0>(a, k);
+    } else {
+        if (k == 1) pipe_body<PAIR, FMT, ES, true, 1>(a, k);
+        else pipe_body<PAIR, FMT, ES, false, 1>(a, k);
+    }
 }
 
 inline size_t pipe_smem_bytes() {

@@ -64,10 +64,14 @@ def main():
                            "(cold-cache, serialised)")
     for c in (2, 4, 5):
         rep = os.path.join(MEAS, f"prof_cfg{c}.ncu-rep")
-        if not os.path.exists(rep):
-            continue
+        pre = os.path.join(MEAS, f"ncu_full_cfg{c}.json")          # summarised on the box
         dst = os.path.join(PROF, f"{tag}_ncu_full_cfg{c}.json")
-        subprocess.check_call([sys.executable, summ, "raw", rep, dst], stdout=subprocess.DEVNULL)
+        if os.path.exists(pre):
+            shutil.copy(pre, dst)
+        elif os.path.exists(rep):
+            subprocess.check_call([sys.executable, summ, "raw", rep, dst], stdout=subprocess.DEVNULL)
+        else:
+            continue
         with open(dst) as f:
             d = json.load(f)[0]
         mb = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}

@@ -16,6 +16,8 @@ for c in 2 4 5; do
   timeout 300 python tools/prof_decode.py --config $c --reps 2 > $OUT/prof_plain_cfg$c.log 2>&1 && \
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K -s 1 -c 1 -o $OUT/prof_cfg$c \
     python tools/prof_decode.py --config $c --reps 2 > $OUT/ncu_cfg$c.log 2>&1; echo "ncu cfg$c rc=$?"
+  # summarise on the box (the full reports exceed what gpurun copies back)
+  python tools/ncu_summary.py raw $OUT/prof_cfg$c.ncu-rep $OUT/ncu_full_cfg$c.json > /dev/null 2>&1 && rm -f $OUT/prof_cfg$c.ncu-rep
 done
 # two-scan baseline launch list (cfg2): per-kernel time and DRAM bytes
 timeout 300 python tools/prof_decode.py --config 2 --sched 1 --reps 1 > /dev/null 2>&1 && \

@@ -53,6 +53,7 @@ struct ResArgs {
     int cols_per_group;               // TMEM columns used by one group of threads
     RegK rk;                          // register constants (simd16.cuh)
     uint32_t cpar;                    // row_parity constant (-(0x00010001), biased: -(0x40014001))
+    int csr_smem, csr_dc;             // barrier-free kernel, general codes: colT rows [0, csr_dc) staged in smem
 };
 
 struct StreamArgs {

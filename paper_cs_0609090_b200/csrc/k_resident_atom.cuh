@@ -44,9 +44,12 @@ __device__ __forceinline__ uint32_t atom_row_parity(const uint32_t (&L)[DC]) {
     return (DC & 1) ? (x ^ 0x80008000u) : x;            // [Z <= 0] = NOT bit 14
 }
 
-template <int DC, bool QC, bool ES, int VM>
+// CSM (general codes): the [dc][M] column table was staged in shared memory at byte
+// address sct (ResArgs::csr_smem), so the per-edge offsets are shared-memory loads
+template <int DC, bool QC, bool ES, int VM, bool CSM = false>
 __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba, int e0,
-                                         uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
+                                         uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd,
+                                         uint32_t sct = 0) {
     uint32_t d[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
@@ -54,6 +57,8 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
             const uint2 e = t.ent[e0 + j];
             const uint32_t u = r4 + e.x;
             d[j] = min(u - t.Z4, u) + e.y;                 // 4 * (jZ + (r + s) mod Z)
+        } else if (CSM) {
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(d[j]) : "r"(sct + 4u * (uint32_t)(j * a.M + p)));
         } else {
             d[j] = __ldg(a.colT + (size_t)j * a.M + p);
         }
@@ -244,17 +249,17 @@ __device__ __forceinline__ int atom_qc_dispatch(int dc, int b, int bend, int g, 
     }
 }
 
-template <bool ES, int VM>
+template <bool ES, int VM, bool CSM>
 __device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba,
-                                                  int p, bool first_iter, RowState &st, uint32_t &synd) {
+                                                  int p, bool first_iter, RowState &st, uint32_t &synd, uint32_t sct) {
     switch (dc) {
-    case 2: atom_row<2, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 3: atom_row<3, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 4: atom_row<4, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 5: atom_row<5, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 6: atom_row<6, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 7: atom_row<7, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
-    case 8: atom_row<8, false, ES, VM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd); break;
+    case 2: atom_row<2, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 3: atom_row<3, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 4: atom_row<4, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 5: atom_row<5, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 6: atom_row<6, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 7: atom_row<7, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 8: atom_row<8, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
     }
 }
 
@@ -327,6 +332,12 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
     const uint32_t zbytes = 4u * (uint32_t)a.Np;
     const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(buf0), s1 = (uint32_t)__cvta_generic_to_shared(buf1);
     uint32_t zphase = 0;
+    // general codes: stage the [dc][M] column table after the posterior buffers (planner:
+    // ResArgs::csr_smem when it fits without costing occupancy); visible after the first
+    // barrier of the pair loop
+    const uint32_t sct = s0 + 8u * (uint32_t)a.Np;
+    if (!QC && a.csr_smem)
+        for (int i = tid; i < a.csr_dc * a.M; i += nth) smem[2 * a.Np + i] = __ldg(a.colT + i);
 
     for (int pair = blockIdx.x; pair < a.npairs; pair += gridDim.x) {
         const int f0 = 2 * pair, f1 = f0 + 1;
@@ -345,9 +356,10 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             const VarK vk = a.nsched ? a.vk_sched[k - 1] : a.vk;   // lambda_k / beta_k
             // one scan over this thread's rows; the check-node variant (offset / normalized)
             // is fixed per iteration, so it is a template parameter of the row code
-            auto scan = [&](auto vm_tag, auto fi_tag) {
+            auto scan = [&](auto vm_tag, auto fi_tag, auto cs_tag) {
                 constexpr int VM = decltype(vm_tag)::value;
                 constexpr bool FI = decltype(fi_tag)::value;   // first iteration: no rebuild, no state load
+                constexpr bool CSM = decltype(cs_tag)::value;  // general codes: column table in shared memory
                 if (QC) {
 #pragma unroll 1
                     for (int b = 0; b < nb;) {
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
                         } else {
                             RowState st = {0u, 0u, 0u};
                             if (!FI) state_tmem_load<FMT>(tw, b, nb, st);
-                            if (p < a.M) atom_csr_dispatch<ES, VM>(a.dcT[p], a, t, vk, bp, ba, p, FI, st, synd);
+                            if (p < a.M) atom_csr_dispatch<ES, VM, CSM>(a.dcT[p], a, t, vk, bp, ba, p, FI, st, synd, sct);
                             state_tmem_store<FMT>(tw, b, nb, st);
                         }
                     }
@@ -375,13 +387,17 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             };
             using F1 = std::integral_constant<bool, true>;
             using F0 = std::integral_constant<bool, false>;
-            if (vk.norm) {
-                if (first_iter) scan(std::integral_constant<int, 1>{}, F1{});
-                else scan(std::integral_constant<int, 1>{}, F0{});
-            } else {
-                if (first_iter) scan(std::integral_constant<int, 0>{}, F1{});
-                else scan(std::integral_constant<int, 0>{}, F0{});
-            }
+            auto run = [&](auto vm) {
+                if (!QC && FMT != FMT_FULL && a.csr_smem) {
+                    if (first_iter) scan(vm, F1{}, F1{});
+                    else scan(vm, F0{}, F1{});
+                } else {
+                    if (first_iter) scan(vm, F1{}, F0{});
+                    else scan(vm, F0{}, F0{});
+                }
+            };
+            if (vk.norm) run(std::integral_constant<int, 1>{});
+            else run(std::integral_constant<int, 0>{});
             tmem_wait_st();
             const char *Lpb = (const char *)((k & 1) ? buf0 : buf1);
             if (ES) {

@@ -545,6 +545,7 @@ struct Plan {
     size_t slot_words = 0;
     uint32_t tmem_cols = 0, tmem_cols_needed = 0;
     int cols_per_group = 0;
+    int csr_smem = 0;            // barrier-free kernel, general codes: column table in shared memory
     // stream
     int tile = 64, ntiles = 0;
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
@@ -767,6 +768,18 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "occupancy query: %s", cudaGetErrorString(e));
         if (getenv("LDPC_DEBUG")) fprintf(stderr, "[ldpc] occupancy API: %d blocks/SM\n", blocks);
         blocks = std::min(blocks, (int)(512 / cols));     // TMEM capacity per SM
+        // barrier-free kernel on a general (CSR) code: stage its [dc][M] column table in
+        // shared memory (per-edge offsets become shared loads) when that costs no occupancy
+        if (pl.kind == RES_ATOM && !c->qc && pl.fmt != FMT_FULL) {
+            Plan ps = pl;
+            ps.smem = pl.smem + (size_t)4 * c->max_dc * c->M;
+            int bs = 0;
+            if (ps.smem <= c->smem_optin && res_occupancy_any(c, p, ps, &bs) == cudaSuccess &&
+                std::min(bs, (int)(512 / cols)) >= blocks) {
+                pl.csr_smem = 1;
+                pl.smem = ps.smem;
+            }
+        }
         if (blocks < 1) return fail(LDPC_ERR_UNSUPPORTED, "resident kernel does not fit on an SM");
         // One frame pair per CTA (grid = pairs, up to 64 waves): the block scheduler then
         // balances the SMs dynamically.  Measured against a persistent grid of `blocks x SMs`
@@ -836,6 +849,8 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.colT = natural ? c->d_colT_lay : c->d_colT;
     a.dcT = natural ? c->d_dcT_lay : c->d_dcT;
     a.cpar = pl.kind == RES_ATOM ? 0xBFFFC000u : 0xFFFEFFFFu;   // -(bias + 1) per lane (atom: bias 0x3FFF)
+    a.csr_smem = pl.csr_smem;
+    a.csr_dc = c->max_dc;
     a.alpha = pl.alpha;
     a.beta = pl.betaf;
     if ((pl.kind == RES_F32 || pl.kind == RES_F32_LAY) && !pl.alphas.empty()) {

@@ -15,7 +15,8 @@ Engines (PAPER.md section / lines):
   LAYERED_FULL   Eq.(3) with ONE in-place posterior array, rows in ascending m (layered /
                  Gauss-Seidel reading D25); per-edge L, Eq.(1) literally
   LAYERED        the same schedule over the §5 compact state -- the GPU layered target
-Numeric modes: "int" (int32 raw LSBs; offset beta + clamp Q), "f64", "f32".
+Numeric modes: "int" (int32 raw LSBs; offset beta + clamp Q), "f64", "f32" (one rounding per
+operation, reading D11; posterior sums exact and rounded once, reading D28).
 """
 from __future__ import annotations
 
@@ -73,6 +74,8 @@ def lib():
             h = getattr(L, f"orc_check_compact_{suf}")
             h.argtypes = [ctypes.c_int, vp, ctypes.POINTER(Params), vp, vp, vp, vp, vp]
         L.orc_hardware_threads.restype = ctypes.c_int
+        L.orc_f32_exact_sum.argtypes = [ctypes.c_int, vp]
+        L.orc_f32_exact_sum.restype = ctypes.c_float
         _lib = L
     return _lib
 
@@ -171,6 +174,13 @@ def decode(code, z0: np.ndarray, engine="compact", mode="int", max_iter=10, earl
     if nt < 0:
         raise ValueError("invalid code")
     return Result(post, bits, ok, iters, tp, tm, nt)
+
+
+def f32_exact_sum(x) -> np.float32:
+    """The fp32 posterior-sum rule of reading D28 on one list of terms: each term saturated
+    to [-2^20, 2^20] and placed on the 2^-34 grid, summed exactly, rounded once to fp32."""
+    x = np.ascontiguousarray(x, np.float32)
+    return np.float32(lib().orc_f32_exact_sum(len(x), _ptr(x)))
 
 
 def pack_bits(bits: np.ndarray) -> np.ndarray:

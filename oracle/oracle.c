@@ -18,7 +18,8 @@
  *                      layered / Gauss-Seidel reading, DESIGN D25),
  *                      per-edge L_mn and Eq.(1) evaluated literally.
  *   ENG_LAYERED        the same schedule over the §5 compact state (GPU layered target).
- * Numeric types: int32 (fixed point, offset + clamp), double, float.
+ * Numeric types: int32 (fixed point, offset + clamp), double, float (one rounding per
+ * operation, D11; posterior sums exact and rounded once, D28).
  * Readings of silent/ambiguous passages are listed in DESIGN.md §3 (D1-D27).
  * Parity pins: tests/test_oracle.py, tests/golden/ (none of this file is "parity unpinned").
  */
@@ -75,32 +76,78 @@ static void orc_code_free(orc_code *c) { free(c->vptr); free(c->vedge); }
 #define FN2(a, b) a##_##b
 #define FN1(a, b) FN2(a, b)
 
+/* Sums of several messages into a posterior (the flooding Z^(k)_n = Z^(0)_n + sum_m L_mn of
+ * P:164-165 / P:318-322 and the two-scan variable rule Eq.(2)) go through an
+ * accumulator type ACC: ACC_OF(x) enters a value, VAL_OF(a) leaves.  int and f64: the value
+ * type itself, added in ascending m.  f32 (reading D28): the sum is evaluated
+ * EXACTLY and rounded to fp32 once -- every term is placed on the fixed-point grid 2^-34
+ * (exact for |x| >= 2^-11, round-half-even below), the grid integers are added in int64 (no
+ * overflow: |x| <= 2^20 by the saturation below and at most 255 terms), and the total is
+ * rounded to the nearest fp32.  Integer addition is associative, so the result does not
+ * depend on the order of the terms. */
+#define ORC_F32_GRID 34
+#define ORC_F32_SAT 1048576.0f   /* 2^20: fp32 channel LLRs and message magnitudes saturate here (D28) */
+static inline int64_t orc_f32_to_grid(float x) { return (int64_t)nearbyint(ldexp((double)x, ORC_F32_GRID)); }
+static inline float orc_grid_to_f32(int64_t a) { return ldexpf((float)a, -ORC_F32_GRID); }
+
 /* fixed point: raw integer LSB units */
 #define VAL int32_t
 #define VAL_IS_INT 1
+#define VAL_IS_F32 0
+#define ACC int32_t
+#define ACC_OF(x) (x)
+#define VAL_OF(a) (a)
 #define FN(x) FN1(x, i32)
 #include "engine.inc"
 #undef VAL
 #undef VAL_IS_INT
+#undef VAL_IS_F32
+#undef ACC
+#undef ACC_OF
+#undef VAL_OF
 #undef FN
 
 /* float64 */
 #define VAL double
 #define VAL_IS_INT 0
+#define VAL_IS_F32 0
+#define ACC double
+#define ACC_OF(x) (x)
+#define VAL_OF(a) (a)
 #define FN(x) FN1(x, f64)
 #include "engine.inc"
 #undef VAL
 #undef VAL_IS_INT
+#undef VAL_IS_F32
+#undef ACC
+#undef ACC_OF
+#undef VAL_OF
 #undef FN
 
-/* float32 (reading D11: one round-to-nearest per operation, no contraction) */
+/* float32 (reading D11: one round-to-nearest per operation, no contraction; reading D28:
+ * posterior sums exact, rounded once) */
 #define VAL float
 #define VAL_IS_INT 0
+#define VAL_IS_F32 1
+#define ACC int64_t
+#define ACC_OF(x) orc_f32_to_grid(x)
+#define VAL_OF(a) orc_grid_to_f32(a)
 #define FN(x) FN1(x, f32)
 #include "engine.inc"
 #undef VAL
 #undef VAL_IS_INT
+#undef VAL_IS_F32
+#undef ACC
+#undef ACC_OF
+#undef VAL_OF
 #undef FN
+
+/* test hooks for the D28 accumulator (tests/test_oracle.py pins it against exact rational sums) */
+float orc_f32_exact_sum(int n, const float *x) {
+    int64_t a = 0;
+    for (int i = 0; i < n; ++i) a += orc_f32_to_grid(x[i] > ORC_F32_SAT ? ORC_F32_SAT : (x[i] < -ORC_F32_SAT ? -ORC_F32_SAT : x[i]));
+    return orc_grid_to_f32(a);
+}
 
 int orc_hardware_threads(void) {
     long n = sysconf(_SC_NPROCESSORS_ONLN);

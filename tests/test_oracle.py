@@ -449,3 +449,63 @@ def test_float_schedule_matches_scalar_and_twoscan():
     s1 = oracle.decode(code, z0, "compact", "f64", 15, 0, alpha=0.8, trace=True)
     s2 = oracle.decode(code, z0, "compact", "f64", 15, 0, trace=True, alpha_sched=[0.8] * 15)
     assert np.array_equal(s1.trace_post, s2.trace_post)
+
+
+# ---------------------------------------- reading D28: fp32 posterior sums
+def _rn_f32(q):
+    """Round a Fraction to the nearest float32, ties to even (no double rounding)."""
+    from fractions import Fraction
+    a = np.float32(float(q))
+    best = None
+    for c in (np.nextafter(a, np.float32(-np.inf)), a, np.nextafter(a, np.float32(np.inf))):
+        d = abs(Fraction(float(c)) - q)
+        key = (d, int(np.array(c, np.float32).view(np.uint32)) & 1)
+        if best is None or key < best[0]:
+            best = (key, c)
+    return np.float32(best[1])
+
+
+def test_f32_posterior_sum_is_exact_then_rounded_once():
+    """D28: Z_n = Z0_n + sum_m L_mn is the exact rational sum rounded once to fp32 (pinned
+    against Fraction arithmetic, not against the oracle's own grid), for terms with
+    2^-11 <= |x| <= 2^20 where the 2^-34 grid holds every fp32 value exactly; the result does
+    not depend on the order of the terms; magnitudes beyond 2^20 saturate."""
+    from fractions import Fraction
+    rng = np.random.default_rng(28)
+    for trial in range(400):
+        n = int(rng.integers(1, 12))
+        mag = np.exp2(rng.uniform(-11, 20, n)).astype(np.float32)
+        x = (mag * rng.choice([-1, 1], n)).astype(np.float32)
+        x = np.clip(x, -2.0 ** 20, 2.0 ** 20).astype(np.float32)
+        exact = sum((Fraction(float(v)) for v in x), Fraction(0))
+        want = _rn_f32(exact)
+        got = oracle.f32_exact_sum(x)
+        assert got.view(np.uint32) == want.view(np.uint32), (x, got, want)
+        perm = x[rng.permutation(n)]
+        assert oracle.f32_exact_sum(perm).view(np.uint32) == got.view(np.uint32)
+    # a sequential fp32 sum is order-dependent where the exact sum is not
+    x = np.array([1.0, 2.0 ** -24, 2.0 ** -24], np.float32)
+    assert oracle.f32_exact_sum(x) == np.float32(1.0 + 2.0 ** -23)
+    assert np.float32(np.float32(1.0) + np.float32(2.0 ** -24)) + np.float32(2.0 ** -24) == np.float32(1.0)
+    # saturation at 2^20 and terms far below the grid
+    assert oracle.f32_exact_sum(np.array([3e7], np.float32)) == np.float32(2.0 ** 20)
+    assert oracle.f32_exact_sum(np.array([2.5, 1e-12], np.float32)) == np.float32(2.5)
+
+
+def test_f32_flooding_engines_order_free():
+    """D28 consequences in fp32: the compact single-scan equals the per-edge single-scan bit
+    for bit (same messages, exact sums), and since the order of the rows does not enter an
+    exact sum, permuting the rows of H leaves every posterior unchanged (a sequential fp32
+    sum would not be order-free)."""
+    code = g.dvbs2like(600, 300, 120, 8, 3, seed=6)
+    z0 = g.llr(2005, 0, 8, code.n_vars, g.ebn0_to_sigma2(1.0, code.rate), g.LLR_F32)
+    a = oracle.decode(code, z0, "compact", "f32", 20, 0, alpha=0.75)
+    b = oracle.decode(code, z0, "singlescan", "f32", 20, 0, alpha=0.75)
+    assert np.array_equal(a.post.view(np.uint32), b.post.view(np.uint32))
+    rng = np.random.default_rng(3)
+    order = rng.permutation(code.n_checks)
+    rows = [code.col_idx[code.row_ptr[m]:code.row_ptr[m + 1]] for m in order]
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int32)
+    perm = g.Code(code.n_vars, code.n_checks, rp, np.concatenate(rows).astype(np.int32), name="perm")
+    c = oracle.decode(perm, z0, "compact", "f32", 20, 0, alpha=0.75)
+    assert np.array_equal(a.post.view(np.uint32), c.post.view(np.uint32))

@@ -11,7 +11,7 @@
  *   - with the normalized / offset modifications,
  *   - hard decision and syndrome stop rule (§3),
  * decoding a batch of independent frames, using only check->variable addressing
- * (P:219-224).  Numeric readings of silent passages: DESIGN.md §3 (D1-D27).
+ * (P:219-224).  Numeric readings of silent passages: DESIGN.md §3 (D1-D28).
  *
  * Conventions (all entry points):
  *   - Plain C types only.  `stream` is a cudaStream_t passed as void* (NULL =
@@ -121,6 +121,25 @@ enum { LDPC_MSG_COMPACT = 0, LDPC_MSG_1BIT = 1,
  *               F32 LLRs (F32 layered is bit-exact with a sequential implementation). */
 enum { LDPC_SCHED_SINGLESCAN = 0, LDPC_SCHED_TWOSCAN = 1, LDPC_SCHED_LAYERED = 2 };
 
+/* Optional plan overrides (kernel cross-checks and tuning).  A NULL ldpc_decode_params.tuning
+ * or a zero field selects the automatic choice.  The library reads no environment variables:
+ * the plan depends only on the call's arguments. */
+enum { LDPC_PATH_AUTO = 0,               /* resident kernel when the code fits on chip, else streaming */
+       LDPC_PATH_STREAM = 1,             /* force the streaming (HBM) kernels */
+       LDPC_PATH_RESIDENT_BATCHED = 2 }; /* integer flooding: the resident kernel with conflict-free row
+                                            batches and a barrier per batch (instead of shared atomics) */
+typedef struct {
+    int32_t path;            /* LDPC_PATH_* */
+    int32_t resident_waves;  /* resident grid cap in waves of co-resident CTAs (0 = 64); larger
+                                batches loop over frame pairs */
+    int32_t stream_chunk_tiles; /* streaming: frame tiles decoded together through all iterations
+                                   (0 = all tiles at once) */
+    int32_t stream_register_kernels; /* streaming: 1 = the register kernels instead of the cp.async
+                                        row pipeline (cross-check), 0 = automatic */
+    int32_t host_chunks;     /* ldpc_decode_batch_host: frame chunks (0 = automatic) */
+    int32_t host_streams;    /* ldpc_decode_batch_host: internal streams, 1..4 (0 = automatic) */
+} ldpc_tuning;
+
 typedef struct {
     int32_t max_iter;      /* >= 1: the iteration cap of P:174-175 */
     int32_t early_stop;    /* 0: run max_iter iterations; 1: per frame, stop at the first k >= 0
@@ -140,8 +159,8 @@ typedef struct {
                               Ignored for F32. */
     int32_t llr_type;      /* LDPC_LLR_I16 | LDPC_LLR_I8 | LDPC_LLR_F32 */
     int32_t msg_format;    /* LDPC_MSG_COMPACT | LDPC_MSG_1BIT | LDPC_MSG_FULL (1BIT and FULL
-                              require integer LLRs).  F32 LLRs: row degree <= 16 (resident
-                              kernel: <= 8, wider codes stream); integer: row degree <= 8. */
+                              require integer LLRs).  F32 LLRs: row degree <= 16 (LAYERED:
+                              <= 8); integer: row degree <= 8. */
     int32_t schedule;      /* LDPC_SCHED_SINGLESCAN (0, default) | _TWOSCAN | _LAYERED */
     /* Optional per-iteration variants (P:179 lambda_k, P:186 beta_k): HOST arrays of
      * max_iter entries, read during the call only; NULL = the constants above.
@@ -156,6 +175,7 @@ typedef struct {
     const int32_t *offset_per_iter;
     const float   *offset_f_per_iter;
     const float   *alpha_per_iter;
+    const ldpc_tuning *tuning;   /* HOST, optional (NULL = automatic), read during the call only */
 } ldpc_decode_params;
 
 /* Device workspace bytes needed by ldpc_decode_batch for n_frames frames. */
@@ -172,16 +192,35 @@ ldpc_status ldpc_decode_workspace_size(const ldpc_code *code, int64_t n_frames,
  *   iterations_used device or NULL, [n_frames] int32: iterations run for the frame (D10)
  *   workspace    device, >= ldpc_decode_workspace_size() bytes, 256-byte aligned
  * Fully asynchronous on `stream`; all outputs are valid once the stream reaches this point.
- * Integer paths are bit-exact and reproducible; the F32 path accumulates posteriors in an
- * order that can vary run to run (fp32 sums), see DESIGN.md §3 D11.
- * Kernel choice (automatic): codes whose posterior double buffer fits in shared memory
- * decode resident (one launch; integer: a frame pair per CTA, F32: a frame per CTA, row
- * degree <= 8) when the compact state of a CTA's rows fits in the SM's Tensor Memory;
- * other codes use the streaming kernels (one launch per iteration). */
+ * Every path is deterministic: integer posteriors are exact, and F32 posteriors sum their
+ * messages exactly (int64 on the 2^-34 grid) and round once (DESIGN.md §3 D28), so outputs
+ * are bit-reproducible run to run and independent of batch composition.  F32 channel LLRs
+ * and message magnitudes saturate at +-2^20 (D28).
+ * Kernel choice (automatic, see ldpc_tuning): integer codes whose posterior double buffer
+ * fits in shared memory decode resident (one launch, a frame pair per CTA) when the compact
+ * state of a CTA's rows fits in the SM's Tensor Memory; other codes, and F32 flooding /
+ * two-scan decodes, use the streaming kernels (one launch per iteration). */
 ldpc_status ldpc_decode_batch(const ldpc_code *code, const ldpc_decode_params *params, int64_t n_frames,
                               const void *llr, uint32_t *hard_bits, void *posteriors,
                               uint8_t *syndrome_ok, int32_t *iterations_used,
                               void *workspace, size_t workspace_bytes, void *stream);
+
+/* Parity / debug export: ldpc_decode_batch plus the check messages at exit.
+ *   messages  device, [n_frames][E]: int16 (integer LLRs, raw input units) or float (F32);
+ *             entry (f, e) is L_mn of edge e = (m, n) in the CSR order of H (row_ptr[m] + j),
+ *             the message of the last iteration: for SINGLESCAN rebuilt from the row's
+ *             persistent state as the next iteration would (L_mn = s_mn f(A_m, B_m, n, ñ_m),
+ *             so the export pins A_m, B_m, s_mn and ñ_m wherever A_m != B_m),
+ *             for TWOSCAN the stored per-edge message of the last horizontal scan.
+ * Defined for frames that ran all max_iter iterations (iterations_used == max_iter); the
+ * entries of frames that stopped early are unspecified.  The same workspace as
+ * ldpc_decode_batch.  LDPC_ERR_UNSUPPORTED for the LAYERED schedule and for the batched
+ * resident kernel (tuning.path = LDPC_PATH_RESIDENT_BATCHED, or codes with
+ * 2Q(max_dv+1) >= 16384 on the resident path). */
+ldpc_status ldpc_decode_batch_messages(const ldpc_code *code, const ldpc_decode_params *params, int64_t n_frames,
+                                       const void *llr, uint32_t *hard_bits, void *posteriors,
+                                       uint8_t *syndrome_ok, int32_t *iterations_used, void *messages,
+                                       void *workspace, size_t workspace_bytes, void *stream);
 
 /* Device workspace bytes for ldpc_decode_batch_host (includes device staging of inputs/outputs). */
 ldpc_status ldpc_decode_host_workspace_size(const ldpc_code *code, int64_t n_frames,

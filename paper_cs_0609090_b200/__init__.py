@@ -23,11 +23,13 @@ LDPC_LLR_I16, LDPC_LLR_I8, LDPC_LLR_F32 = 0, 1, 2
 LDPC_MINSUM_OFFSET, LDPC_MINSUM_NORMALIZED = 0, 1
 LDPC_MSG_COMPACT, LDPC_MSG_1BIT, LDPC_MSG_FULL = 0, 1, 2
 LDPC_SCHED_SINGLESCAN, LDPC_SCHED_TWOSCAN, LDPC_SCHED_LAYERED = 0, 1, 2
+LDPC_PATH_AUTO, LDPC_PATH_STREAM, LDPC_PATH_RESIDENT_BATCHED = 0, 1, 2
 
 # every symbol include/ldpc.h declares
 EXPORTS = [
     "ldpc_code_create", "ldpc_code_destroy", "ldpc_code_query", "ldpc_decode_workspace_size",
-    "ldpc_decode_batch", "ldpc_decode_host_workspace_size", "ldpc_decode_batch_host", "ldpc_count_errors",
+    "ldpc_decode_batch", "ldpc_decode_batch_messages", "ldpc_decode_host_workspace_size", "ldpc_decode_batch_host",
+    "ldpc_count_errors",
     "ldpc_last_launch_count", "ldpc_status_string", "ldpc_last_error_detail", "ldpc_version",
 ]
 
@@ -39,6 +41,12 @@ class ldpc_code_desc(ctypes.Structure):
                 ("qc_shift", ctypes.POINTER(ctypes.c_int16))]
 
 
+class ldpc_tuning(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int32), ("resident_waves", ctypes.c_int32),
+                ("stream_chunk_tiles", ctypes.c_int32), ("stream_register_kernels", ctypes.c_int32),
+                ("host_chunks", ctypes.c_int32), ("host_streams", ctypes.c_int32)]
+
+
 class ldpc_decode_params(ctypes.Structure):
     _fields_ = [("max_iter", ctypes.c_int32), ("early_stop", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("offset_raw", ctypes.c_int32), ("offset_f", ctypes.c_float), ("alpha", ctypes.c_float),
@@ -46,7 +54,8 @@ class ldpc_decode_params(ctypes.Structure):
                 ("schedule", ctypes.c_int32),
                 ("offset_per_iter", ctypes.POINTER(ctypes.c_int32)),
                 ("offset_f_per_iter", ctypes.POINTER(ctypes.c_float)),
-                ("alpha_per_iter", ctypes.POINTER(ctypes.c_float))]
+                ("alpha_per_iter", ctypes.POINTER(ctypes.c_float)),
+                ("tuning", ctypes.POINTER(ldpc_tuning))]
 
 
 class LdpcError(RuntimeError):
@@ -77,10 +86,11 @@ def lib():
         L.ldpc_decode_workspace_size.argtypes = [vp, i64, PP, ctypes.POINTER(sz)]
         L.ldpc_decode_host_workspace_size.argtypes = [vp, i64, PP, ctypes.POINTER(sz)]
         L.ldpc_decode_batch.argtypes = [vp, PP, i64, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.ldpc_decode_batch_messages.argtypes = [vp, PP, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp]
         L.ldpc_decode_batch_host.argtypes = [vp, PP, i64, vp, vp, vp, vp, vp, vp, sz, vp]
         L.ldpc_count_errors.argtypes = [vp, i64, vp, vp, vp, vp, vp]
         for f in ("ldpc_code_create", "ldpc_code_query", "ldpc_decode_workspace_size", "ldpc_decode_host_workspace_size",
-                  "ldpc_decode_batch", "ldpc_decode_batch_host", "ldpc_count_errors"):
+                  "ldpc_decode_batch", "ldpc_decode_batch_messages", "ldpc_decode_batch_host", "ldpc_count_errors"):
             getattr(L, f).restype = ctypes.c_int
         L.ldpc_status_string.argtypes = [ctypes.c_int]
         L.ldpc_status_string.restype = ctypes.c_char_p
@@ -156,8 +166,9 @@ def ldpc_code_query(handle: int):
 def make_params(max_iter=10, early_stop=0, variant=LDPC_MINSUM_OFFSET, offset_raw=0, offset_f=0.0, alpha=1.0,
                 clamp_raw=0, llr_type=LDPC_LLR_I16, msg_format=LDPC_MSG_COMPACT,
                 schedule=None, offset_per_iter=None, offset_f_per_iter=None,
-                alpha_per_iter=None) -> ldpc_decode_params:
-    """ldpc_decode_params; the optional per-iteration arrays (max_iter entries) are kept
+                alpha_per_iter=None, tuning=None) -> ldpc_decode_params:
+    """ldpc_decode_params; the optional per-iteration arrays (max_iter entries) and the
+    optional plan overrides (``tuning``: an ldpc_tuning or a dict of its fields) are kept
     alive on the returned object."""
     import numpy as np
     sched = LDPC_SCHED_SINGLESCAN if schedule is None else int(schedule)
@@ -173,7 +184,21 @@ def make_params(max_iter=10, early_stop=0, variant=LDPC_MINSUM_OFFSET, offset_ra
                 raise ValueError(f"{name} needs max_iter = {max_iter} entries")
             p._keep.append(a)
             setattr(p, name, a.ctypes.data_as(ctypes.POINTER(ct)))
+    if tuning is not None:
+        set_tuning(p, tuning)
     return p
+
+
+def set_tuning(params: ldpc_decode_params, tuning) -> ldpc_decode_params:
+    """Attach plan overrides (include/ldpc.h ldpc_tuning) to params: an ldpc_tuning, a dict of
+    its fields, or None to clear."""
+    if tuning is None:
+        params.tuning = None
+        return params
+    t = tuning if isinstance(tuning, ldpc_tuning) else ldpc_tuning(**tuning)
+    params._tuning = t
+    params.tuning = ctypes.pointer(t)
+    return params
 
 
 def ldpc_decode_workspace_size(handle: int, n_frames: int, params: ldpc_decode_params) -> int:
@@ -198,6 +223,16 @@ def ldpc_decode_batch(handle: int, params: ldpc_decode_params, n_frames: int, ll
                                    hard_bits or None, posteriors or None, syndrome_ok or None,
                                    iterations_used or None, workspace or None, int(workspace_bytes), stream or None),
            "ldpc_decode_batch")
+
+
+def ldpc_decode_batch_messages(handle: int, params: ldpc_decode_params, n_frames: int, llr: int, hard_bits: int,
+                               posteriors: int, syndrome_ok: int, iterations_used: int, messages: int, workspace: int,
+                               workspace_bytes: int, stream: int) -> None:
+    """ldpc_decode_batch plus the exit check messages [n_frames][E] (device address)."""
+    _check(lib().ldpc_decode_batch_messages(ctypes.c_void_p(handle), ctypes.byref(params), int(n_frames), llr or None,
+                                            hard_bits or None, posteriors or None, syndrome_ok or None,
+                                            iterations_used or None, messages or None, workspace or None,
+                                            int(workspace_bytes), stream or None), "ldpc_decode_batch_messages")
 
 
 def ldpc_decode_batch_host(handle: int, params: ldpc_decode_params, n_frames: int, llr_host: int,
@@ -289,6 +324,23 @@ class Decoder:
                           out.posteriors.data_ptr() if out.posteriors is not None else 0,
                           out.syndrome_ok.data_ptr(), out.iterations.data_ptr(), ws.data_ptr(), nbytes, stream)
         return out
+
+    def decode_messages(self, llr, params: ldpc_decode_params, out: Optional[DecodeOutputs] = None):
+        """decode() plus the exit check messages: returns (outputs, messages [F][E] int16 / float32)."""
+        torch = self.torch
+        assert llr.is_cuda and llr.is_contiguous() and llr.shape[1] == self.N
+        F = llr.shape[0]
+        if out is None:
+            out = self.alloc_outputs(F, params.llr_type, True)
+        msg = torch.empty((F, self.E), dtype=torch.float32 if params.llr_type == LDPC_LLR_F32 else torch.int16,
+                          device=f"cuda:{self.device}")
+        ws, nbytes = self.workspace(F, params)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ldpc_decode_batch_messages(self.handle, params, F, llr.data_ptr(), out.hard_bits.data_ptr(),
+                                   out.posteriors.data_ptr() if out.posteriors is not None else 0,
+                                   out.syndrome_ok.data_ptr(), out.iterations.data_ptr(), msg.data_ptr(),
+                                   ws.data_ptr(), nbytes, stream)
+        return out, msg
 
     def decode_host(self, llr_host, params: ldpc_decode_params, hb_host, ok_host, it_host=None, post_host=None):
         """Host (pinned) tensors in/out; copies + decode enqueued on the current stream."""

@@ -23,6 +23,7 @@ struct QcTab {
     int32_t dc[kQcMaxSB][kQcGroups];    // its degree (0 = group idle in this super-batch)
     int32_t run_end[kQcMaxSB][kQcGroups];  // first later super-batch where the group's degree changes
     int16_t tcol[kQcMaxSB][kQcGroups];     // FMT_FULL: first TMEM column of slot b's messages in group g
+    int16_t brow[kQcMaxSB][kQcGroups];     // base row of slot b in group g (message export)
     uint2 ent[kQcMaxEnt];               // (4 * shift, 4 * (j * Z)) per base-matrix entry
 };
 
@@ -54,6 +55,11 @@ struct ResArgs {
     RegK rk;                          // register constants (simd16.cuh)
     uint32_t cpar;                    // row_parity constant (-(0x00010001), biased: -(0x40014001))
     int csr_smem, csr_dc;             // barrier-free kernel, general codes: colT rows [0, csr_dc) staged in smem
+    // message export (ldpc_decode_batch_messages): the exit messages L_mn rebuilt from each
+    // row's state, int16 [nframes][E] in CSR edge order; nullptr = no export
+    int16_t *msg_out;
+    const int32_t *row_ptr;
+    int64_t E;
 };
 
 struct StreamArgs {
@@ -76,6 +82,8 @@ struct StreamArgs {
     void *post;
     uint8_t *ok;
     int32_t *iters;
+    void *msg_out;               // message export: int16 / float [nframes][E], nullptr = none
+    int64_t E;
 };
 
 // two-scan baseline (k_twoscan.cuh): column addressing and the per-edge message planes

@@ -312,6 +312,72 @@ __device__ __forceinline__ void atom_ingest(const ResArgs &a, const TIN *__restr
     }
 }
 
+// ---------------------------------------------------------------- message export
+// Exit messages of one row for both frames of the pair, rebuilt from the persistent state
+// exactly as the next iteration would rebuild them:
+// L_mn = s_mn f(A_m, B_m, n, ñ_m), doubled values halved; written in CSR edge order.
+__device__ __forceinline__ void export_row_compact(const ResArgs &a, int m, int dc, const RowState &st, int f0,
+                                                   bool hi_valid) {
+    const int64_t e0 = __ldg(a.row_ptr + m);
+    for (int j = 0; j < dc; ++j) {
+        const int i = j >> 1, h = j & 1;
+#pragma unroll
+        for (int fr = 0; fr < 2; ++fr) {
+            if (fr == 1 && !hi_valid) break;
+            const int byte = h + 2 * fr;                       // W layout: rowcore.cuh header
+            const uint32_t wb = st.W >> (8 * byte);
+            const bool neg = (wb >> i) & 1u, isidx = (wb >> (4 + i)) & 1u;
+            const int mag = (int)(((isidx ? st.B : st.A) >> (16 * fr)) & 0xFFFFu);   // doubled magnitude
+            a.msg_out[(size_t)(f0 + fr) * a.E + e0 + j] = (int16_t)((neg ? -mag : mag) / 2);
+        }
+    }
+}
+// FMT_FULL: the stored word c = kAtomQ0 - V(2 L_mn) of each edge
+__device__ __forceinline__ void export_row_full(const ResArgs &a, int m, int dc, const uint32_t (&c)[8], int f0,
+                                                bool hi_valid) {
+    const int64_t e0 = __ldg(a.row_ptr + m);
+    for (int j = 0; j < dc; ++j) {
+        const uint32_t v = kAtomQ0 - c[j];                    // V form hi * 65536 + lo
+        const int lo = (int)(int16_t)(v & 0xFFFFu), hi = (int)((int32_t)(v - (uint32_t)lo) >> 16);
+        a.msg_out[(size_t)f0 * a.E + e0 + j] = (int16_t)(lo / 2);
+        if (hi_valid) a.msg_out[(size_t)(f0 + 1) * a.E + e0 + j] = (int16_t)(hi / 2);
+    }
+}
+// all rows of this thread (TMEM loads are warp-collective: issued whenever the slot exists
+// for the warp, results used only by threads that own a row)
+template <bool QC, int FMT>
+__device__ __forceinline__ void atom_export(const ResArgs &a, const QcTab &t, uint32_t tw, int nb, int grp, int rloc,
+                                            int f0, bool hi_valid) {
+    const int tid = threadIdx.x, nth = blockDim.x;
+    tmem_wait_st();
+    for (int b = 0; b < nb; ++b) {
+        int m = -1, dc;
+        if (QC) {
+            dc = t.dc[b][grp];
+            if (dc == 0) continue;                              // uniform over the group
+            if (rloc < a.Z) m = t.brow[b][grp] * a.Z + rloc;
+        } else {
+            const int p = b * nth + tid;
+            dc = p < a.M ? a.dcT[p] : 0;
+            if (p < a.M) m = p;
+        }
+        if constexpr (FMT == FMT_FULL) {
+            uint32_t c[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            const uint32_t col = QC ? tw + (uint32_t)t.tcol[b][grp] : tw + 8u * b;
+            const int ncol = QC ? dc : 8;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)                         // constant indices: c stays in registers
+                if (j < ncol) tmem_ld1(col + j, c[j]);
+            tmem_wait_ld_dep8(c);
+            if (m >= 0) export_row_full(a, m, dc, c, f0, hi_valid);
+        } else {
+            RowState st;
+            state_tmem_load<FMT>(tw, b, nb, st);
+            if (m >= 0) export_row_compact(a, m, dc, st, f0, hi_valid);
+        }
+    }
+}
+
 template <bool QC, bool ES, int FMT, typename TIN>
 __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(const __grid_constant__ ResArgs a,
                                                           const __grid_constant__ QcTab t) {
@@ -439,6 +505,7 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             const int which = 3 & ~done;
             if (which) res_write_outputs(a, (const uint32_t *)Lpb, f0, which, a.K, fail_lo, fail_hi, kAtomBias);
         }
+        if (a.msg_out) atom_export<QC, FMT>(a, t, tw, nb, grp, rloc, f0, hi_valid);
     }
     tmem_free_cta(tbase, a.tmem_cols);
 }

@@ -16,8 +16,9 @@
 // messages are added by a 32-bit RED as V(L) + 0x8000 (rowcore new_state<B8>) and each
 // accumulator starts d_v(n) * 0x8000 lower (the Z^(0) plane holds that start value), so
 // the sums are exact and the gathers read the words directly -- the same representation
-// as the barrier-free resident kernel (reading D26).  fp32 path: one frame per lane,
-// RED.F32.
+// as the barrier-free resident kernel (reading D26).  fp32 path: one frame per lane; the
+// posterior planes hold the exact sums of reading D28 as int64 values on the 2^-34 grid
+// (64-bit integer RED, order-free), read back as fl32(X 2^-34); the Z^(0) plane is fp32.
 #pragma once
 #include "args.cuh"
 #include "rowcore.cuh"
@@ -27,6 +28,14 @@ namespace ldpc {
 
 constexpr uint32_t kPairBias = 0x40004000u;      // 0x4000 per 16-bit lane
 constexpr uint32_t kParBiased = 0xBFFEBFFFu;     // row_parity constant for biased words
+
+// fp32 posteriors (reading D28): a sum of messages is exact on the grid 2^-34 (int64) and
+// rounded to fp32 once when read.  Terms are saturated to +-2^20 (channel LLRs on ingest,
+// message magnitudes in the row core), so the scaling by 2^34 is exact and sums of up to
+// 255 terms stay far inside int64.
+constexpr float kSatF = 1048576.0f;
+__device__ __forceinline__ long long grid_of(float x) { return __float2ll_rn(x * 0x1p34f); }
+__device__ __forceinline__ float val_of(long long X) { return __ll2float_rn(X) * 0x1p-34f; }
 
 // Early stop: frozen lanes (mask `keep`) must come out of an accumulation unchanged.
 // Every edge always adds 0x8000 to the low lane -- V(L) + 0x8000 for active lanes, a bare
@@ -195,13 +204,16 @@ __global__ void __launch_bounds__(256, 3) k_stream_iter_i(const StreamArgs a, in
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
 }
 
-// syndrome of the buffer read by iteration k (final check)
+// syndrome of the posterior after iteration k (Z^(0) for k = 0): the final check, and the
+// two-scan's per-iteration check.  fp32: Z^(0) is the fp32 plane, later posteriors the
+// int64 grid planes ([Z <= 0] = [X <= 0]).
 template <bool PAIR>
-__global__ void __launch_bounds__(256) k_stream_syndrome(const StreamArgs a, int bufidx) {
+__global__ void __launch_bounds__(256) k_stream_syndrome(const StreamArgs a, int k) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nwg = gridDim.x * (blockDim.x >> 5);
-    const uint32_t *Lp = a.Lb[bufidx];
+    const uint32_t *Lp = a.Lb[k % 3];
+    const long long *Xp = (const long long *)a.Lb[k % 3];
     uint32_t synd = 0;
     for (int m = wg; m < a.M; m += nwg) {
         const int e0 = __ldg(a.row_ptr + m), e1 = __ldg(a.row_ptr + m + 1);
@@ -209,7 +221,8 @@ __global__ void __launch_bounds__(256) k_stream_syndrome(const StreamArgs a, int
         for (int e = e0; e < e1; ++e) {
             const size_t idx = ((size_t)tile * a.N + __ldg(a.col_idx + e)) * 32 + lane;
             if (PAIR) p ^= fadd32(__ldcg(Lp + idx), kParBiased, a.rk);
-            else p ^= (__int_as_float(__ldcg(Lp + idx)) <= 0.0f) ? 1u : 0u;
+            else if (k == 0) p ^= (__uint_as_float(__ldcg(a.Z0 + idx)) <= 0.0f) ? 1u : 0u;
+            else p ^= (__ldcg(Xp + idx) <= 0) ? 1u : 0u;
         }
         synd |= PAIR ? (p & 0x80008000u) : (p & 1u);
     }
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(256) k_stream_output(const StreamArgs a) {
             } else {
                 const int f = tile * 32 + lane;
                 const int kk = f < a.nframes ? a.it_ws[f] : a.K;
-                val = __ldcg(a.Lb[kk % 3] + idx);
+                val = kk == 0 ? __ldcg(a.Z0 + idx) : __float_as_uint(val_of(__ldcg((const long long *)a.Lb[kk % 3] + idx)));
             }
         }
         sh[v][lane] = val;
@@ -300,6 +313,48 @@ __global__ void __launch_bounds__(256) k_stream_output(const StreamArgs a) {
     }
 }
 
+// Message export (ldpc_decode_batch_messages): the exit messages L_mn rebuilt from each
+// row's persistent state, one warp per (row, tile), lane = frame pair
+// (integer) or frame (fp32); messages [nframes][E] in CSR edge order (int16 raw units /
+// float).  Integer state: doubled magnitudes A, B and the byte-interleaved W of rowcore.cuh;
+// fp32 state: A, B and W = sign bits | one-hot ñ at bit 16 + position (rowcore_f32.cuh).
+template <bool PAIR, int FMT>
+__global__ void __launch_bounds__(256) k_stream_export(const StreamArgs a) {
+    const int tile = blockIdx.y, lane = threadIdx.x & 31;
+    const int nst = PAIR ? StateIO<FMT>::kWords : 3;
+    const uint32_t *stt = a.st + (size_t)tile * nst * a.M * 32;
+    const size_t ss = (size_t)a.M * 32;
+    const int nwg = gridDim.x * (blockDim.x >> 5);
+    for (int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); m < a.M; m += nwg) {
+        const int64_t e0 = __ldg(a.row_ptr + m);
+        const int dc = __ldg(a.row_ptr + m + 1) - (int)e0;
+        if (PAIR) {
+            const RowState st = StateIO<FMT>::load(stt + lane, ss, (size_t)m * 32);
+            for (int fr = 0; fr < 2; ++fr) {
+                const int f = tile * 64 + 2 * lane + fr;
+                if (f >= a.nframes) break;
+                int16_t *out = (int16_t *)a.msg_out + (size_t)f * a.E + e0;
+                for (int j = 0; j < dc; ++j) {
+                    const uint32_t wb = st.W >> (8 * ((j & 1) + 2 * fr));
+                    const bool neg = (wb >> (j >> 1)) & 1u, isidx = (wb >> (4 + (j >> 1))) & 1u;
+                    const int mag = (int)(((isidx ? st.B : st.A) >> (16 * fr)) & 0xFFFFu);
+                    out[j] = (int16_t)((neg ? -mag : mag) / 2);
+                }
+            }
+        } else {
+            const int f = tile * 32 + lane;
+            if (f >= a.nframes) continue;
+            const size_t so = (size_t)m * 32 + lane;
+            const uint32_t A = __ldcg(stt + so), B = __ldcg(stt + ss + so), W = __ldcg(stt + 2 * ss + so);
+            float *out = (float *)a.msg_out + (size_t)f * a.E + e0;
+            for (int j = 0; j < dc; ++j) {
+                const uint32_t mag = ((W >> (16 + j)) & 1u) ? B : A;
+                out[j] = __uint_as_float(mag ^ (((W >> j) & 1u) << 31));
+            }
+        }
+    }
+}
+
 // frames not frozen by early stop: iterations = K, ok from the final syndrome
 template <bool PAIR>
 __global__ void k_stream_finalize_flags(const StreamArgs a) {
@@ -318,6 +373,8 @@ __global__ void k_stream_finalize_flags(const StreamArgs a) {
 }
 
 // -------------------------------------------------------------- fp32 path
+// ingest: Z^(0) plane (fp32, saturated to +-2^20 and -0.0 -> +0.0, readings D13, D28) and the
+// accumulator of iteration 1 (Lb[1] = grid(Z^(0))); iteration 1 reads the fp32 plane itself
 __global__ void k_stream_ingest_f(const StreamArgs a) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int f = tile * 32 + lane;
@@ -325,21 +382,44 @@ __global__ void k_stream_ingest_f(const StreamArgs a) {
     for (int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < a.N; n += gridDim.x * (blockDim.x >> 5)) {
         float z = 0.0f;
         if (f < a.nframes) z = llr[(size_t)f * a.N + n];
-        z = z + 0.0f;                                   // canonicalise -0.0 (reading D13)
-        const uint32_t v = __float_as_uint(z);
+        z = fminf(fmaxf(z + 0.0f, -kSatF), kSatF);
         const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
-        a.Z0[idx] = v;
-        a.Lb[0][idx] = v;
-        a.Lb[1][idx] = v;
+        a.Z0[idx] = __float_as_uint(z);
+        ((long long *)a.Lb[1])[idx] = grid_of(z);
+    }
+}
+
+// Accumulator start of the next iteration, X = grid(Z^(0)), for a tile with no frozen frame:
+// 4 fp32 values in, 4 int64 out per thread (contiguous [n][32] plane segment of the tile).
+__device__ __forceinline__ void stream_init_next_f(const uint32_t *Z0t, long long *Xnt, int N, int wg, int nwg,
+                                                   int lane) {
+    const uint4 *src = (const uint4 *)Z0t;
+    longlong2 *dst = (longlong2 *)Xnt;
+    const int total = N * 8;
+    const int step = nwg * 32;
+    for (int i = wg * 32 + lane; i < total; i += step) {
+        const uint4 v = __ldcg(src + i);
+        __stcg(dst + 2 * i, make_longlong2(grid_of(__uint_as_float(v.x)), grid_of(__uint_as_float(v.y))));
+        __stcg(dst + 2 * i + 1, make_longlong2(grid_of(__uint_as_float(v.z)), grid_of(__uint_as_float(v.w))));
+    }
+}
+// the same per lane, skipping frozen frames (early stop: their buffers keep the exit posterior)
+__device__ __forceinline__ void stream_init_next_f_lanes(const uint32_t *Z0t, long long *Xnt, int N, int wg, int nwg,
+                                                         int lane, bool frozen) {
+    if (frozen) return;
+    for (int n = wg; n < N; n += nwg) {
+        const size_t idx = (size_t)n * 32 + lane;
+        __stcg(Xnt + idx, grid_of(__uint_as_float(__ldcg(Z0t + idx))));
     }
 }
 
 // NR rows, one frame per lane, fp32 (reading D11: one RN rounding per operation,
-// no FMA contraction: __fsub_rn / __fmul_rn).  All loads issued before any compute.
+// no FMA contraction: __fsub_rn / __fmul_rn; reading D28: exact int64 accumulation).
+// All loads issued before any compute.  Iteration 1 reads the fp32 Z^(0) plane.
 template <int DC, int NR, bool ES>
 __device__ __forceinline__ void stream_rows_f(const StreamArgs &a, int lane, const int (&m)[NR], const RowT *rt,
-                                              const float *Lpt, float *Lat, uint32_t *stt, bool first_iter,
-                                              bool frozen, uint32_t &synd) {
+                                              const uint32_t *Z0t, const long long *Xpt, long long *Xat,
+                                              uint32_t *stt, bool first_iter, bool frozen, uint32_t &synd) {
     uint32_t off[NR][DC];
 #pragma unroll
     for (int r = 0; r < NR; ++r)
@@ -365,7 +445,8 @@ __device__ __forceinline__ void stream_rows_f(const StreamArgs &a, int lane, con
 #pragma unroll
     for (int r = 0; r < NR; ++r)
 #pragma unroll
-        for (int j = 0; j < DC; ++j) L[r][j] = __ldcg(Lpt + off[r][j]);
+        for (int j = 0; j < DC; ++j)
+            L[r][j] = first_iter ? __uint_as_float(__ldcg(Z0t + off[r][j])) : val_of(__ldcg(Xpt + off[r][j]));
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
         if (ES) {
@@ -384,43 +465,38 @@ __device__ __forceinline__ void stream_rows_f(const StreamArgs &a, int lane, con
         __stcg(stt + 2 * ss + so, Wn);
         if (!frozen) {
 #pragma unroll
-            for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], rr[j]);   // Z^(k)_n += L^(k)_mn
+            for (int j = 0; j < DC; ++j)                                          // Z^(k)_n += L^(k)_mn (exact)
+                atomicAdd((unsigned long long *)(Xat + off[r][j]), (unsigned long long)grid_of(rr[j]));
         }
     }
 }
 
 template <int NR, bool ES>
 __device__ __forceinline__ void stream_dispatch_f(int dc, const StreamArgs &a, int lane, const int (&m)[NR],
-                                                  const RowT *rt, const float *Lpt, float *Lat, uint32_t *stt,
-                                                  bool first_iter, bool frozen, uint32_t &synd) {
+                                                  const RowT *rt, const uint32_t *Z0t, const long long *Xpt,
+                                                  long long *Xat, uint32_t *stt, bool first_iter, bool frozen,
+                                                  uint32_t &synd) {
     switch (dc) {
-    case 2: stream_rows_f<2, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 3: stream_rows_f<3, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 4: stream_rows_f<4, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 5: stream_rows_f<5, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 6: stream_rows_f<6, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 7: stream_rows_f<7, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 8: stream_rows_f<8, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 9: stream_rows_f<9, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 10: stream_rows_f<10, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 11: stream_rows_f<11, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 12: stream_rows_f<12, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 13: stream_rows_f<13, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 14: stream_rows_f<14, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 15: stream_rows_f<15, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
-    case 16: stream_rows_f<16, NR, ES>(a, lane, m, rt, Lpt, Lat, stt, first_iter, frozen, synd); break;
+#define LDPC_SF(D) \
+    case D: stream_rows_f<D, NR, ES>(a, lane, m, rt, Z0t, Xpt, Xat, stt, first_iter, frozen, synd); break;
+    LDPC_SF(2) LDPC_SF(3) LDPC_SF(4) LDPC_SF(5) LDPC_SF(6) LDPC_SF(7) LDPC_SF(8) LDPC_SF(9) LDPC_SF(10)
+    LDPC_SF(11) LDPC_SF(12) LDPC_SF(13) LDPC_SF(14) LDPC_SF(15) LDPC_SF(16)
+#undef LDPC_SF
     }
 }
 
+// Register version of the fp32 iteration kernel (rows of degree 9..16; the pipelined
+// kernel takes rows of degree <= 8)
 template <bool ES>
 __global__ void __launch_bounds__(256, 4) k_stream_iter_f(const StreamArgs a, int k) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nwg = gridDim.x * (blockDim.x >> 5);
     const size_t plane = (size_t)tile * a.N * 32;
-    const float *Lpt = (const float *)a.Lb[(k - 1) % 3] + plane;
-    float *Lat = (float *)a.Lb[k % 3] + plane;
-    uint32_t *Lnt = a.Lb[(k + 1) % 3] + plane;
+    const uint32_t *Z0t = a.Z0 + plane;
+    const long long *Xpt = (const long long *)a.Lb[(k - 1) % 3] + plane;
+    long long *Xat = (long long *)a.Lb[k % 3] + plane;
+    long long *Xnt = (long long *)a.Lb[(k + 1) % 3] + plane;
     uint32_t *stt = a.st + (size_t)tile * 3 * a.M * 32;
     bool frozen = false;
     if (ES) {
@@ -428,14 +504,8 @@ __global__ void __launch_bounds__(256, 4) k_stream_iter_f(const StreamArgs a, in
         if (__all_sync(0xFFFFFFFFu, frozen)) return;
     }
     if (k < a.K) {
-        if (!ES || !__any_sync(0xFFFFFFFFu, frozen)) {
-            stream_init_next(a.Z0 + plane, Lnt, a.N, wg, nwg, lane);
-        } else {
-            for (int n = wg; n < a.N; n += nwg) {
-                const size_t idx = (size_t)n * 32 + lane;
-                if (!frozen) __stcg(Lnt + idx, __ldcg(a.Z0 + plane + idx));
-            }
-        }
+        if (!ES || !__any_sync(0xFFFFFFFFu, frozen)) stream_init_next_f(Z0t, Xnt, a.N, wg, nwg, lane);
+        else stream_init_next_f_lanes(Z0t, Xnt, a.N, wg, nwg, lane, frozen);
     }
     uint32_t synd = 0;
     const bool first_iter = (k == 1);
@@ -444,7 +514,7 @@ __global__ void __launch_bounds__(256, 4) k_stream_iter_f(const StreamArgs a, in
         int dc = rt.dc;
         if (dc == 15) dc = __ldg(a.row_ptr + m + 1) - __ldg(a.row_ptr + m);
         const int mm[1] = {m};
-        stream_dispatch_f<1, ES>(dc, a, lane, mm, &rt, Lpt, Lat, stt, first_iter, frozen, synd);
+        stream_dispatch_f<1, ES>(dc, a, lane, mm, &rt, Z0t, Xpt, Xat, stt, first_iter, frozen, synd);
     }
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
 }

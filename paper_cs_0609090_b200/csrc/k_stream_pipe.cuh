@@ -22,10 +22,21 @@ namespace ldpc {
 #ifndef LDPC_PIPE_RB
 #define LDPC_PIPE_RB 64
 #endif
+#ifndef LDPC_PIPE_DF
+#define LDPC_PIPE_DF 3
+#endif
 constexpr int kPipeRB = LDPC_PIPE_RB;   // rows per CTA
 constexpr int kPipeWarps = 8;      // warps per CTA
-constexpr int kPipeD = LDPC_PIPE_D;     // rows in flight per warp
-constexpr int kPipeLines = 11;     // 8 posterior lines + up to 3 state lines per row
+// Ring slot of one row.  Integer pairs: 8 posterior lines (one 128-byte line of 32 lanes per
+// variable) + up to 3 state lines, kPipeD rows in flight.  fp32 (reading D28): a posterior is
+// an int64 grid value, two lines per variable: 16 + 3 lines, kPipeDF rows in flight (the
+// first iteration reads the fp32 Z^(0) plane, one line per variable).
+template <bool PAIR> struct PipeCfg {
+    static constexpr int LPV = PAIR ? 1 : 2;          // lines per variable (later iterations)
+    static constexpr int SB = 8 * LPV;                // first state line
+    static constexpr int LINES = SB + 3;
+    static constexpr int D = PAIR ? LDPC_PIPE_D : LDPC_PIPE_DF;
+};
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -34,27 +45,23 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Issue the copies of one row's lines into a slot: lines 0..dc-1 are posterior lines
-// (variable col[l] of this tile), lines 8..8+nst-1 the state words of row m.
-__device__ __forceinline__ void pipe_issue_row(uint32_t slot, const uint32_t *Lpt, const uint32_t *stt, size_t sstride,
+// Issue the copies of one row's lines into a slot: posterior lines 0 .. dc*LPV-1 (variable
+// col[l / LPV], 128-byte half l % LPV of its LPV*128-byte tile segment), state lines SB ..
+// SB+nst-1 (the state words of row m).  Lane handles 16-byte chunk (lane & 7) of lines
+// (lane >> 3) + 4 s; branch-free source selection, predicated copies.
+template <int LPV, int SB>
+__device__ __forceinline__ void pipe_issue_row(uint32_t slot, const char *Lpt, const uint32_t *stt, size_t sstride,
                                                const uint32_t *cols, int dc, int nst, int m, int lane) {
-    // lane handles 16-byte chunk (lane & 7) of lines (lane >> 3) + {0, 4, 8}; branch-free
-    // source selection, predicated copies (lines 0..dc-1 posterior, 8.. state).
     const int chunk = lane & 7, l0 = lane >> 3;
-    const char *sbase = (const char *)(stt + (size_t)m * 32) + chunk * 16;
 #pragma unroll
-    for (int step = 0; step < 3; ++step) {
+    for (int step = 0; step < 2 * LPV; ++step) {         // posterior lines
         const int l = l0 + 4 * step;
-        const char *src;
-        bool on;
-        if (step < 2) {                                  // lines 0..7: posterior lines
-            on = l < dc;
-            src = (const char *)(Lpt + (size_t)cols[l] * 32) + chunk * 16;
-        } else {                                         // lines 8..10: state words
-            on = l - 8 < nst;
-            src = sbase + (size_t)(l - 8) * sstride * 4;
-        }
-        if (on) cp_async16(slot + (uint32_t)(l * 128 + chunk * 16), src);
+        const char *src = Lpt + (size_t)cols[l / LPV] * (128 * LPV) + (l % LPV) * 128 + chunk * 16;
+        if (l < dc * LPV) cp_async16(slot + (uint32_t)(l * 128 + chunk * 16), src);
+    }
+    if (l0 < nst) {                                        // state lines
+        const char *src = (const char *)(stt + (size_t)m * 32) + chunk * 16 + (size_t)l0 * sstride * 4;
+        cp_async16(slot + (uint32_t)((SB + l0) * 128 + chunk * 16), src);
     }
 }
 
@@ -91,13 +98,17 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
     for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, red_value(rn[j], keep));
 }
 
-template <int DC, bool ES>
+// fp32 row (reading D11 arithmetic, D28 exact accumulation): posteriors from the ring
+// (FI: fp32 Z^(0) lines; later: int64 grid values, rounded to fp32 here)
+template <int DC, bool ES, bool FI>
 __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *sl, const uint32_t *cols, int m,
-                                           int lane, float *Lat, uint32_t *stt, size_t ss, bool first_iter,
-                                           bool frozen, uint32_t &synd) {
+                                           int lane, long long *Xat, uint32_t *stt, size_t ss, bool frozen,
+                                           uint32_t &synd) {
+    constexpr int SB = PipeCfg<false>::SB;
     float L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = __uint_as_float(sl[j * 32 + lane]);
+    for (int j = 0; j < DC; ++j)
+        L[j] = FI ? __uint_as_float(sl[j * 32 + lane]) : val_of(((const long long *)sl)[j * 32 + lane]);
     if (ES) {
         uint32_t p = 0;
 #pragma unroll
@@ -106,26 +117,30 @@ __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *
     }
     float A0 = 0.f, B0 = 0.f;
     uint32_t W0 = 0;
-    if (!first_iter) {
-        A0 = __uint_as_float(sl[8 * 32 + lane]);
-        B0 = __uint_as_float(sl[9 * 32 + lane]);
-        W0 = sl[10 * 32 + lane];
+    if (!FI) {
+        A0 = __uint_as_float(sl[SB * 32 + lane]);
+        B0 = __uint_as_float(sl[(SB + 1) * 32 + lane]);
+        W0 = sl[(SB + 2) * 32 + lane];
     }
     float A, B, r[DC];
     uint32_t Wn;
-    f32_row<DC>(L, first_iter, A0, B0, W0, a.alpha, a.beta, A, B, Wn, r);
+    f32_row<DC>(L, FI, A0, B0, W0, a.alpha, a.beta, A, B, Wn, r);
     const size_t so = (size_t)m * 32 + lane;
     __stcg(stt + so, __float_as_uint(A));
     __stcg(stt + ss + so, __float_as_uint(B));
     __stcg(stt + 2 * ss + so, Wn);
     if (!frozen) {
 #pragma unroll
-        for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, r[j]);   // Z^(k)_n += L^(k)_mn
+        for (int j = 0; j < DC; ++j)                                      // Z^(k)_n += L^(k)_mn, exact
+            atomicAdd((unsigned long long *)(Xat + (size_t)cols[j] * 32 + lane), (unsigned long long)grid_of(r[j]));
     }
 }
 
 template <bool PAIR, int FMT, bool ES, bool FI, int VM>
 __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
+    using C = PipeCfg<PAIR>;
+    // first fp32 iteration: one line per variable (the fp32 Z^(0) plane), no state
+    constexpr int LPV = (!PAIR && FI) ? 1 : C::LPV;
     extern __shared__ __align__(128) uint32_t psm[];
     uint32_t *coltab = psm;                                       // [RB][8]
     uint8_t *dctab = (uint8_t *)(psm + kPipeRB * 8);              // [RB]
@@ -134,9 +149,14 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
     const int mb0 = blockIdx.x * kPipeRB;
     const int nrows = min(kPipeRB, a.M - mb0);
     const size_t plane = (size_t)tile * a.N * 32;
+    // integer pairs: biased 32-bit words; fp32: int64 grid values (Z^(0): fp32 plane)
     const uint32_t *Lpt = a.Lb[(k - 1) % 3] + plane;
     uint32_t *Lat = a.Lb[k % 3] + plane;
     uint32_t *Lnt = a.Lb[(k + 1) % 3] + plane;
+    long long *Xat = (long long *)a.Lb[k % 3] + plane;
+    long long *Xnt = (long long *)a.Lb[(k + 1) % 3] + plane;
+    const char *Lsrc = PAIR ? (const char *)Lpt
+                            : (FI ? (const char *)(a.Z0 + plane) : (const char *)((const long long *)a.Lb[(k - 1) % 3] + plane));
     const int nst = PAIR ? StateIO<FMT>::kWords : 3;
     uint32_t *stt = a.st + (size_t)tile * nst * a.M * 32;
     const size_t sstride = (size_t)a.M * 32;
@@ -165,76 +185,71 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
     // launch: no barrier needed)
     if (k < a.K) {
         const int wg = blockIdx.x * kPipeWarps + warp, nwg = gridDim.x * kPipeWarps;
-        if (!ES || !__any_sync(0xFFFFFFFFu, keep != 0 || frozen)) {
+        const bool any_frozen = ES && __any_sync(0xFFFFFFFFu, keep != 0 || frozen);
+        if (!PAIR) {
+            if (!any_frozen) stream_init_next_f(a.Z0 + plane, Xnt, a.N, wg, nwg, lane);
+            else stream_init_next_f_lanes(a.Z0 + plane, Xnt, a.N, wg, nwg, lane, frozen);
+        } else if (!any_frozen) {
             stream_init_next(a.Z0 + plane, Lnt, a.N, wg, nwg, lane);
         } else {
             for (int n = wg; n < a.N; n += nwg) {
                 const size_t idx = (size_t)n * 32 + lane;
-                if (PAIR) {
-                    uint32_t v = __ldcg(a.Z0 + plane + idx);
-                    if (keep) v = keep_start(v, __ldcg(Lnt + idx), keep, (uint32_t)__ldg(a.coldeg + n));
-                    __stcg(Lnt + idx, v);
-                } else if (!frozen) {
-                    __stcg(Lnt + idx, __ldcg(a.Z0 + plane + idx));
-                }
+                uint32_t v = __ldcg(a.Z0 + plane + idx);
+                if (keep) v = keep_start(v, __ldcg(Lnt + idx), keep, (uint32_t)__ldg(a.coldeg + n));
+                __stcg(Lnt + idx, v);
             }
         }
     }
     __syncwarp();
     constexpr bool first_iter = FI;                   // compile-time: no rebuild / state copy in iteration 1
     const int nst_copy = first_iter ? 0 : nst;
-    uint32_t *wring = ring + (size_t)warp * kPipeD * kPipeLines * 32;
+    constexpr int D = C::D, LINES = C::LINES;
+    uint32_t *wring = ring + (size_t)warp * D * LINES * 32;
     const uint32_t wring_s = (uint32_t)__cvta_generic_to_shared(wring);
     // rows of this warp: warp, warp + W, ...
     int nmy = 0;
     for (int r = warp; r < nrows; r += kPipeWarps) ++nmy;
     // prologue
 #pragma unroll
-    for (int i = 0; i < kPipeD; ++i) {
+    for (int i = 0; i < D; ++i) {
         if (i < nmy) {
             const int r = warp + i * kPipeWarps;
-            pipe_issue_row(wring_s + (uint32_t)(i * kPipeLines * 128), Lpt, stt, sstride, coltab + r * 8, dctab[r],
-                           nst_copy, mb0 + r, lane);
+            pipe_issue_row<LPV, C::SB>(wring_s + (uint32_t)(i * LINES * 128), Lsrc, stt, sstride, coltab + r * 8,
+                                       dctab[r], nst_copy, mb0 + r, lane);
         }
         cp_async_commit();
     }
     uint32_t synd = 0;
     for (int i = 0; i < nmy; ++i) {
-        cp_async_wait<kPipeD - 1>();
+        cp_async_wait<D - 1>();
         __syncwarp();
         const int r = warp + i * kPipeWarps;
         const int m = mb0 + r;
-        const int slot = i % kPipeD;
-        const uint32_t *sl = wring + slot * kPipeLines * 32;
+        const int slot = i % D;
+        const uint32_t *sl = wring + slot * LINES * 32;
         const uint32_t *cols = coltab + r * 8;
         const int dc = dctab[r];
         if (PAIR) {
             switch (dc) {
-            case 2: pipe_row_i<2, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 3: pipe_row_i<3, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 4: pipe_row_i<4, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 5: pipe_row_i<5, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 6: pipe_row_i<6, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 7: pipe_row_i<7, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            case 8: pipe_row_i<8, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+#define LDPC_PI(DD) \
+            case DD: pipe_row_i<DD, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+            LDPC_PI(2) LDPC_PI(3) LDPC_PI(4) LDPC_PI(5) LDPC_PI(6) LDPC_PI(7) LDPC_PI(8)
+#undef LDPC_PI
             }
         } else {
             switch (dc) {
-            case 2: pipe_row_f<2, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
-            case 3: pipe_row_f<3, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
-            case 4: pipe_row_f<4, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
-            case 5: pipe_row_f<5, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
-            case 6: pipe_row_f<6, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
-            case 7: pipe_row_f<7, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
-            case 8: pipe_row_f<8, ES>(a, sl, cols, m, lane, (float *)Lat, stt, sstride, first_iter, frozen, synd); break;
+#define LDPC_PF(DD) \
+            case DD: pipe_row_f<DD, ES, FI>(a, sl, cols, m, lane, Xat, stt, sstride, frozen, synd); break;
+            LDPC_PF(2) LDPC_PF(3) LDPC_PF(4) LDPC_PF(5) LDPC_PF(6) LDPC_PF(7) LDPC_PF(8)
+#undef LDPC_PF
             }
         }
         __syncwarp();                                          // slot consumed before it is refilled
-        const int inext = i + kPipeD;
+        const int inext = i + D;
         if (inext < nmy) {
             const int rn = warp + inext * kPipeWarps;
-            pipe_issue_row(wring_s + (uint32_t)(slot * kPipeLines * 128), Lpt, stt, sstride, coltab + rn * 8,
-                           dctab[rn], nst_copy, mb0 + rn, lane);
+            pipe_issue_row<LPV, C::SB>(wring_s + (uint32_t)(slot * LINES * 128), Lsrc, stt, sstride, coltab + rn * 8,
+                                       dctab[rn], nst_copy, mb0 + rn, lane);
         }
         cp_async_commit();
     }
@@ -262,8 +277,9 @@ __global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe
     }
 }
 
-inline size_t pipe_smem_bytes() {
-    return (size_t)kPipeRB * 8 * 4 + kPipeRB + (size_t)kPipeWarps * kPipeD * kPipeLines * 128 + 64;
+template <bool PAIR>
+constexpr size_t pipe_smem_bytes() {
+    return (size_t)kPipeRB * 8 * 4 + kPipeRB + (size_t)kPipeWarps * PipeCfg<PAIR>::D * PipeCfg<PAIR>::LINES * 128 + 64;
 }
 
 }  // namespace ldpc

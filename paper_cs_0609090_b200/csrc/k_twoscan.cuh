@@ -18,9 +18,10 @@
 // syndrome / freeze / output kernels are shared.
 //
 // Reading (DESIGN.md §3 D24): the extrinsic Z_mn is computed as Z_n - L_mn.  In the
-// integer modes this equals Eq.(2)'s Z0_n + sum_{m' != m} L_m'n exactly; in fp32 it is
-// one rounding away from the ordered sum (checked against the oracle's Eq.(2) within
-// the BASELINE fp32 tolerance).
+// integer modes this equals Eq.(2)'s Z0_n + sum_{m' != m} L_m'n exactly.  fp32 (reading
+// D28): the column's sum is exact in int64 on the 2^-34 grid, so Z_n - L_mn is the exact
+// sum over m' != m too, each rounded to fp32 once -- bit-exact with the oracle's Eq.(2);
+// the posterior planes hold the int64 sums like the fp32 single-scan's.
 #pragma once
 #include "k_stream.cuh"
 
@@ -53,7 +54,7 @@ __device__ __forceinline__ void ts_store_hb(const StreamArgs &a, uint32_t *hbt, 
         const uint32_t hi = __ballot_sync(0xFFFFFFFFu, (p & 0x80000000u) != 0);
         if (lane == 0) ((uint2 *)hbt)[n] = make_uint2(lo, hi);
     } else {
-        const uint32_t h = __ballot_sync(0xFFFFFFFFu, __uint_as_float(out) <= 0.0f);
+        const uint32_t h = __ballot_sync(0xFFFFFFFFu, out != 0u);   // fp32: out = [Z <= 0]
         if (lane == 0) hbt[n] = h;
     }
 }
@@ -155,14 +156,18 @@ __device__ __forceinline__ void ts_var_col(const StreamArgs &a, const TwoScanArg
         __stcg(post + ni, out);
         if (ES) ts_store_hb<true>(a, hbt, n, out, lane);
     } else {
-        float Zf = __uint_as_float(Z);
+        long long g[DV];
+        long long X = grid_of(__uint_as_float(Z));                     // exact sums (reading D28)
 #pragma unroll
-        for (int b = 0; b < DV; ++b) Zf = __fadd_rn(Zf, __uint_as_float(mv[b]));          // ascending m
+        for (int b = 0; b < DV; ++b) {
+            g[b] = grid_of(__uint_as_float(mv[b]));
+            X += g[b];                                                 // Z_n
+        }
 #pragma unroll
-        for (int b = 0; b < DV; ++b)
-            __stcg(zvt + (size_t)eid[b] * 32 + lane, __float_as_uint(__fsub_rn(Zf, __uint_as_float(mv[b]))));
-        if (!(ES && keep)) __stcg(post + ni, __float_as_uint(Zf));
-        if (ES) ts_store_hb<false>(a, hbt, n, __float_as_uint(Zf), lane);
+        for (int b = 0; b < DV; ++b)                                   // Eq.(2): sum over m' != m
+            __stcg(zvt + (size_t)eid[b] * 32 + lane, __float_as_uint(val_of(X - g[b])));
+        if (!(ES && keep)) __stcg((long long *)post + ni, X);
+        if (ES) ts_store_hb<false>(a, hbt, n, X <= 0 ? 1u : 0u, lane);
     }
 }
 
@@ -174,17 +179,17 @@ __device__ __noinline__ void ts_var_col_wide(const StreamArgs &a, const TwoScanA
                                              int b0, int dv, int lane, uint32_t keep) {
     const size_t ni = (size_t)n * 32 + lane;
     uint32_t Z = __ldcg(z0t + ni);
-    float Zf = __uint_as_float(Z);
+    long long X = PAIR ? 0 : grid_of(__uint_as_float(Z));               // fp32: exact sums (D28)
     if (PAIR) Z = vadd(Z, 0xC000C000u);
     for (int b = 0; b < dv; ++b) {
         const uint32_t m = __ldcg(msgt + (size_t)__ldg(t.vedge + b0 + b) * 32 + lane);
         if (PAIR) Z = vadd(Z, m);
-        else Zf = __fadd_rn(Zf, __uint_as_float(m));                      // ascending m
+        else X += grid_of(__uint_as_float(m));
     }
     for (int b = 0; b < dv; ++b) {
         const size_t ei = (size_t)__ldg(t.vedge + b0 + b) * 32 + lane;
         const uint32_t m = __ldcg(msgt + ei);
-        __stcg(zvt + ei, PAIR ? vadd(Z, vneg(m, a.rk)) : __float_as_uint(__fsub_rn(Zf, __uint_as_float(m))));
+        __stcg(zvt + ei, PAIR ? vadd(Z, vneg(m, a.rk)) : __float_as_uint(val_of(X - grid_of(__uint_as_float(m)))));
     }
     if (PAIR) {
         uint32_t out = vadd(Z, kPairBias);
@@ -192,8 +197,8 @@ __device__ __noinline__ void ts_var_col_wide(const StreamArgs &a, const TwoScanA
         __stcg(post + ni, out);
         if (ES) ts_store_hb<true>(a, hbt, n, out, lane);
     } else {
-        if (!(ES && keep)) __stcg(post + ni, __float_as_uint(Zf));
-        if (ES) ts_store_hb<false>(a, hbt, n, __float_as_uint(Zf), lane);
+        if (!(ES && keep)) __stcg((long long *)post + ni, X);
+        if (ES) ts_store_hb<false>(a, hbt, n, X <= 0 ? 1u : 0u, lane);
     }
 }
 
@@ -208,7 +213,9 @@ __global__ void __launch_bounds__(256) k_ts_var(const StreamArgs a, const TwoSca
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const uint32_t *msgt = t.msg + (size_t)tile * t.E * 32;
     uint32_t *zvt = t.zv + (size_t)tile * t.E * 32;
-    uint32_t *post = a.Lb[k % 3] + (size_t)tile * a.N * 32;
+    // integer pairs: biased words; fp32: int64 grid sums (ts_var_col casts)
+    uint32_t *post = PAIR ? a.Lb[k % 3] + (size_t)tile * a.N * 32
+                          : (uint32_t *)((long long *)a.Lb[k % 3] + (size_t)tile * a.N * 32);
     const uint32_t *z0t = a.Z0 + (size_t)tile * a.N * 32;
     uint32_t *hbt = t.hb + (size_t)tile * a.N * (PAIR ? 2 : 1);
     uint32_t keep = 0;
@@ -234,6 +241,26 @@ __global__ void __launch_bounds__(256) k_ts_var(const StreamArgs a, const TwoSca
             }
         }
 #undef LDPC_TS_COL
+    }
+}
+
+// Message export (ldpc_decode_batch_messages): the check messages L_mn of the last
+// horizontal scan, [tile][E][32] -> [nframes][E] (integer: doubled 16x2 pairs, halved)
+template <bool PAIR>
+__global__ void __launch_bounds__(256) k_ts_export(const StreamArgs a, const TwoScanArgs t) {
+    const int tile = blockIdx.y, lane = threadIdx.x & 31;
+    const uint32_t *msgt = t.msg + (size_t)tile * t.E * 32;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < t.E; e += nw) {
+        const uint32_t v = __ldcg(msgt + e * 32 + lane);
+        if (PAIR) {
+            const int f = tile * 64 + 2 * lane;
+            if (f < a.nframes) ((int16_t *)a.msg_out)[(size_t)f * t.E + e] = (int16_t)(lo16(v) / 2);
+            if (f + 1 < a.nframes) ((int16_t *)a.msg_out)[(size_t)(f + 1) * t.E + e] = (int16_t)(hi16(v) / 2);
+        } else {
+            const int f = tile * 32 + lane;
+            if (f < a.nframes) ((float *)a.msg_out)[(size_t)f * t.E + e] = __uint_as_float(v);
+        }
     }
 }
 

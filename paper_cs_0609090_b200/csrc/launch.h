@@ -9,9 +9,8 @@ namespace ldpc {
 // Resident kernels.  i8 selects int8 channel LLRs (else int16).  kind: RES_BATCHED
 // (k_resident.cuh, flooding in conflict-free batches), RES_LAYERED (k_resident.cuh,
 // in-place schedule), RES_ATOM (k_resident_atom.cuh, flooding with shared atomics),
-// RES_F32 (k_resident_f32.cuh, fp32 LLRs, one frame per CTA), RES_F32_LAY (the same with the
-// layered schedule).
-enum { RES_BATCHED = 0, RES_LAYERED = 1, RES_ATOM = 2, RES_F32 = 3, RES_F32_LAY = 4 };
+// RES_F32_LAY (k_resident_f32.cuh, fp32 LLRs, layered schedule, one frame per CTA).
+enum { RES_BATCHED = 0, RES_LAYERED = 1, RES_ATOM = 2, RES_F32_LAY = 4 };
 cudaError_t res_occupancy(bool qc, bool es, int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,
                           int threads, int *blocks);
 cudaError_t res_launch(bool qc, bool es, int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,
@@ -25,6 +24,7 @@ struct StreamRun {
     bool es;              // per-frame early stop
     int max_iter, max_dc, ntiles;
     int chunk_tiles;      // tiles decoded together through all iterations (0 = all)
+    bool register_kernels;  // integer / fp32 rows of degree <= 8: register kernels instead of the pipeline
     size_t flags_bytes;   // bytes from a.synd to the end of the per-tile flag words (zeroed first)
     // per-iteration variants (host arrays of max_iter entries, NULL = the constants in a)
     const VarK *vk_sched;

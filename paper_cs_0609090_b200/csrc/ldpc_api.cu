@@ -324,6 +324,7 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                     const int i = g < groups ? rows[g] : -1;
                     t.e0[b][g] = i >= 0 ? rstart[i] : 0;
                     t.dc[b][g] = i >= 0 ? (int)cols[i].size() : 0;
+                    t.brow[b][g] = (int16_t)(i >= 0 ? i : 0);
                 }
             }
             for (int g = 0; g < kQcGroups; ++g)
@@ -351,6 +352,7 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                         const int r = rows[g];
                         u.e0[nsb][g] = r >= 0 ? rstart[r] : 0;
                         u.dc[nsb][g] = r >= 0 ? (int)cols[r].size() : 0;
+                        u.brow[nsb][g] = (int16_t)(r >= 0 ? r : 0);
                     }
                     ++nsb;
                     i += j >= 0 ? 2 : 1;
@@ -388,6 +390,7 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                         const int r = (g < groups && b < (int)lists[g].size()) ? lists[g][b] : -1;
                         u.e0[b][g] = r >= 0 ? rstart[r] : 0;
                         u.dc[b][g] = r >= 0 ? (int)cols[r].size() : 0;
+                        u.brow[b][g] = (int16_t)(r >= 0 ? r : 0);
                     }
                 u.nsb = nsb;
                 for (int g = 0; g < kQcGroups; ++g)
@@ -551,6 +554,7 @@ struct Plan {
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
     size_t off_msg = 0, off_zv = 0, off_hb = 0;   // two-scan: per-edge L_mn and Z_mn planes, hard-bit ballots
     size_t ws_bytes = 0;
+    ldpc_tuning tn{};            // the call's plan overrides (zero = automatic)
 };
 
 // integer variant of one iteration: offset beta (LSBs), normalization lambda = na / 2^ns
@@ -597,6 +601,12 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         p->schedule != LDPC_SCHED_LAYERED)
         return fail(LDPC_ERR_INVALID_ARG, "bad schedule %d", p->schedule);
     pl.sched = p->schedule;
+    if (p->tuning) pl.tn = *p->tuning;
+    if (pl.tn.path < LDPC_PATH_AUTO || pl.tn.path > LDPC_PATH_RESIDENT_BATCHED)
+        return fail(LDPC_ERR_INVALID_ARG, "bad tuning.path %d", pl.tn.path);
+    if (pl.tn.resident_waves < 0 || pl.tn.stream_chunk_tiles < 0 || pl.tn.host_chunks < 0 || pl.tn.host_streams < 0 ||
+        pl.tn.host_streams > 4)
+        return fail(LDPC_ERR_INVALID_ARG, "bad tuning value");
     if (pl.sched == LDPC_SCHED_TWOSCAN) {
         if (p->msg_format != LDPC_MSG_COMPACT)
             return fail(LDPC_ERR_UNSUPPORTED, "two-scan stores full per-edge messages: msg_format must be COMPACT");
@@ -629,14 +639,9 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                 pl.betafs.push_back(b);
             }
         }
-        // codes whose fp32 posterior double buffer fits in shared memory decode resident
-        // (k_resident_f32.cuh, one frame per CTA); LDPC_FORCE_STREAM=1 (test hook) and
-        // everything else take the fp32 streaming kernel
-        const char *force = getenv("LDPC_FORCE_STREAM");
-        const bool fres = c->res_ok && c->max_dc <= kMaxDC && c->nbatch_atom > 0 && pl.sched == LDPC_SCHED_SINGLESCAN &&
-                          !(force && force[0] == '1') && (pl.alphas.empty() || p->max_iter <= kMaxSched);
-        pl.path = fres ? PATH_RESIDENT : PATH_STREAM_F;
-        if (fres) pl.kind = RES_F32;
+        // fp32 flooding and two-scan decode on the streaming kernels, whose exact int64
+        // accumulation (reading D28) is order-free; the layered schedule is resident
+        pl.path = PATH_STREAM_F;
         if (pl.sched == LDPC_SCHED_LAYERED) {
             // layered schedule (D25): resident only (k_resident_f32_lay, one posterior array)
             if (!c->res_ok || c->max_dc > kMaxDC)
@@ -683,17 +688,14 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                 if (vs != LDPC_OK) return vs;
             }
         }
-        // LDPC_FORCE_STREAM=1 (test hook) routes integer decodes through the streaming kernels
-        const char *force = getenv("LDPC_FORCE_STREAM");
-        pl.path = (c->res_ok && !(force && force[0] == '1') && pl.sched == LDPC_SCHED_SINGLESCAN) ? PATH_RESIDENT
+        // tuning.path = LDPC_PATH_STREAM routes integer decodes through the streaming kernels
+        pl.path = (c->res_ok && pl.tn.path != LDPC_PATH_STREAM && pl.sched == LDPC_SCHED_SINGLESCAN) ? PATH_RESIDENT
                                                                                                    : PATH_STREAM_I;
         // the streaming integer kernels (and two-scan) keep posteriors as 2Z + 0x4000 per
         // 16-bit lane (reading D26): needs 2Q(max_dv+1) < 0x4000
         if (pl.path == PATH_STREAM_I && (int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
             return fail(LDPC_ERR_UNSUPPORTED, "streaming integer decode needs 2*Q*(max_dv+1) < 16384 (Q=%d, max_dv=%d)",
                         pl.Q, c->max_dv);
-        if (pl.fmt == FMT_FULL && pl.path != PATH_RESIDENT)
-            return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages (LDPC_MSG_FULL) need a code on the resident path");
         if (pl.sched == LDPC_SCHED_LAYERED) {
             if (!c->res_ok)
                 return fail(LDPC_ERR_UNSUPPORTED, "layered schedule needs a code whose posteriors fit in shared memory "
@@ -707,7 +709,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     } else {
         return fail(LDPC_ERR_INVALID_ARG, "bad llr_type %d", p->llr_type);
     }
-    const bool f32res = pl.kind == RES_F32 || pl.kind == RES_F32_LAY;
+    const bool f32res = pl.kind == RES_F32_LAY;
     const int64_t npairs = f32res ? F : (F + 1) / 2;   // CTA work units: frame pairs (fp32: frames)
     if (pl.path == PATH_RESIDENT && !pl.vks.empty() && p->max_iter > kMaxSched) {
         if (pl.lay) return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
@@ -718,15 +720,13 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     }
     if (pl.path == PATH_RESIDENT) {
         // flooding uses the barrier-free atomic kernel when the biased 16-bit lanes cannot
-        // overflow: 2 Q (max_dv + 1) < 0x4000 (k_resident_atom.cuh); LDPC_RES_BATCHED=1
-        // selects the batched kernel
-        const char *be = getenv("LDPC_RES_BATCHED");
+        // overflow: 2 Q (max_dv + 1) < 0x4000 (k_resident_atom.cuh); tuning.path =
+        // LDPC_PATH_RESIDENT_BATCHED selects the batched kernel
         const bool atom_ok = (int64_t)2 * pl.Q * (c->max_dv + 1) < 0x4000 && c->nbatch_atom > 0;
-        if (!f32res) pl.kind = pl.lay ? RES_LAYERED : ((atom_ok && !(be && be[0] == '1')) ? RES_ATOM : RES_BATCHED);
-        if (pl.fmt == FMT_FULL && pl.kind != RES_ATOM)
-            return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages (LDPC_MSG_FULL) need the barrier-free resident "
-                                              "kernel: SINGLESCAN schedule and 2*Q*(max_dv+1) < 16384");
-        const bool atom_rows = pl.kind == RES_ATOM || pl.kind == RES_F32;   // barrier-free row ownership
+        if (!f32res)
+            pl.kind = pl.lay ? RES_LAYERED
+                             : ((atom_ok && pl.tn.path != LDPC_PATH_RESIDENT_BATCHED) ? RES_ATOM : RES_BATCHED);
+        const bool atom_rows = pl.kind == RES_ATOM;   // barrier-free row ownership
         pl.threads = pl.lay ? c->res_threads_lay : (atom_rows ? c->res_threads_atom : c->res_threads);
         pl.nbatch = pl.lay ? c->nbatch_lay : (atom_rows ? c->nbatch_atom : c->nbatch);
         pl.smem = pl.lay ? c->res_smem / 2 : c->res_smem;   // layered: one posterior array
@@ -760,13 +760,18 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
             pl.tile = f32 ? 32 : 64;
         }
     }
+    // FULL per-edge messages exist only in the barrier-free resident kernel: checked after
+    // every path switch above (long per-iteration schedules, TMEM fallback, forced streaming)
+    if (pl.fmt == FMT_FULL && (pl.path != PATH_RESIDENT || pl.kind != RES_ATOM))
+        return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages (LDPC_MSG_FULL) need the barrier-free resident "
+                                          "kernel: SINGLESCAN schedule, a code on the resident path, at most %d "
+                                          "iterations of per-iteration schedules and 2*Q*(max_dv+1) < 16384", kMaxSched);
     if (pl.path == PATH_RESIDENT) {
         const uint32_t cols = pl.tmem_cols_needed;
         pl.tmem_cols = cols;
         int blocks = 0;
         cudaError_t e = res_occupancy_any(c, p, pl, &blocks);
         if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "occupancy query: %s", cudaGetErrorString(e));
-        if (getenv("LDPC_DEBUG")) fprintf(stderr, "[ldpc] occupancy API: %d blocks/SM\n", blocks);
         blocks = std::min(blocks, (int)(512 / cols));     // TMEM capacity per SM
         // barrier-free kernel on a general (CSR) code: stage its [dc][M] column table in
         // shared memory (per-edge offsets become shared loads) when that costs no occupancy
@@ -785,25 +790,21 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         // balances the SMs dynamically.  Measured against a persistent grid of `blocks x SMs`
         // CTAs looping over pairs: cfg2 2.91 -> 2.67 ms, cfg3 40.6 -> 35.9 ms.  The price is
         // one Z^(0) slot per CTA in the workspace; the 64-wave cap bounds it (cfg2: <= 0.9 GB)
-        // for huge batches, whose CTAs then loop over pairs.  LDPC_RES_GRID_MULT=m sets the cap
-        // to m waves (tuning hook).
-        pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)blocks * c->sm_count * 64);
-        if (const char *ge = getenv("LDPC_RES_GRID_MULT"))
-            pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1),
-                                             (int64_t)blocks * c->sm_count * std::max(1, atoi(ge)));
+        // for huge batches, whose CTAs then loop over pairs.  tuning.resident_waves sets the cap.
+        const int waves = pl.tn.resident_waves > 0 ? pl.tn.resident_waves : 64;
+        pl.grid = (int)std::min<int64_t>(std::max<int64_t>(npairs, 1), (int64_t)blocks * c->sm_count * waves);
         pl.slot_words = ((size_t)c->N + 63) & ~(size_t)63;
-        if (getenv("LDPC_DEBUG"))
-            fprintf(stderr, "[ldpc] resident: threads=%d smem=%zu tmem_cols=%u (%d per group) occ_blocks=%d grid=%d batches=%d\n",
-                    pl.threads, pl.smem, cols, pl.cols_per_group, blocks, pl.grid, pl.nbatch);
         pl.ws_bytes = align256((size_t)pl.grid * pl.slot_words * 4);
     } else {
         // streaming layout (also the fallback of a resident plan that does not fit in TMEM)
         pl.ntiles = (int)((F + pl.tile - 1) / pl.tile);
         const size_t plane = (size_t)pl.ntiles * c->N * 32 * 4;
+        // fp32: the posterior planes hold int64 exact sums (reading D28)
+        const size_t lplane = pl.path == PATH_STREAM_F ? 2 * plane : plane;
         const int sw = pl.path == PATH_STREAM_F ? 3 : (pl.fmt == FMT_C16 ? 3 : 2);
         size_t off = 0;
         pl.off_z0 = off; off += align256(plane);
-        for (int i = 0; i < 3; ++i) { pl.off_lb[i] = off; off += align256(plane); }
+        for (int i = 0; i < 3; ++i) { pl.off_lb[i] = off; off += align256(lplane); }
         if (pl.sched == LDPC_SCHED_TWOSCAN) {
             const size_t eplane = (size_t)pl.ntiles * (size_t)c->E * 32 * 4;
             pl.off_msg = off; off += align256(eplane);
@@ -822,9 +823,12 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
 }
 
 cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_params *p, int64_t F,
-                         const void *llr, uint32_t *hb, void *post, uint8_t *ok, int32_t *it, void *ws,
+                         const void *llr, uint32_t *hb, void *post, uint8_t *ok, int32_t *it, void *msg, void *ws,
                          cudaStream_t s) {
     ResArgs a{};
+    a.msg_out = (int16_t *)msg;
+    a.row_ptr = c->d_row_ptr;
+    a.E = c->E;
     a.N = c->N;
     a.Np = (c->N + 3) & ~3;
     a.M = c->M;
@@ -853,7 +857,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.csr_dc = c->max_dc;
     a.alpha = pl.alpha;
     a.beta = pl.betaf;
-    if ((pl.kind == RES_F32 || pl.kind == RES_F32_LAY) && !pl.alphas.empty()) {
+    if (pl.kind == RES_F32_LAY && !pl.alphas.empty()) {
         a.nsched = (int)pl.alphas.size();
         for (size_t k = 0; k < pl.alphas.size(); ++k) {
             a.alpha_sched[k] = pl.alphas[k];
@@ -868,7 +872,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.rk = make_regk();
     static const QcTab empty_tab{};
     const QcTab *qt = (pl.kind == RES_LAYERED || pl.kind == RES_F32_LAY) ? c->qtab_lay
-                                             : ((pl.kind == RES_ATOM || pl.kind == RES_F32) ? c->qtab_atom : c->qtab);
+                                                                          : (pl.kind == RES_ATOM ? c->qtab_atom : c->qtab);
     cudaError_t e = res_launch(c->qc, p->early_stop != 0, pl.fmt, p->llr_type == LDPC_LLR_I8, pl.kind, pl.grid,
                                pl.threads, pl.smem, a, qt ? *qt : empty_tab, s);
     ++g_launches;
@@ -876,9 +880,11 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
 }
 
 cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_params *p, int64_t F, const void *llr,
-                       uint32_t *hb, void *post, uint8_t *ok, int32_t *it, void *ws, cudaStream_t s) {
+                       uint32_t *hb, void *post, uint8_t *ok, int32_t *it, void *msg, void *ws, cudaStream_t s) {
     char *w = (char *)ws;
     StreamArgs a{};
+    a.msg_out = msg;
+    a.E = c->E;
     a.N = c->N;
     a.M = c->M;
     a.ntiles = pl.ntiles;
@@ -918,11 +924,11 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     r.vk_sched = pl.vks.empty() ? nullptr : pl.vks.data();
     r.alpha_sched = pl.alphas.empty() ? nullptr : pl.alphas.data();
     r.beta_sched = pl.betafs.empty() ? nullptr : pl.betafs.data();
-    // L2 chunking (opt-in, LDPC_CHUNK_TILES = tiles per chunk): measured SLOWER on cfg4/cfg5
-    // at every chunk size (the streaming kernels are issue/latency-bound,
-    // not HBM-bound, and chunks add launch tails), so all tiles run together by default.
-    r.chunk_tiles = 0;
-    if (const char *ce = getenv("LDPC_CHUNK_TILES")) r.chunk_tiles = atoi(ce);
+    // L2 chunking (opt-in, tuning.stream_chunk_tiles = tiles per chunk): measured SLOWER on
+    // cfg4/cfg5 at every chunk size (the streaming kernels are issue/latency-
+    // bound, not HBM-bound, and chunks add launch tails), so all tiles run together by default.
+    r.chunk_tiles = pl.tn.stream_chunk_tiles;
+    r.register_kernels = pl.tn.stream_register_kernels == 1;
     int32_t n = 0;
     cudaError_t e;
     if (pl.sched == LDPC_SCHED_TWOSCAN) {
@@ -945,14 +951,17 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
 
 ldpc_status decode_device(const ldpc_code *c, const ldpc_decode_params *p, int64_t F, const void *llr, uint32_t *hb,
                           void *post, uint8_t *ok, int32_t *it, void *ws, size_t wsb, cudaStream_t s,
-                          const Plan &pl) {
+                          const Plan &pl, void *msg = nullptr) {
     if (F == 0) return LDPC_OK;
+    if (msg && pl.path == PATH_RESIDENT && pl.kind != RES_ATOM)
+        return fail(LDPC_ERR_UNSUPPORTED, "message export needs the SINGLESCAN flooding kernels (barrier-free resident "
+                                          "or streaming) or TWOSCAN; not the batched / layered resident kernels");
     if (!llr || !hb || !ok) return fail(LDPC_ERR_INVALID_ARG, "llr, hard_bits and syndrome_ok must be non-NULL");
     if (!ws || wsb < pl.ws_bytes)
         return fail(LDPC_ERR_INVALID_ARG, "workspace too small: %zu < %zu bytes", wsb, pl.ws_bytes);
     if (((uintptr_t)ws & 255) != 0) return fail(LDPC_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
-    cudaError_t e = pl.path == PATH_RESIDENT ? run_resident(c, pl, p, F, llr, hb, post, ok, it, ws, s)
-                                             : run_stream(c, pl, p, F, llr, hb, post, ok, it, ws, s);
+    cudaError_t e = pl.path == PATH_RESIDENT ? run_resident(c, pl, p, F, llr, hb, post, ok, it, msg, ws, s)
+                                             : run_stream(c, pl, p, F, llr, hb, post, ok, it, msg, ws, s);
     if (e != cudaSuccess) return fail(LDPC_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
     return LDPC_OK;
 }
@@ -987,6 +996,23 @@ extern "C" ldpc_status ldpc_decode_batch(const ldpc_code *code, const ldpc_decod
                          workspace_bytes, (cudaStream_t)stream, pl);
 }
 
+extern "C" ldpc_status ldpc_decode_batch_messages(const ldpc_code *code, const ldpc_decode_params *params,
+                                                  int64_t n_frames, const void *llr, uint32_t *hard_bits,
+                                                  void *posteriors, uint8_t *syndrome_ok, int32_t *iterations_used,
+                                                  void *messages, void *workspace, size_t workspace_bytes,
+                                                  void *stream) {
+    g_detail.clear();
+    g_launches = 0;
+    if (!code) return fail(LDPC_ERR_INVALID_ARG, "code is NULL");
+    if (!messages && n_frames > 0) return fail(LDPC_ERR_INVALID_ARG, "messages is NULL");
+    DeviceGuard guard(code->device);
+    Plan pl;
+    ldpc_status st = make_plan(code, n_frames, params, pl);
+    if (st != LDPC_OK) return st;
+    return decode_device(code, params, n_frames, llr, hard_bits, posteriors, syndrome_ok, iterations_used, workspace,
+                         workspace_bytes, (cudaStream_t)stream, pl, messages);
+}
+
 // ------------------------------------------------------------------ host I/O
 namespace {
 struct HostLayout {
@@ -1009,7 +1035,7 @@ ldpc_status host_layout(const ldpc_code *c, int64_t F, const ldpc_decode_params 
     // chunks of >= 256 frames (resident kernels) or >= one 64-frame tile (streaming), <= 16
     const int64_t min_chunk = pf.path == PATH_RESIDENT ? 256 : 64;
     h.nchunks = std::max<int64_t>(1, std::min<int64_t>(16, F / min_chunk));
-    if (const char *e = getenv("LDPC_HOST_CHUNKS")) h.nchunks = std::max(1, atoi(e));
+    if (pf.tn.host_chunks > 0) h.nchunks = pf.tn.host_chunks;
     h.chunk = (F + h.nchunks - 1) / h.nchunks;
     h.chunk = ((h.chunk + 63) / 64) * 64;
     if (h.chunk == 0) h.chunk = 64;
@@ -1027,7 +1053,7 @@ ldpc_status host_layout(const ldpc_code *c, int64_t F, const ldpc_decode_params 
     h.off_ok = off; off += align256((size_t)F);
     h.off_it = off; off += align256((size_t)F * 4);
     h.nstreams = (int)std::min<int64_t>(h.nchunks, 4);
-    if (const char *e = getenv("LDPC_HOST_STREAMS")) h.nstreams = std::max(1, std::min(4, atoi(e)));
+    if (pf.tn.host_streams > 0) h.nstreams = pf.tn.host_streams;
     h.chunk_ws = pl.ws_bytes;
     for (int i = 0; i < h.nstreams; ++i) { h.off_ws[i] = off; off += align256(pl.ws_bytes); }
     h.total = off;

@@ -4,6 +4,7 @@
 // res_launch.cu.
 #pragma once
 #include <algorithm>
+#include <mutex>
 
 #include "k_resident.cuh"
 #include "k_resident_atom.cuh"
@@ -17,9 +18,22 @@ template <bool QC, bool ES, int FMT, typename TIN, int KIND>
 struct Kern {
     static auto get() {
         if constexpr (KIND == 4) return k_resident_f32_lay<QC, ES>;
-        else if constexpr (KIND == 3) return k_resident_f32<QC, ES>;
         else if constexpr (KIND == 2) return k_resident_atom<QC, ES, FMT, TIN>;
         else return k_resident<QC, ES, FMT, TIN, KIND == 1>;
+    }
+    // The dynamic shared memory cap is raised once per kernel to the device's opt-in limit
+    // (it is only a cap: occupancy follows the size each launch asks for), so concurrent
+    // host threads never race on the attribute.
+    static cudaError_t prepare() {
+        static std::once_flag once;
+        static cudaError_t err = cudaSuccess;
+        std::call_once(once, [] {
+            int dev = 0, optin = 0;
+            err = cudaGetDevice(&dev);
+            if (err == cudaSuccess) err = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            if (err == cudaSuccess) err = cudaFuncSetAttribute(get(), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        });
+        return err;
     }
 };
 
@@ -29,7 +43,7 @@ cudaError_t occ(size_t dyn_smem, size_t smem_per_sm, int threads, int *blocks) {
     // limit from the kernel's registers, shared memory and threads instead (TMEM is
     // accounted for by the caller).
     auto kern = Kern<QC, ES, FMT, TIN, KIND>::get();
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    cudaError_t e = Kern<QC, ES, FMT, TIN, KIND>::prepare();
     if (e != cudaSuccess) return e;
     cudaFuncAttributes fa;
     if ((e = cudaFuncGetAttributes(&fa, kern)) != cudaSuccess) return e;
@@ -45,7 +59,7 @@ cudaError_t occ(size_t dyn_smem, size_t smem_per_sm, int threads, int *blocks) {
 template <bool QC, bool ES, int FMT, typename TIN, int KIND>
 cudaError_t launch(int grid, int threads, size_t dyn_smem, const ResArgs &a, const QcTab &t, cudaStream_t s) {
     auto kern = Kern<QC, ES, FMT, TIN, KIND>::get();
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    cudaError_t e = Kern<QC, ES, FMT, TIN, KIND>::prepare();
     if (e != cudaSuccess) return e;
     kern<<<grid, threads, dyn_smem, s>>>(a, t);
     return cudaGetLastError();
@@ -62,8 +76,7 @@ cudaError_t dispatch_qe(int fmt, bool i8, int kind, Args... args) {
     // FMT_FULL (§4 per-edge messages) exists for the barrier-free kernel only
     if (fmt == FMT_FULL && kind == 2)
         return i8 ? K<Q, E, FMT_FULL, int8_t, 2>::run(args...) : K<Q, E, FMT_FULL, int16_t, 2>::run(args...);
-    // fp32 LLRs: one frame per CTA (k_resident_f32.cuh; kind 4: layered schedule)
-    if (kind == 3) return K<Q, E, FMT_C16, float, 3>::run(args...);
+    // fp32 LLRs, layered schedule: one frame per CTA (k_resident_f32.cuh)
     if (kind == 4) return K<Q, E, FMT_C16, float, 4>::run(args...);
 #undef LDPC_RES_CASE
 #undef LDPC_RES_KIND

@@ -1,5 +1,6 @@
-// rowcore_f32.cuh -- fp32 check-row core shared by the fp32 streaming kernel
-// (k_stream.cuh) and the fp32 decode-resident kernel (k_resident_f32.cuh).
+// rowcore_f32.cuh -- fp32 check-row core shared by the fp32 streaming kernels
+// (k_stream.cuh, k_stream_pipe.cuh), the two-scan check pass and the fp32 layered kernel
+// (k_resident_f32.cuh).
 #pragma once
 #include <cstdint>
 
@@ -42,8 +43,9 @@ __device__ __forceinline__ void f32_row_q(const float (&L)[DC], bool first_iter,
         sq |= (q[j] < 0.0f ? 1u : 0u) << j;
     }
     const uint32_t par = __popc(sq) & 1u;
-    A = fmaxf(__fsub_rn(__fmul_rn(alpha, m1), beta), 0.0f);
-    B = fmaxf(__fsub_rn(__fmul_rn(alpha, m2), beta), 0.0f);
+    // P:341-353; magnitudes saturate at 2^20 (reading D28: keeps the exact posterior sums bounded)
+    A = fminf(fmaxf(__fsub_rn(__fmul_rn(alpha, m1), beta), 0.0f), 1048576.0f);
+    B = fminf(fmaxf(__fsub_rn(__fmul_rn(alpha, m2), beta), 0.0f), 1048576.0f);
     const uint32_t sg = par ? (~sq & ((1u << DC) - 1u)) : sq;       // s = prod of the others' signs
     const uint32_t oh = 0x10000u << i1;
     Wn = sg | oh;

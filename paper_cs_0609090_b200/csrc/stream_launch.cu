@@ -1,6 +1,6 @@
 // stream_launch.cu -- launches of the streaming kernels (long codes) and the error counter.
 #include <algorithm>
-#include <cstdlib>
+#include <mutex>
 
 #include "k_stream_pipe.cuh"
 #include "k_twoscan.cuh"
@@ -51,6 +51,24 @@ void set_iteration(StreamArgs &c, const StreamRun &r, int k) {
     if (r.alpha_sched) c.alpha = r.alpha_sched[k - 1];
     if (r.beta_sched) c.beta = r.beta_sched[k - 1];
 }
+// raise the dynamic shared memory cap of the pipelined kernels once (a cap only; each
+// launch asks for its own size), so concurrent host threads never race on the attribute
+cudaError_t pipe_prepare() {
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        auto set = [](auto kern, size_t bytes) {
+            if (err == cudaSuccess) err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        };
+        set(k_stream_pipe<true, FMT_C16, true>, pipe_smem_bytes<true>());
+        set(k_stream_pipe<true, FMT_C16, false>, pipe_smem_bytes<true>());
+        set(k_stream_pipe<true, FMT_1BIT, true>, pipe_smem_bytes<true>());
+        set(k_stream_pipe<true, FMT_1BIT, false>, pipe_smem_bytes<true>());
+        set(k_stream_pipe<false, FMT_C16, true>, pipe_smem_bytes<false>());
+        set(k_stream_pipe<false, FMT_C16, false>, pipe_smem_bytes<false>());
+    });
+    return err;
+}
 }  // namespace
 
 cudaError_t count_errors_launch(int64_t nframes, int wpf, const uint32_t *hb, const uint8_t *ok, const int32_t *it,
@@ -78,19 +96,12 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
         e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); }, nl);
     }
     if (e != cudaSuccess) return e;
+    // software-pipelined iteration kernel (cp.async row prefetch) for rows of degree <= 8,
+    // unless the register kernels are requested (tuning cross-check)
     const unsigned fgrid = (unsigned)((r.ntiles * 32 + 255) / 256);
-    // software-pipelined iteration kernel (cp.async row prefetch) unless LDPC_PIPE=0
-    const char *pipe_env = getenv("LDPC_PIPE");
-    const bool use_pipe = r.max_dc <= 8 && !(pipe_env && pipe_env[0] == '0');
-    const size_t psmem = pipe_smem_bytes();
-    if (use_pipe && psmem > 48 * 1024) {
-        cudaFuncSetAttribute(k_stream_pipe<true, FMT_C16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-        cudaFuncSetAttribute(k_stream_pipe<true, FMT_C16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-        cudaFuncSetAttribute(k_stream_pipe<true, FMT_1BIT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-        cudaFuncSetAttribute(k_stream_pipe<true, FMT_1BIT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-        cudaFuncSetAttribute(k_stream_pipe<false, FMT_C16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-        cudaFuncSetAttribute(k_stream_pipe<false, FMT_C16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-    }
+    const bool use_pipe = r.max_dc <= 8 && !r.register_kernels;
+    const size_t psmem = pair ? pipe_smem_bytes<true>() : pipe_smem_bytes<false>();
+    if (use_pipe && (e = pipe_prepare()) != cudaSuccess) return e;
     // Frame tiles are decoded in CHUNKS whose per-iteration working set (Z^(0), the three
     // posterior planes and the compact state of the chunk's tiles) fits in L2: all
     // iterations of a chunk run before the next chunk starts, so after the first
@@ -105,7 +116,7 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
         StreamArgs c = a;
         const size_t plane = (size_t)t0 * a.N * 32;
         c.Z0 = a.Z0 + plane;
-        for (int i = 0; i < 3; ++i) c.Lb[i] = a.Lb[i] + plane;
+        for (int i = 0; i < 3; ++i) c.Lb[i] = a.Lb[i] + (pair ? plane : 2 * plane);   // fp32: int64 planes
         c.st = a.st + (size_t)t0 * nst * a.M * 32;
         c.synd = a.synd + (size_t)t0 * 32;
         c.done = a.done + (size_t)t0 * 32;
@@ -159,9 +170,8 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
             }
         }
     }
-    const int kb = r.max_iter % 3;
-    if (pair) e = launch([&] { k_stream_syndrome<true><<<gr, 256, 0, s>>>(a, kb); }, nl);
-    else e = launch([&] { k_stream_syndrome<false><<<gr, 256, 0, s>>>(a, kb); }, nl);
+    if (pair) e = launch([&] { k_stream_syndrome<true><<<gr, 256, 0, s>>>(a, r.max_iter); }, nl);
+    else e = launch([&] { k_stream_syndrome<false><<<gr, 256, 0, s>>>(a, r.max_iter); }, nl);
     if (e != cudaSuccess) return e;
     if (pair) e = launch([&] { k_stream_finalize_flags<true><<<fgrid, 256, 0, s>>>(a); }, nl);
     else e = launch([&] { k_stream_finalize_flags<false><<<fgrid, 256, 0, s>>>(a); }, nl);
@@ -169,7 +179,10 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
     dim3 go((unsigned)a.wpf, (unsigned)r.ntiles);
     if (pair) e = launch([&] { k_stream_output<true><<<go, 256, 0, s>>>(a); }, nl);
     else e = launch([&] { k_stream_output<false><<<go, 256, 0, s>>>(a); }, nl);
-    return e;
+    if (e != cudaSuccess || !a.msg_out) return e;
+    if (!pair) return launch([&] { k_stream_export<false, FMT_C16><<<gr, 256, 0, s>>>(a); }, nl);
+    if (r.fmt == FMT_C16) return launch([&] { k_stream_export<true, FMT_C16><<<gr, 256, 0, s>>>(a); }, nl);
+    return launch([&] { k_stream_export<true, FMT_1BIT><<<gr, 256, 0, s>>>(a); }, nl);
 }
 
 
@@ -193,9 +206,9 @@ cudaError_t twoscan_run(const StreamArgs &a0, const TwoScanArgs &t, const Stream
     const dim3 gn((unsigned)std::max(1, std::min((a.N + 7) / 8, 4096)), (unsigned)r.ntiles);
     const dim3 gr((unsigned)std::max(1, (a.M + 63) / 64), (unsigned)r.ntiles);
     const unsigned fgrid = (unsigned)((r.ntiles * 32 + 255) / 256);
-    auto syndrome = [&](int bufidx) {
-        return pair ? launch([&] { k_stream_syndrome<true><<<gr, 256, 0, s>>>(a, bufidx); }, nl)
-                    : launch([&] { k_stream_syndrome<false><<<gr, 256, 0, s>>>(a, bufidx); }, nl);
+    auto syndrome = [&](int k) {      // posterior after iteration k (k = 0: Z^(0))
+        return pair ? launch([&] { k_stream_syndrome<true><<<gr, 256, 0, s>>>(a, k); }, nl)
+                    : launch([&] { k_stream_syndrome<false><<<gr, 256, 0, s>>>(a, k); }, nl);
     };
     auto freeze = [&](int k) {
         return pair ? launch([&] { k_stream_freeze<true><<<fgrid, 256, 0, s>>>(a, k); }, nl)
@@ -230,13 +243,17 @@ cudaError_t twoscan_run(const StreamArgs &a0, const TwoScanArgs &t, const Stream
         }
     }
     // final syndrome of Z^(K); frames not frozen get iterations_used = K
-    if ((e = syndrome(r.max_iter % 3)) != cudaSuccess) return e;
+    if ((e = syndrome(r.max_iter)) != cudaSuccess) return e;
     e = pair ? launch([&] { k_stream_finalize_flags<true><<<fgrid, 256, 0, s>>>(a); }, nl)
              : launch([&] { k_stream_finalize_flags<false><<<fgrid, 256, 0, s>>>(a); }, nl);
     if (e != cudaSuccess) return e;
     dim3 go((unsigned)a.wpf, (unsigned)r.ntiles);
-    return pair ? launch([&] { k_stream_output<true><<<go, 256, 0, s>>>(a); }, nl)
-                : launch([&] { k_stream_output<false><<<go, 256, 0, s>>>(a); }, nl);
+    e = pair ? launch([&] { k_stream_output<true><<<go, 256, 0, s>>>(a); }, nl)
+             : launch([&] { k_stream_output<false><<<go, 256, 0, s>>>(a); }, nl);
+    if (e != cudaSuccess || !a.msg_out) return e;
+    const dim3 ge((unsigned)std::max<int64_t>(1, std::min<int64_t>((t.E + 7) / 8, 8192)), (unsigned)r.ntiles);
+    return pair ? launch([&] { k_ts_export<true><<<ge, 256, 0, s>>>(a, t); }, nl)
+                : launch([&] { k_ts_export<false><<<ge, 256, 0, s>>>(a, t); }, nl);
 }
 
 }  // namespace ldpc

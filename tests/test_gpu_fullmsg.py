@@ -71,3 +71,22 @@ def test_full_unsupported():
     with pytest.raises(P.LdpcError) as e:                    # layered keeps the compact state
         dec.workspace(64, P.params_for_config(g.CONFIGS[2], P.LDPC_SCHED_LAYERED, msg_format=FULL))
     assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+
+
+def test_full_unsupported_after_path_switch():
+    """Requests that the planner moves off the barrier-free resident kernel after the format
+    check -- per-iteration schedules longer than 64 iterations (streaming kernels), a forced
+    streaming path, the batched resident kernel -- are rejected, never silently decoded with
+    byte-wide magnitudes (round-1 advisor finding)."""
+    code = g.CONFIGS[1].code()
+    dec = decoder(code)
+    long = P.make_params(70, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, FULL,
+                         alpha_per_iter=[1.0] * 70)
+    for params in (long,
+                   P.make_params(5, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, FULL,
+                                 tuning={"path": P.LDPC_PATH_STREAM}),
+                   P.make_params(5, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, FULL,
+                                 tuning={"path": P.LDPC_PATH_RESIDENT_BATCHED})):
+        with pytest.raises(P.LdpcError) as e:
+            dec.workspace(8, params)
+        assert e.value.status == P.LDPC_ERR_UNSUPPORTED

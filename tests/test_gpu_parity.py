@@ -1,9 +1,11 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
 
 Integer paths (int16 compact, int8 1-bit): bit-exact posteriors, hard bits,
-syndrome flags and iteration counts (BASELINE.json north star).  fp32 normalized
-path: |dL| <= 1e-4 (1 + |L|), hard bits may differ only where |L| < 1e-3.
-Oracle inputs are the generator's bytes (ldpcgen), never the GPU's.
+syndrome flags and iteration counts (BASELINE.json north star).  fp32 path: bit-exact
+as well -- both sides sum posteriors exactly and round once (reading D28) -- and, as the
+north star's bar, within |dL| <= 1e-4 (1 + |L|) of the float64 oracle with hard bits
+differing only where |L| < 1e-3.  Oracle inputs are the generator's bytes (ldpcgen),
+never the GPU's.
 """
 import os
 
@@ -30,6 +32,11 @@ def decoder(code):
     if key not in _DECODERS:
         _DECODERS[key] = (code, P.Decoder(code, 0))
     return _DECODERS[key][1]
+
+
+def tuned(params, **kw):
+    """params with plan overrides (include/ldpc.h ldpc_tuning), e.g. path=P.LDPC_PATH_STREAM."""
+    return P.set_tuning(params, kw)
 
 
 def gpu_decode(code, llr, params, posteriors=True):
@@ -73,9 +80,7 @@ def small_codes():
 @pytest.mark.parametrize("code", small_codes(), ids=lambda c: c.name)
 @pytest.mark.parametrize("force_stream", [False, True])
 @pytest.mark.parametrize("fmt", ["compact", "1bit"])
-def test_small_codes_int(code, force_stream, fmt, monkeypatch):
-    if force_stream:
-        monkeypatch.setenv("LDPC_FORCE_STREAM", "1")
+def test_small_codes_int(code, force_stream, fmt):
     Q = 511 if fmt == "compact" else 127
     kind, frac = (g.LLR_I16, 3) if fmt == "compact" else (g.LLR_I8, 2)
     sigma2 = g.ebn0_to_sigma2(1.5, max(code.rate, 0.3))
@@ -85,6 +90,8 @@ def test_small_codes_int(code, force_stream, fmt, monkeypatch):
             params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q,
                                    P.LDPC_LLR_I16 if kind == g.LLR_I16 else P.LDPC_LLR_I8,
                                    P.LDPC_MSG_COMPACT if fmt == "compact" else P.LDPC_MSG_1BIT)
+            if force_stream:
+                tuned(params, path=P.LDPC_PATH_STREAM)
             assert_int_parity(code, llr, params, K, es, beta, Q)
 
 
@@ -114,10 +121,11 @@ def test_cfg2_parity_subset_and_early_stop():
 
 
 def test_cfg3_parity_subset():
-    """Config 3: 1-bit messages, int8 Q2 LLRs, 30 iterations (512-frame subset)."""
+    """Config 3: 1-bit messages, int8 Q2 LLRs, 30 iterations (2048-frame subset, SURVEY
+    §8(d): 64 whole 32-frame sign words)."""
     cfg = g.CONFIGS[3]
     code = cfg.code()
-    llr = cfg.llrs(code, 0, 512)
+    llr = cfg.llrs(code, 0, 2048)
     assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, 0, cfg.offset_raw, cfg.clamp)
 
 
@@ -130,6 +138,7 @@ def test_cfg4_parity_subset():
 
 
 def _assert_f32_parity(post, hb, ok, ref_post):
+    """The north star's fp32 bar (used against the float64 oracle)."""
     scale = 1.0 + np.abs(ref_post)
     assert np.max(np.abs(post.astype(np.float64) - ref_post) / scale) <= 1e-4
     bits = (post <= 0).astype(np.uint8)
@@ -138,18 +147,28 @@ def _assert_f32_parity(post, hb, ok, ref_post):
     assert np.all(np.abs(ref_post[diff]) < 1e-3)
 
 
+def assert_f32_exact(post, hb, ok, it, ref):
+    """fp32 GPU vs the fp32 oracle: identical bits (reading D28 makes both order-free)."""
+    np.testing.assert_array_equal(it, ref.iters)
+    np.testing.assert_array_equal(ok, ref.ok)
+    np.testing.assert_array_equal(post.view(np.uint32), ref.post.astype(np.float32).view(np.uint32))
+    np.testing.assert_array_equal(hb, oracle.pack_bits(ref.bits))
+
+
 def test_cfg5_parity_subset():
-    """Config 5: fp32 normalized (alpha 0.75), 50 iterations, 64 frames, BJ tolerance."""
+    """Config 5: fp32 normalized (alpha 0.75), 50 iterations, 64 frames: bit-exact with the
+    fp32 oracle, within the BJ tolerance of the float64 oracle, and byte-identical run to run."""
     cfg = g.CONFIGS[5]
     code = cfg.code()
     llr = cfg.llrs(code, 0, cfg.parity_frames)
     post, hb, ok, it = gpu_decode(code, llr, _cfg_params(cfg))
     ref = oracle.decode(code, llr, "compact", "f32", cfg.max_iter, 0, alpha=cfg.alpha, nthreads=NT)
-    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
-    np.testing.assert_array_equal(it, ref.iters)
+    assert_f32_exact(post, hb, ok, it, ref)
     ref64 = oracle.decode(code, llr.astype(np.float64), "compact", "f64", cfg.max_iter, 0, alpha=cfg.alpha,
                           nthreads=NT)
     _assert_f32_parity(post, hb, ok, ref64.post)
+    again = gpu_decode(code, llr, _cfg_params(cfg))
+    np.testing.assert_array_equal(again[0].view(np.uint32), post.view(np.uint32))
 
 
 @pytest.mark.parametrize("code", small_codes()[1:], ids=lambda c: c.name)
@@ -158,10 +177,12 @@ def test_small_codes_f32(code):
     for F in (1, 33):
         llr = g.llr(5 + F, 0, F, code.n_vars, s2, g.LLR_F32)
         for variant, alpha, beta, es in ((P.LDPC_MINSUM_NORMALIZED, 0.75, 0.0, 0), (P.LDPC_MINSUM_OFFSET, 1.0, 0.25, 1)):
-            params = P.make_params(10, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
-            post, hb, ok, it = gpu_decode(code, llr, params)
-            ref = oracle.decode(code, llr, "compact", "f32", 10, es, beta=beta, alpha=alpha, nthreads=NT)
-            _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+            for reg in (0, 1):                    # cp.async row pipeline / register kernels
+                params = P.make_params(25, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT,
+                                       tuning={"stream_register_kernels": reg})
+                post, hb, ok, it = gpu_decode(code, llr, params)
+                ref = oracle.decode(code, llr, "compact", "f32", 25, es, beta=beta, alpha=alpha, nthreads=NT)
+                assert_f32_exact(post, hb, ok, it, ref)
 
 
 @pytest.mark.parametrize("cfg_idx", [1, 2, 3, 4, 5])
@@ -176,7 +197,7 @@ def test_full_size_sampled_frames(cfg_idx):
     picks = np.unique(np.r_[0, 1, F - 2, F - 1, np.linspace(0, F - 1, 12).astype(int)])
     if cfg.llr_kind == g.LLR_F32:
         ref = oracle.decode(code, llr[picks], "compact", "f32", cfg.max_iter, 0, alpha=cfg.alpha, nthreads=NT)
-        _assert_f32_parity(post[picks], hb[picks], ok[picks], ref.post.astype(np.float64))
+        assert_f32_exact(post[picks], hb[picks], ok[picks], it[picks], ref)
     else:
         ref = oracle_decode_int(code, llr, cfg.max_iter, cfg.early_stop, cfg.offset_raw, cfg.clamp, picks)
         np.testing.assert_array_equal(post[picks].astype(np.int32), ref.post)
@@ -296,7 +317,7 @@ def test_wide_rows_f32_and_unsupported_int():
     params = P.make_params(8, 1, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
     post, hb, ok, it = gpu_decode(code, llr, params)
     ref = oracle.decode(code, llr, "compact", "f32", 8, 1, alpha=0.75, nthreads=NT)
-    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    assert_f32_exact(post, hb, ok, it, ref)
     dec = decoder(code)
     with pytest.raises(P.LdpcError) as e:
         dec.workspace(4, P.make_params(8, 0, P.LDPC_MINSUM_OFFSET, 1, 0, 1.0, 63, P.LDPC_LLR_I16))
@@ -327,41 +348,43 @@ def test_qc_odd_batch_and_mixed_convergence():
     assert_int_parity(g.CONFIGS[2].code(), llr, _cfg_params(g.CONFIGS[2]), 15, 1, 1, 511)
 
 
-@pytest.mark.parametrize("chunk", ["1", "2"])
-def test_stream_l2_chunks(chunk, monkeypatch):
-    """Streaming kernels decoding the frame tiles in chunks (LDPC_CHUNK_TILES, opt-in):
-    int16 with early stop on a QC code (mixed stopping iterations), 1-bit, and fp32 --
-    several tiles plus a ragged last tile, identical to the oracle."""
-    monkeypatch.setenv("LDPC_FORCE_STREAM", "1")
-    monkeypatch.setenv("LDPC_CHUNK_TILES", chunk)
+@pytest.mark.parametrize("chunk", [1, 2])
+def test_stream_l2_chunks(chunk):
+    """Streaming kernels decoding the frame tiles in chunks (tuning.stream_chunk_tiles,
+    opt-in): int16 with early stop on a QC code (mixed stopping iterations), 1-bit, and
+    fp32 -- several tiles plus a ragged last tile, identical to the oracle."""
+    tn = {"path": P.LDPC_PATH_STREAM, "stream_chunk_tiles": chunk}
     code = g.qc(6, 12, 37, np.array([3, 4] * 6, np.int32), seed=8)
     s2 = g.ebn0_to_sigma2(2.5, code.rate)
     llr = g.llr(41, 0, 230, code.n_vars, s2, g.LLR_I16, 3, 511)
-    params = P.make_params(12, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 0, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+    params = P.make_params(12, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 0, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT, tuning=tn)
     assert_int_parity(code, llr, params, 12, 1, 1, 511)
     llr = g.llr(43, 0, 230, code.n_vars, s2, g.LLR_I8, 2, 127)
-    params = P.make_params(12, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 127, P.LDPC_LLR_I8, P.LDPC_MSG_1BIT)
+    params = P.make_params(12, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 127, P.LDPC_LLR_I8, P.LDPC_MSG_1BIT, tuning=tn)
     assert_int_parity(code, llr, params, 12, 0, 1, 127)
     llr = g.llr(42, 0, 100, code.n_vars, s2, g.LLR_F32)
-    params = P.make_params(10, 1, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT)
+    params = P.make_params(10, 1, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT,
+                           tuning=tn)
     post, hb, ok, it = gpu_decode(code, llr, params)
     ref = oracle.decode(code, llr, "compact", "f32", 10, 1, alpha=0.75, nthreads=NT)
-    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
-    np.testing.assert_array_equal(it, ref.iters)
+    assert_f32_exact(post, hb, ok, it, ref)
 
 
 @pytest.mark.parametrize("cfg_idx", [1, 2, 3])
-def test_batched_resident_kernel(cfg_idx, monkeypatch):
-    """The conflict-free-batch resident kernel (LDPC_RES_BATCHED=1; the default flooding
-    kernel accumulates with shared-memory atomics instead) stays bit-exact too."""
-    monkeypatch.setenv("LDPC_RES_BATCHED", "1")
+def test_batched_resident_kernel(cfg_idx):
+    """The conflict-free-batch resident kernel (tuning.path = LDPC_PATH_RESIDENT_BATCHED;
+    the default flooding kernel accumulates with shared-memory atomics instead) stays
+    bit-exact too."""
+    tn = {"path": P.LDPC_PATH_RESIDENT_BATCHED}
     cfg = g.CONFIGS[cfg_idx]
     code = cfg.code()
     llr = cfg.llrs(code, 0, 129)
-    assert_int_parity(code, llr, _cfg_params(cfg), cfg.max_iter, cfg.early_stop, cfg.offset_raw, cfg.clamp)
+    assert_int_parity(code, llr, tuned(_cfg_params(cfg), **tn), cfg.max_iter, cfg.early_stop, cfg.offset_raw,
+                      cfg.clamp)
     for c in small_codes()[:4]:
         z = g.llr(11, 0, 33, c.n_vars, g.ebn0_to_sigma2(1.5, max(c.rate, 0.3)), g.LLR_I16, 3, 511)
-        params = P.make_params(10, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
+        params = P.make_params(10, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT,
+                               tuning=tn)
         assert_int_parity(c, z, params, 10, 1, 1, 511)
 
 
@@ -394,7 +417,7 @@ def test_tmem_capacity_falls_back_to_streaming():
     post, hb, ok, it = gpu_decode(code, z, pf)
     assert P.ldpc_last_launch_count() > 1
     ref = oracle.decode(code, z, "compact", "f32", 5, 0, alpha=0.75, nthreads=NT)
-    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    assert_f32_exact(post, hb, ok, it, ref)
     dec = decoder(code)
     for fmt, sched in ((P.LDPC_MSG_FULL, P.LDPC_SCHED_SINGLESCAN), (P.LDPC_MSG_COMPACT, P.LDPC_SCHED_LAYERED)):
         bad = P.make_params(5, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, fmt, sched)
@@ -411,14 +434,9 @@ def test_high_column_degree_batched_kernel():
     params = P.make_params(8, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
     assert_int_parity(code, llr, params, 8, 1, 1, 511)
     dec = decoder(code)
-    import os
-    os.environ["LDPC_FORCE_STREAM"] = "1"
-    try:
-        with pytest.raises(P.LdpcError) as e:
-            dec.workspace(33, params)
-        assert e.value.status == P.LDPC_ERR_UNSUPPORTED
-    finally:
-        del os.environ["LDPC_FORCE_STREAM"]
+    with pytest.raises(P.LdpcError) as e:
+        dec.workspace(33, tuned(params, path=P.LDPC_PATH_STREAM))
+    assert e.value.status == P.LDPC_ERR_UNSUPPORTED
 
 
 def test_many_iterations():

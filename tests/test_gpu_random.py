@@ -52,7 +52,7 @@ CASES = list(range(120))
 
 
 @pytest.mark.parametrize("i", CASES)
-def test_random_case(i, monkeypatch):
+def test_random_case(i):
     rng = np.random.default_rng(1000 + i)
     code = _code(rng, i)
     max_dc = int(np.max(np.diff(code.row_ptr)))
@@ -72,12 +72,10 @@ def test_random_case(i, monkeypatch):
         fmt = P.LDPC_MSG_COMPACT
     elif sched == P.LDPC_SCHED_SINGLESCAN and rng.integers(0, 3) == 0:
         fmt = P.LDPC_MSG_FULL                      # the §4 per-edge form (resident kernel only)
-    env = [None, "LDPC_FORCE_STREAM", "LDPC_RES_BATCHED", "LDPC_PIPE"][int(rng.integers(0, 4))]
-    if env == "LDPC_PIPE":
-        monkeypatch.setenv("LDPC_PIPE", "0")
-        monkeypatch.setenv("LDPC_FORCE_STREAM", "1")
-    elif env:
-        monkeypatch.setenv(env, "1")
+    env = [None, "stream", "batched", "stream-registers"][int(rng.integers(0, 4))]
+    tuning = {None: None, "stream": {"path": P.LDPC_PATH_STREAM},
+              "batched": {"path": P.LDPC_PATH_RESIDENT_BATCHED},
+              "stream-registers": {"path": P.LDPC_PATH_STREAM, "stream_register_kernels": 1}}[env]
     K = int(rng.integers(1, 14))
     es = int(rng.integers(0, 2))
     beta = int(rng.integers(0, 3))
@@ -85,7 +83,7 @@ def test_random_case(i, monkeypatch):
     ebn0 = float(rng.uniform(0.5, 4.0))
     llr = g.llr(int(rng.integers(1, 1 << 30)), 0, F, code.n_vars, g.ebn0_to_sigma2(ebn0, max(code.rate, 0.2)),
                 kind, frac, Q)
-    params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, lt, fmt, sched)
+    params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, lt, fmt, sched, tuning=tuning)
     try:
         post, hb, ok, it = gpu_decode(code, llr, params)
     except P.LdpcError as e:

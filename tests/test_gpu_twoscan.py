@@ -4,8 +4,9 @@ two-scan engine (§3).
 Integer LLRs: bit-exact posteriors, hard bits, flags and iteration counts -- the oracle's
 two-scan is itself bit-exact with the compact single-scan (pinned in
 tests/test_oracle.py), so these also show the GPU two-scan and single-scan agree.
-fp32: the BASELINE tolerance |dL| <= 1e-4 (1 + |L|) against the oracle's ordered Eq.(2)
-sums (reading D24: the GPU forms the extrinsic as Z_n - L_mn).
+fp32: bit-exact as well -- both sides evaluate Eq.(2)'s sums exactly and round once
+(reading D28), so the GPU's extrinsic Z_n - L_mn (reading D24) equals the oracle's sum over
+m' != m.
 """
 import numpy as np
 import pytest
@@ -20,7 +21,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_cs_0609090_b200 as P  # noqa: E402
-from test_gpu_parity import NT, _assert_f32_parity, gpu_decode, small_codes  # noqa: E402
+from test_gpu_parity import NT, assert_f32_exact, gpu_decode, small_codes  # noqa: E402
 
 TS = P.LDPC_SCHED_TWOSCAN
 
@@ -55,7 +56,7 @@ def test_twoscan_small_codes_f32(code):
             params = P.make_params(10, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, TS)
             post, hb, ok, it = gpu_decode(code, llr, params)
             ref = oracle.decode(code, llr, "twoscan", "f32", 10, es, beta=beta, alpha=alpha, nthreads=NT)
-            _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+            assert_f32_exact(post, hb, ok, it, ref)
 
 
 @pytest.mark.parametrize("cfg_idx", [1, 2, 3, 4])
@@ -79,7 +80,7 @@ def test_twoscan_cfg5_f32():
     llr = cfg.llrs(code, 0, 32)
     post, hb, ok, it = gpu_decode(code, llr, P.params_for_config(cfg, TS))
     ref = oracle.decode(code, llr, "twoscan", "f32", cfg.max_iter, 0, alpha=cfg.alpha, nthreads=NT)
-    _assert_f32_parity(post, hb, ok, ref.post.astype(np.float64))
+    assert_f32_exact(post, hb, ok, it, ref)
 
 
 def test_twoscan_unsupported():

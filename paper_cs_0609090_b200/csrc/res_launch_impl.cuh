@@ -31,7 +31,12 @@ struct Kern {
             int dev = 0, optin = 0;
             err = cudaGetDevice(&dev);
             if (err == cudaSuccess) err = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-            if (err == cudaSuccess) err = cudaFuncSetAttribute(get(), cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+            cudaFuncAttributes fa;
+            if (err == cudaSuccess) err = cudaFuncGetAttributes(&fa, get());
+            // the cap excludes the kernel's static shared memory
+            if (err == cudaSuccess)
+                err = cudaFuncSetAttribute(get(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           optin - (int)fa.sharedSizeBytes);
         });
         return err;
     }

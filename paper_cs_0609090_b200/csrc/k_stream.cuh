@@ -397,11 +397,20 @@ __device__ __forceinline__ void stream_init_next_f(const uint32_t *Z0t, long lon
     longlong2 *dst = (longlong2 *)Xnt;
     const int total = N * 8;
     const int step = nwg * 32;
-    for (int i = wg * 32 + lane; i < total; i += step) {
-        const uint4 v = __ldcg(src + i);
+    auto put = [&](int i, const uint4 &v) {
         __stcg(dst + 2 * i, make_longlong2(grid_of(__uint_as_float(v.x)), grid_of(__uint_as_float(v.y))));
         __stcg(dst + 2 * i + 1, make_longlong2(grid_of(__uint_as_float(v.z)), grid_of(__uint_as_float(v.w))));
+    };
+    int i = wg * 32 + lane;
+    for (; i + 3 * step < total; i += 4 * step) {     // 4 loads in flight (the loop is latency-bound)
+        const uint4 v0 = __ldcg(src + i), v1 = __ldcg(src + i + step), v2 = __ldcg(src + i + 2 * step),
+                    v3 = __ldcg(src + i + 3 * step);
+        put(i, v0);
+        put(i + step, v1);
+        put(i + 2 * step, v2);
+        put(i + 3 * step, v3);
     }
+    for (; i < total; i += step) put(i, __ldcg(src + i));
 }
 // the same per lane, skipping frozen frames (early stop: their buffers keep the exit posterior)
 __device__ __forceinline__ void stream_init_next_f_lanes(const uint32_t *Z0t, long long *Xnt, int N, int wg, int nwg,

@@ -80,3 +80,34 @@ def test_rank_shards_compose_to_the_global_batch():
     _, b = _decode_counts(code, cfg, 4, 4)
     assert np.array_equal(np.concatenate([a.post, b.post]), whole.post)
     assert np.array_equal(np.concatenate([a.iters, b.iters]), whole.iters)
+
+
+def _run_bench(args, timeout=240):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, capture_output=True, text=True,
+                       timeout=timeout, env=env, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return lines[0]
+
+
+def test_bench_spawns_two_ranks_and_reduces():
+    """`bench.py --gpus 2` with no launcher re-executes itself under torch.distributed.run
+    (2 ranks, 127.0.0.1 rendezvous); --dist-check drives the bench's own sharding and SUM /
+    MAX all-reduce (gloo on CPU, NCCL on GPUs) end to end and checks them on rank 0."""
+    line = _run_bench(["--gpus", "2", "--dist-check", "--config", "1", "--frames", "8"])
+    assert line["dist_check"] is True and line["n_ranks"] == 2
+
+
+def test_bench_reference_arm_two_ranks():
+    """The reference arm under 2 ranks: rank 0 alone times the oracle and prints one line."""
+    line = _run_bench(["--gpus", "2", "--impl", "reference", "--config", "1", "--steps", "1", "--warmup", "3",
+                       "--ref-frames", "4"])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0

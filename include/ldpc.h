@@ -138,6 +138,8 @@ typedef struct {
                                         row pipeline (cross-check), 0 = automatic */
     int32_t host_chunks;     /* ldpc_decode_batch_host: frame chunks (0 = automatic) */
     int32_t host_streams;    /* ldpc_decode_batch_host: internal streams, 1..4 (0 = automatic) */
+    int32_t resident_threads; /* general (non-QC) codes on the barrier-free resident kernel: threads
+                                 per CTA, a multiple of 32 in [32, 256] (0 = automatic) */
 } ldpc_tuning;
 
 typedef struct {

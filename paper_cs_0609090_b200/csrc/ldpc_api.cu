@@ -605,7 +605,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (pl.tn.path < LDPC_PATH_AUTO || pl.tn.path > LDPC_PATH_RESIDENT_BATCHED)
         return fail(LDPC_ERR_INVALID_ARG, "bad tuning.path %d", pl.tn.path);
     if (pl.tn.resident_waves < 0 || pl.tn.stream_chunk_tiles < 0 || pl.tn.host_chunks < 0 || pl.tn.host_streams < 0 ||
-        pl.tn.host_streams > 4)
+        pl.tn.host_streams > 4 || pl.tn.resident_threads < 0 || pl.tn.resident_threads > 256 ||
+        pl.tn.resident_threads % 32 != 0)
         return fail(LDPC_ERR_INVALID_ARG, "bad tuning value");
     if (pl.sched == LDPC_SCHED_TWOSCAN) {
         if (p->msg_format != LDPC_MSG_COMPACT)
@@ -729,6 +730,10 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         const bool atom_rows = pl.kind == RES_ATOM;   // barrier-free row ownership
         pl.threads = pl.lay ? c->res_threads_lay : (atom_rows ? c->res_threads_atom : c->res_threads);
         pl.nbatch = pl.lay ? c->nbatch_lay : (atom_rows ? c->nbatch_atom : c->nbatch);
+        if (atom_rows && !c->qc && pl.tn.resident_threads > 0) {   // rows t, t + T, ... of a general code
+            pl.threads = pl.tn.resident_threads;
+            pl.nbatch = (c->M + pl.threads - 1) / pl.threads;
+        }
         pl.smem = pl.lay ? c->res_smem / 2 : c->res_smem;   // layered: one posterior array
         // TMEM columns: 3 (COMPACT) or 2 (1BIT) per batch per 128-thread group; layered
         // general codes keep the state in shared memory instead ([3][M] words, by row)

@@ -55,6 +55,7 @@ struct ResArgs {
     RegK rk;                          // register constants (simd16.cuh)
     uint32_t cpar;                    // row_parity constant (-(0x00010001), biased: -(0x40014001))
     int csr_smem, csr_dc;             // barrier-free kernel, general codes: colT rows [0, csr_dc) staged in smem
+    int dc_uniform;                   // general codes: the row degree if every row has it, else 0
     // message export (ldpc_decode_batch_messages): the exit messages L_mn rebuilt from each
     // row's state, int16 [nframes][E] in CSR edge order; nullptr = no export
     int16_t *msg_out;

@@ -63,7 +63,7 @@ __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.pr
 // ------------------------------------------------------------ one check row
 // LAY = false: flooding (Z^(k-1) read from Lpb, Z^(k) accumulated in Lab).
 // LAY = true : layered / in-place (reading D25): one array, Z_n <- (Z_n - L_old) + L_new.
-template <int DC, bool QC, bool ES, bool LAY>
+template <int DC, bool QC, bool ES, bool LAY, int FMT>
 __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const VarK &vk, const char *Lpb, char *Lab,
                                         int e0, uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd) {
     // shared-memory byte addresses of the row's variables in both buffers:
@@ -97,7 +97,7 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
         rebuild_q<DC>(L, st, q, a.rk);
     }
     uint32_t rn[DC];
-    new_state<DC>(q, vk, st, rn, a.rk);
+    new_state<DC, false, -1, FMT == FMT_1BIT>(q, vk, st, rn, a.rk);
     if (LAY) {
 #pragma unroll
         for (int j = 0; j < DC; ++j)                          // Z_n = (Z_n - L^(k-1)_mn) + L^(k)_mn
@@ -112,18 +112,18 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
     }
 }
 
-template <bool QC, bool ES, bool LAY>
+template <bool QC, bool ES, bool LAY, int FMT>
 __device__ __forceinline__ void res_dispatch(int dc, const ResArgs &a, const QcTab &t, const VarK &vk, const char *Lpb, char *Lab,
                                              int e0, uint32_t r4, int p, bool first_iter, RowState &st,
                                              uint32_t &synd) {
     switch (dc) {
-    case 2: res_row<2, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 3: res_row<3, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 4: res_row<4, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 5: res_row<5, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 6: res_row<6, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 7: res_row<7, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
-    case 8: res_row<8, QC, ES, LAY>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 2: res_row<2, QC, ES, LAY, FMT>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 3: res_row<3, QC, ES, LAY, FMT>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 4: res_row<4, QC, ES, LAY, FMT>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 5: res_row<5, QC, ES, LAY, FMT>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 6: res_row<6, QC, ES, LAY, FMT>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 7: res_row<7, QC, ES, LAY, FMT>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
+    case 8: res_row<8, QC, ES, LAY, FMT>(a, t, vk, Lpb, Lab, e0, r4, p, first_iter, st, synd); break;
     }
 }
 
@@ -205,6 +205,7 @@ __device__ __forceinline__ void state_tmem_load(uint32_t tw, int b, int nb, RowS
         tmem_wait_ld_dep(X, st.W, st.W);
         st.A = prmt(X, 0u, 0x4240u);
         st.B = prmt(X, 0u, 0x4341u);
+        st.W = expand_idx(st.W);                 // index-coded ñ (rowcore.cuh)
     }
 }
 template <int FMT>
@@ -228,7 +229,7 @@ __device__ __forceinline__ int qc_run(int b, int bend, int g, const ResArgs &a, 
         RowState st = {0u, 0u, 0u};
         if constexpr (DC > 0) {
             if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-            if (rloc < a.Z) res_row<DC, true, ES, LAY>(a, t, vk, Lpb, Lab, t.e0[b][g], r4, 0, first_iter, st, synd);
+            if (rloc < a.Z) res_row<DC, true, ES, LAY, FMT>(a, t, vk, Lpb, Lab, t.e0[b][g], r4, 0, first_iter, st, synd);
             state_tmem_store<FMT>(tw, b, nb, st);
         }
         __syncthreads();                         // batch b's accumulations complete
@@ -362,11 +363,15 @@ __global__ void __launch_bounds__(256, 3) k_resident(const __grid_constant__ Res
                         if (LAY) {
                             // layered general codes: batches can be single rows (e.g. a staircase),
                             // so the state lives in shared memory indexed by row, [3][M] words
-                            if (!FI && valid) { st.A = sst[p]; st.B = sst[a.M + p]; st.W = sst[2 * a.M + p]; }
+                            if (!FI && valid) {
+                                st.A = sst[p];
+                                st.B = sst[a.M + p];
+                                st.W = FMT == FMT_1BIT ? expand_idx(sst[2 * a.M + p]) : sst[2 * a.M + p];
+                            }
                         } else if (!FI) {
                             state_tmem_load<FMT>(tw, b, nb, st);
                         }
-                        if (valid) res_dispatch<QC, RES, LAY>(a.dcT[p], a, t, vk, Lpb, Lab, 0, 0, p, FI, st, synd);
+                        if (valid) res_dispatch<QC, RES, LAY, FMT>(a.dcT[p], a, t, vk, Lpb, Lab, 0, 0, p, FI, st, synd);
                         if (LAY) {
                             if (valid) { sst[p] = st.A; sst[a.M + p] = st.B; sst[2 * a.M + p] = st.W; }
                         } else {

@@ -46,7 +46,7 @@ __device__ __forceinline__ uint32_t atom_row_parity(const uint32_t (&L)[DC]) {
 
 // CSM (general codes): the [dc][M] column table was staged in shared memory at byte
 // address sct (ResArgs::csr_smem), so the per-edge offsets are shared-memory loads
-template <int DC, bool QC, bool ES, int VM, bool CSM = false>
+template <int DC, bool QC, bool ES, int VM, int FMT, bool CSM = false>
 __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba, int e0,
                                          uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd,
                                          uint32_t sct = 0) {
@@ -75,7 +75,7 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
         rebuild_q_b8<DC, kAtomQ0>(L, st, q, a.rk);                         // Z_n - L^(k-1)_mn
     }
     uint32_t rn[DC];                                                     // V(L^(k)_mn) + 0x8000
-    new_state<DC, true, VM>(q, vk, st, rn, a.rk);
+    new_state<DC, true, VM, FMT == FMT_1BIT>(q, vk, st, rn, a.rk);
 #pragma unroll
     for (int j = 0; j < DC; ++j)                                          // Z^(k)_n += L^(k)_mn
         asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");
@@ -226,7 +226,7 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
         for (; b < bend; ++b) {
             RowState st = {0u, 0u, 0u};
             if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
-            if (rloc < a.Z) atom_row<DC, true, ES, VM>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
+            if (rloc < a.Z) atom_row<DC, true, ES, VM, FMT>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
             state_tmem_store<FMT>(tw, b, nb, st);
         }
         return b;
@@ -249,17 +249,17 @@ __device__ __forceinline__ int atom_qc_dispatch(int dc, int b, int bend, int g, 
     }
 }
 
-template <bool ES, int VM, bool CSM>
+template <bool ES, int VM, int FMT, bool CSM>
 __device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba,
                                                   int p, bool first_iter, RowState &st, uint32_t &synd, uint32_t sct) {
     switch (dc) {
-    case 2: atom_row<2, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 3: atom_row<3, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 4: atom_row<4, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 5: atom_row<5, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 6: atom_row<6, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 7: atom_row<7, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 8: atom_row<8, false, ES, VM, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 2: atom_row<2, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 3: atom_row<3, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 4: atom_row<4, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 5: atom_row<5, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 6: atom_row<6, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 7: atom_row<7, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 8: atom_row<8, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
     }
 }
 
@@ -432,6 +432,30 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
                         if (grp == 0) b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, bp, ba, FI, synd);
                         else b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, bp, ba, FI, synd);
                     }
+                } else if (FMT != FMT_FULL && a.dc_uniform) {
+                    // row-regular code (e.g. config 1's (3,6)-regular H): one dispatch on the
+                    // degree per iteration instead of a switch in every row
+                    auto rows = [&](auto dc_tag) {
+                        constexpr int DC = decltype(dc_tag)::value;
+#pragma unroll 1
+                        for (int b = 0; b < nb; ++b) {
+                            const int p = b * nth + tid;
+                            RowState st = {0u, 0u, 0u};
+                            if (!FI) state_tmem_load<FMT>(tw, b, nb, st);
+                            if (p < a.M)
+                                atom_row<DC, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, FI, st, synd, sct);
+                            state_tmem_store<FMT>(tw, b, nb, st);
+                        }
+                    };
+                    switch (a.dc_uniform) {
+                    case 2: rows(std::integral_constant<int, 2>{}); break;
+                    case 3: rows(std::integral_constant<int, 3>{}); break;
+                    case 4: rows(std::integral_constant<int, 4>{}); break;
+                    case 5: rows(std::integral_constant<int, 5>{}); break;
+                    case 6: rows(std::integral_constant<int, 6>{}); break;
+                    case 7: rows(std::integral_constant<int, 7>{}); break;
+                    case 8: rows(std::integral_constant<int, 8>{}); break;
+                    }
                 } else {
 #pragma unroll 1
                     for (int b = 0; b < nb; ++b) {
@@ -445,7 +469,7 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
                         } else {
                             RowState st = {0u, 0u, 0u};
                             if (!FI) state_tmem_load<FMT>(tw, b, nb, st);
-                            if (p < a.M) atom_csr_dispatch<ES, VM, CSM>(a.dcT[p], a, t, vk, bp, ba, p, FI, st, synd, sct);
+                            if (p < a.M) atom_csr_dispatch<ES, VM, FMT, CSM>(a.dcT[p], a, t, vk, bp, ba, p, FI, st, synd, sct);
                             state_tmem_store<FMT>(tw, b, nb, st);
                         }
                     }

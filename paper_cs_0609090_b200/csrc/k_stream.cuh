@@ -140,7 +140,7 @@ __device__ __forceinline__ void stream_rows_i(const StreamArgs &a, int lane, con
             rebuild_q_b8<DC>(L[r], st[r], q, a.rk);
         }
         uint32_t rn[DC];                                  // V(L^(k)_mn) + 0x8000
-        new_state<DC, true>(q, a.vk, st[r], rn, a.rk);
+        new_state<DC, true, -1, FMT == FMT_1BIT>(q, a.vk, st[r], rn, a.rk);
         StateIO<FMT>::store(stt + lane, sstride, (size_t)m[r] * 32, st[r]);
 #pragma unroll
         for (int j = 0; j < DC; ++j) atomicAdd(Lat + off[r][j], red_value(rn[j], keep));

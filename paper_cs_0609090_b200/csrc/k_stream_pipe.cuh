@@ -87,12 +87,12 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
             const uint32_t X = sl[8 * 32 + lane];
             st.A = prmt(X, 0u, 0x4240u);
             st.B = prmt(X, 0u, 0x4341u);
-            st.W = sl[9 * 32 + lane];
+            st.W = expand_idx(sl[9 * 32 + lane]);       // index-coded ñ (rowcore.cuh)
         }
         rebuild_q_b8<DC>(L, st, q, a.rk);
     }
     uint32_t rn[DC];                                      // V(L^(k)_mn) + 0x8000
-    new_state<DC, true, VM>(q, a.vk, st, rn, a.rk);
+    new_state<DC, true, VM, FMT == FMT_1BIT>(q, a.vk, st, rn, a.rk);
     StateIO<FMT>::store(stt + lane, sstride, (size_t)m * 32, st);
 #pragma unroll
     for (int j = 0; j < DC; ++j) atomicAdd(Lat + (size_t)cols[j] * 32 + lane, red_value(rn[j], keep));

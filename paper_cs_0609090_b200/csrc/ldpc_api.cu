@@ -66,6 +66,7 @@ struct ldpc_code {
     int N = 0, M = 0;
     int64_t E = 0;
     int max_dc = 0, max_dv = 0;
+    int dc_uniform = 0;              // the row degree when H is row-regular, else 0
     // device CSR (stream kernels)
     int32_t *d_row_ptr = nullptr, *d_col_idx = nullptr;
     uint32_t *d_rowtab = nullptr;   // [M][8] padded column table (streaming kernels)
@@ -198,6 +199,9 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
     c->M = desc->n_checks;
     c->E = desc->row_ptr[c->M];
     for (int m = 0; m < c->M; ++m) c->max_dc = std::max(c->max_dc, desc->row_ptr[m + 1] - desc->row_ptr[m]);
+    c->dc_uniform = c->max_dc;
+    for (int m = 0; m < c->M; ++m)
+        if (desc->row_ptr[m + 1] - desc->row_ptr[m] != c->max_dc) c->dc_uniform = 0;
     for (int n = 0; n < c->N; ++n) c->max_dv = std::max(c->max_dv, coldeg[n]);
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) {
@@ -859,6 +863,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.dcT = natural ? c->d_dcT_lay : c->d_dcT;
     a.cpar = pl.kind == RES_ATOM ? 0xBFFFC000u : 0xFFFEFFFFu;   // -(bias + 1) per lane (atom: bias 0x3FFF)
     a.csr_smem = pl.csr_smem;
+    a.dc_uniform = c->dc_uniform;
     a.csr_dc = c->max_dc;
     a.alpha = pl.alpha;
     a.beta = pl.betaf;

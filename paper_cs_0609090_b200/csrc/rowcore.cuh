@@ -16,6 +16,11 @@
 //            byte2 bit i  : s of edge 2i,   frame hi     byte2 bit 4+i : idx, edge 2i,   hi
 //            byte3 bit i  : s of edge 2i+1, frame hi     byte3 bit 4+i : idx, edge 2i+1, hi
 //          s bit = 1 means L_mn < 0; "idx" bit = 1 means n is an argmin (n = ñ_m).  dc <= 8.
+//   1-bit message format (FMT_1BIT, "1-bit messages"): the persistent W keeps only
+//          the sign bits (the only per-edge datum) and ñ_m as an INDEX per check and frame:
+//          byte0 bits 4-7 = t(ñ_lo), byte2 bits 4-7 = t(ñ_hi), bytes 1, 3 bits 4-7 = 0, with
+//          t(j) = 8 (j & 1) + (j >> 1) -- the position of j's flag in the layout above, so
+//          expand_idx() rebuilds the flags with two shifts when the state is loaded.
 #pragma once
 #include "args.cuh"
 #include "rowcore_types.cuh"
@@ -26,6 +31,14 @@ namespace ldpc {
 struct RowState {
     uint32_t A, B, W;
 };
+
+// index-coded ñ (FMT_1BIT) -> the per-edge flag layout the rebuild reads.  The masks keep
+// the flags inside the frame's own bytes: a tie in the minimum (several flags ORed into t)
+// can only happen when A == B, where the flag does not matter (reading D3).
+__device__ __forceinline__ uint32_t expand_idx(uint32_t W) {
+    const uint32_t tl = (W >> 4) & 15u, th = (W >> 20) & 15u;
+    return (W & 0x0F0F0F0Fu) | ((0x10u << tl) & 0x0000F0F0u) | ((0x100000u << th) & 0xF0F00000u);
+}
 
 // Rebuild L^(k-1)_mn = s f(A, B, n, ñ) and form
 // q_mn = Z^(k-1)_n - L^(k-1)_mn (index reading D8) for all edges.
@@ -168,7 +181,8 @@ __device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const
 // unsigned, the per-lane sign mask is [q >= 0] (bit 15), and the returned messages are
 // "V form + 0x8000": r ^ 0x8000 in the low lane == V(r) + 0x8000 as a 32-bit integer, so a
 // 32-bit RED adds them exactly (the accumulator start value is lowered by dv_n 0x8000).
-template <int DC, bool B8 = false, int VM = -1>
+// IDX = true (FMT_1BIT): ñ is stored as the index code t(ñ) (header), one LOP3 per edge.
+template <int DC, bool B8 = false, int VM = -1, bool IDX = false>
 __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &vk, RowState &st, uint32_t (&r)[DC],
                                           const RegK &k) {
     uint32_t mt[DC];
@@ -206,7 +220,7 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
         Bneg = sel(Pm, Bc, nB);
     }
     const uint32_t cm1 = fnot(m1, k);                           // -m1 - 1
-    uint32_t W = 0, sqp = 0, ixp = 0;
+    uint32_t W = 0, sqp = 0, ixp = 0, tacc = 0;
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         const uint32_t ix = vaddmin(mt[j], cm1, k.zero);          // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
@@ -221,18 +235,20 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
         } else {
             r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
         }
+        if (IDX) tacc |= ix & ((uint32_t)(8 * (j & 1) + (j >> 1)) * 0x00010001u);   // t(j) where n_j = ñ
         if ((j & 1) == 0) {
             sqp = sq;
             ixp = ix;
             if (j == DC - 1) {
                 W |= prmt(sqp, 0u, 0x6240u) & (0x01010101u << (j >> 1));
-                W |= prmt(ixp, 0u, 0x6240u) & (0x10101010u << (j >> 1));
+                if (!IDX) W |= prmt(ixp, 0u, 0x6240u) & (0x10101010u << (j >> 1));
             }
         } else {
             W |= prmt(sqp, sq, 0x6240u) & (0x01010101u << (j >> 1));
-            W |= prmt(ixp, ix, 0x6240u) & (0x10101010u << (j >> 1));
+            if (!IDX) W |= prmt(ixp, ix, 0x6240u) & (0x10101010u << (j >> 1));
         }
     }
+    if (IDX) W |= tacc << 4;                                     // t(ñ_lo) -> byte0 bits 4-7, t(ñ_hi) -> byte2
     if (B8) W ^= ~Pm & 0x0F0F0F0Fu;                             // s = sgn(q) * product ([q>=0] bits stored)
     else W ^= Pm & 0x0F0F0F0Fu;                                 // s = sgn(q) * product
     st.A = A;
@@ -268,7 +284,7 @@ struct StateIO {
             const uint32_t X = __ldcg(base + idx);
             s.A = prmt(X, 0u, 0x4240u);
             s.B = prmt(X, 0u, 0x4341u);
-            s.W = __ldcg(base + stride + idx);
+            s.W = expand_idx(__ldcg(base + stride + idx));
         }
         return s;
     }

@@ -40,9 +40,39 @@ def summarize_launches(csv_path, out_path, workload):
         json.dump({"workload": workload, "kernels": out}, f, indent=1)
 
 
+def top_source_lines(csv_path, out_path, n=40):
+    """The SASS lines with the most warp-stall samples of an ncu --page source --csv export,
+    and the executed-instruction count per opcode (the full export is too large to keep)."""
+    import collections
+    import csv
+    rows = list(csv.reader(open(csv_path)))
+    h = rows[1]
+    data = rows[2:]
+    i_s, i_src, i_ex = h.index("Warp Stall Sampling (All Samples)"), h.index("Source"), h.index("Instructions Executed")
+    tot = sum(float(r[i_s] or 0) for r in data)
+    top = sorted(data, key=lambda r: -float(r[i_s] or 0))[:n]
+    ops = collections.Counter()
+    for r in data:
+        toks = r[i_src].split()
+        if not toks:
+            continue
+        op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+        ops[op.split(".")[0]] += float(r[i_ex] or 0)
+    with open(out_path, "w") as f:
+        json.dump({"kernel": rows[0][1] if len(rows[0]) > 1 else "", "stall_samples_total": tot,
+                   "warp_instructions_executed": sum(ops.values()),
+                   "top_lines": [{"samples": float(r[i_s] or 0), "executed": float(r[i_ex] or 0), "sass": r[i_src]}
+                                 for r in top],
+                   "executed_by_opcode": dict(ops.most_common(40))}, f, indent=1)
+
+
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
+    for name in ("bench", "bench_ref"):               # round 2+: one line with per_config
+        src = os.path.join(MEAS, f"{name}.json")
+        if os.path.exists(src):
+            shutil.copy(src, os.path.join(PROF, f"{tag}_{name}.json"))
     for c in (1, 2, 3, 4, 5):
         src = os.path.join(MEAS, f"bench_cfg{c}.json")
         if os.path.exists(src):
@@ -62,7 +92,11 @@ def main():
                            "cfg2 two-scan (LDPC_SCHED_TWOSCAN), 8192 frames, 15 iterations, early stop; ncu --metrics "
                            "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
                            "(cold-cache, serialised)")
-    for c in (2, 4, 5):
+    frames = {1: 1024, 2: 8192, 3: 16384, 4: 512, 5: 1024}     # frames of the profiled decode (measure_r02.sh)
+    for c in (1, 2, 3, 4, 5):
+        src_csv = os.path.join(MEAS, f"ncu_source_cfg{c}.csv")
+        if os.path.exists(src_csv):
+            top_source_lines(src_csv, os.path.join(PROF, f"{tag}_ncu_source_top_cfg{c}.json"))
         rep = os.path.join(MEAS, f"prof_cfg{c}.ncu-rep")
         pre = os.path.join(MEAS, f"ncu_full_cfg{c}.json")          # summarised on the box
         dst = os.path.join(PROF, f"{tag}_ncu_full_cfg{c}.json")
@@ -78,7 +112,7 @@ def main():
         traffic = (d["dram__bytes_read.sum"] * mb.get(d["dram__bytes_read.sum.unit"], 1.0) +
                    d["dram__bytes_write.sum"] * mb.get(d["dram__bytes_write.sum.unit"], 1.0))
         with open(os.path.join(PROF, f"ncu_traffic_cfg{c}.json"), "w") as f:
-            json.dump({"kernel": d["kernel"], "dram_bytes_per_launch": traffic,
+            json.dump({"kernel": d["kernel"], "dram_bytes_per_launch": traffic, "frames_profiled": frames[c],
                        "source": f"profiles/{tag}_ncu_full_cfg{c}.json (ncu --set full, one launch)",
                        "note": "cfg2: the whole decode is one resident launch; cfg4/5: one iteration launch of "
                                "the streaming kernel"}, f, indent=1)

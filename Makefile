@@ -31,8 +31,18 @@ examples/decode_c: examples/decode_c.c include/ldpc.h $(LIB)
 	gcc -O2 -std=c11 -Wall -Iinclude -I$(CUDA_HOME)/include -o $@ $< -Lpaper_cs_0609090_b200 -lldpc \
 	  -L$(CUDA_HOME)/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../paper_cs_0609090_b200' -Wl,-rpath,$(CUDA_HOME)/lib64
 
+# checked build: device-side bounds checks (LDPC_CHECK in csrc/args.cuh) on the hot loops.
+# LDPC_LIBRARY=$(CURDIR)/build/checked/libldpc.so python -m pytest tests -m gpu
+CHK_OBJS := $(patsubst $(CSRC)/%.cu,build/checked/%.o,$(SRCS))
+build/checked/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build/checked
+	$(NVCC) $(NVFLAGS) -DLDPC_CHECKED -c -o $@ $< 2> build/checked/$*.ptxas.log || (cat build/checked/$*.ptxas.log; false)
+build/checked/libldpc.so: $(CHK_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CHK_OBJS) -lcudart
+checked: build/checked/libldpc.so
+
 clean:
 	rm -f build/*.o $(LIB) oracle/liboracle.so ldpcgen/libldpcgen.so examples/decode_c
 
-.PHONY: all clean
+.PHONY: all clean checked
 $(shell mkdir -p build)

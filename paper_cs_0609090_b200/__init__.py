@@ -16,7 +16,9 @@ from dataclasses import dataclass
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libldpc.so")
+# LDPC_LIBRARY selects another build of the same library (tests: the bounds-checked build,
+# `make checked`); default: the in-tree libldpc.so
+LIB_PATH = os.environ.get("LDPC_LIBRARY") or os.path.join(_HERE, "libldpc.so")
 
 LDPC_OK, LDPC_ERR_INVALID_ARG, LDPC_ERR_INVALID_CODE, LDPC_ERR_UNSUPPORTED, LDPC_ERR_CUDA, LDPC_ERR_NO_MEMORY = range(6)
 LDPC_LLR_I16, LDPC_LLR_I8, LDPC_LLR_F32 = 0, 1, 2

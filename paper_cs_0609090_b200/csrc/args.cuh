@@ -8,6 +8,28 @@
 #include "simd16.cuh"
 #include "rowcore_types.cuh"
 
+// Checked build (make checked -> build/checked/libldpc.so, LDPC_CHECKED defined): device-side
+// bounds checks on every computed address of the hot loops (shared-memory gathers and REDs,
+// TMEM row slots, posterior / state / output indices); a violation prints the condition and
+// traps, so the launch fails with a CUDA error.  compute-sanitizer is closed on this GPU pool
+// (profiles/r02_sanitizer_refusal.log); the GPU test suite run against this build is the
+// memory-safety evidence (profiles/r02_checked_build_tests.log).  Compiled out otherwise.
+#ifdef LDPC_CHECKED
+#include <cstdio>
+#define LDPC_CHECK(cond)                                                                          \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("LDPC_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                            \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define LDPC_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace ldpc {
 
 constexpr int kMaxDC = 8;

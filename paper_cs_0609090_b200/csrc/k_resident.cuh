@@ -87,7 +87,10 @@ __device__ __forceinline__ void res_row(const ResArgs &a, const QcTab &t, const 
     }
     uint32_t L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(op[j]));
+    for (int j = 0; j < DC; ++j) {
+        LDPC_CHECK(op[j] - bp < 4u * (uint32_t)a.N && oa[j] - ba < 4u * (uint32_t)a.N);
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(op[j]));
+    }
     if (ES) synd |= row_parity<DC>(L, a.rk);
     uint32_t q[DC];
     if (first_iter) {
@@ -166,6 +169,7 @@ __device__ __forceinline__ uint32_t res_parity_dispatch(int dc, const ResArgs &a
 static __device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc, int f0, int which, int iters,
                                   int fail_lo, int fail_hi, int bias = 0) {
     const int f1 = f0 + 1;
+    LDPC_CHECK(f0 < a.nframes && (!(which & 2) || f1 < a.nframes));
     const int tid = threadIdx.x, nth = blockDim.x;
     if (a.post) {
         for (int n = tid; n < a.N; n += nth) {

@@ -65,7 +65,10 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
     }
     uint32_t L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
+    for (int j = 0; j < DC; ++j) {
+        LDPC_CHECK(d[j] < 4u * (uint32_t)a.N && (d[j] & 3u) == 0);          // a variable of this code
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
+    }
     if (ES) synd |= atom_row_parity<DC>(L);
     uint32_t q[DC];                                                      // q_mn + 0x8000 per lane
     if (first_iter) {
@@ -170,6 +173,8 @@ __device__ __forceinline__ void atom_row_full_x2(const ResArgs &a, const QcTab &
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L1[j]) : "r"(d1[j] + bp));
     }
     if (ES) synd |= atom_row_parity<DC>(L0) | atom_row_parity<DC>(L1);
+#pragma unroll
+    for (int j = 0; j < DC; ++j) LDPC_CHECK(d0[j] < 4u * (uint32_t)a.N && d1[j] < 4u * (uint32_t)a.N);
     uint32_t q0[DC], q1[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
@@ -225,6 +230,7 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
 #pragma unroll 1
         for (; b < bend; ++b) {
             RowState st = {0u, 0u, 0u};
+            LDPC_CHECK(b < nb && (uint32_t)((FMT == FMT_C16 ? 3 : 2) * nb) <= (uint32_t)a.cols_per_group);
             if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
             if (rloc < a.Z) atom_row<DC, true, ES, VM, FMT>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
             state_tmem_store<FMT>(tw, b, nb, st);

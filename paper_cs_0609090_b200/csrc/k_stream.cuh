@@ -117,7 +117,10 @@ __device__ __forceinline__ void stream_rows_i(const StreamArgs &a, int lane, con
 #pragma unroll
     for (int r = 0; r < NR; ++r)
 #pragma unroll
-        for (int j = 0; j < DC; ++j) off[r][j] = rt[r].c[j] * 32u + (uint32_t)lane;
+        for (int j = 0; j < DC; ++j) {
+            LDPC_CHECK(rt[r].c[j] < (uint32_t)a.N && m[r] < a.M);
+            off[r][j] = rt[r].c[j] * 32u + (uint32_t)lane;
+        }
     const size_t sstride = (size_t)a.M * 32;
     RowState st[NR];
     if (!first_iter) {
@@ -333,6 +336,7 @@ __global__ void __launch_bounds__(256) k_stream_export(const StreamArgs a) {
             for (int fr = 0; fr < 2; ++fr) {
                 const int f = tile * 64 + 2 * lane + fr;
                 if (f >= a.nframes) break;
+                LDPC_CHECK(e0 + dc <= a.E);
                 int16_t *out = (int16_t *)a.msg_out + (size_t)f * a.E + e0;
                 for (int j = 0; j < dc; ++j) {
                     const uint32_t wb = st.W >> (8 * ((j & 1) + 2 * fr));
@@ -436,6 +440,7 @@ __device__ __forceinline__ void stream_rows_f(const StreamArgs &a, int lane, con
         for (int j = 0; j < DC; ++j) {
             // rows of degree <= 8 come with their column table; wider rows read the CSR
             const uint32_t c = DC <= 8 ? rt[r].c[j < 8 ? j : 0] : (uint32_t)__ldg(a.col_idx + __ldg(a.row_ptr + m[r]) + j);
+            LDPC_CHECK(c < (uint32_t)a.N && m[r] < a.M);
             off[r][j] = c * 32u + (uint32_t)lane;
         }
     const size_t ss = (size_t)a.M * 32;

@@ -71,7 +71,10 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
                                            uint32_t keep, uint32_t &synd) {
     uint32_t L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j) L[j] = sl[j * 32 + lane];
+    for (int j = 0; j < DC; ++j) {
+        LDPC_CHECK(cols[j] < (uint32_t)a.N && m < a.M);
+        L[j] = sl[j * 32 + lane];
+    }
     if (ES) synd |= row_parity<DC>(L, a.rk, kParBiased);
     RowState st;
     uint32_t q[DC];                                       // q + 0x8000 per lane
@@ -107,8 +110,10 @@ __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *
     constexpr int SB = PipeCfg<false>::SB;
     float L[DC];
 #pragma unroll
-    for (int j = 0; j < DC; ++j)
+    for (int j = 0; j < DC; ++j) {
+        LDPC_CHECK(cols[j] < (uint32_t)a.N && m < a.M);
         L[j] = FI ? __uint_as_float(sl[j * 32 + lane]) : val_of(((const long long *)sl)[j * 32 + lane]);
+    }
     if (ES) {
         uint32_t p = 0;
 #pragma unroll

@@ -140,7 +140,10 @@ __device__ __forceinline__ void ts_var_col(const StreamArgs &a, const TwoScanArg
     int32_t eid[DV];
     uint32_t mv[DV];
 #pragma unroll
-    for (int b = 0; b < DV; ++b) eid[b] = __ldg(t.vedge + b0 + b);
+    for (int b = 0; b < DV; ++b) {
+        eid[b] = __ldg(t.vedge + b0 + b);
+        LDPC_CHECK(eid[b] >= 0 && eid[b] < t.E);
+    }
     const size_t ni = (size_t)n * 32 + lane;
     uint32_t Z = __ldcg(z0t + ni);
 #pragma unroll

@@ -411,8 +411,10 @@ def measure_config(ctx, cfg, steps, warmup, want_e2e=True):
     if os.path.exists(prof):
         with open(prof) as f:
             pj = json.load(f)
-        roof["traffic"] = pj.get("dram_bytes_per_launch")
-        roof["traffic_source"] = pj.get("source", os.path.relpath(prof, ROOT))
+        fp = pj.get("frames_profiled") or F
+        roof["traffic"] = pj.get("dram_bytes_per_launch") * F / fp      # per launch of this run's batch
+        roof["traffic_source"] = (pj.get("source", os.path.relpath(prof, ROOT)) +
+                                  (f", scaled from {fp} to {F} frames" if fp != F else ""))
     res = {"value": value, "unit": UNIT, "ms_per_step": ms, "edge_updates_per_s": eu_s, "dtype": dtype_name(cfg),
            "workload": describe(cfg, code), "frames_per_gpu": F, "info_bits_per_frame": code.K,
            "mean_iterations": c[4] / (F * ctx.world), "frames_converged": ctx.world * F - c[3],

@@ -236,10 +236,26 @@ def run_dist_check(args, cfg, code, rank, world, local):
     the SUM / MAX all-reduce is checked on rank 0 against the single-process count of all
     frames.  NCCL when CUDA is available, else gloo (CPU)."""
     import torch
+    import torch.distributed as tdist
     from paper_cs_0609090_b200.dist import frame_shard, reduce_counters
     use_cuda = torch.cuda.is_available()
-    dist = init_dist(world, local, use_cuda)
     dev = torch.device("cuda", local) if use_cuda else torch.device("cpu")
+    if use_cuda:
+        torch.cuda.set_device(local)
+    # the process group is created even for one rank, so the NCCL init and all-reduce run on
+    # a single-GPU box too
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    if "MASTER_PORT" not in os.environ:
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+        sk.close()
+    if use_cuda:
+        tdist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    else:
+        tdist.init_process_group("gloo", rank=rank, world_size=world)
+    dist = tdist
     F = args.frames or 16
 
     def counts(f0, nf):
@@ -250,16 +266,19 @@ def run_dist_check(args, cfg, code, rank, world, local):
     f0, nf = frame_shard(rank, world, F)
     c = torch.tensor(counts(f0, nf), dtype=torch.int64, device=dev)
     t = torch.tensor([1.0 + rank], dtype=torch.float64, device=dev)
-    reduce_counters(c, t)
+    if world > 1:
+        reduce_counters(c, t)
+    else:                                              # reduce_counters skips one rank; run the collectives anyway
+        tdist.all_reduce(c, op=tdist.ReduceOp.SUM)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     if rank == 0:
         want = counts(0, F * world)
         got = c.cpu().tolist()
         line = {"dist_check": got == want and float(t.item()) == float(world), "n_ranks": world,
-                "backend": "nccl" if use_cuda else "gloo", "counters": got, "expected": want,
+                "backend": tdist.get_backend(), "counters": got, "expected": want,
                 "max_elapsed": float(t.item()), "frames_per_rank": F}
         print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------- GPU timing

@@ -493,9 +493,10 @@ def test_plain_c_consumer():
     """examples/decode_c.c: the C ABI used from plain C (no Python, no PyTorch) -- code
     creation from a QC shift table, both decode entry points, error counters."""
     import subprocess
-    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "decode_c")
-    if not os.path.exists(exe):
-        pytest.skip("examples/decode_c not built (make examples/decode_c)")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "decode_c")
+    if not os.path.exists(exe):                       # build it (gcc + the in-tree libldpc.so)
+        subprocess.check_call(["make", "-C", root, "examples/decode_c"], stdout=subprocess.DEVNULL)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout

@@ -9,6 +9,8 @@
 // their column tables are staged in shared memory once.  Accumulation into
 // Z^(k) stays a coalesced global RED (fire-and-forget).
 #pragma once
+#include <type_traits>
+
 #include "k_stream.cuh"
 
 namespace ldpc {
@@ -225,39 +227,54 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
         cp_async_commit();
     }
     uint32_t synd = 0;
-    for (int i = 0; i < nmy; ++i) {
-        cp_async_wait<D - 1>();
-        __syncwarp();
-        const int r = warp + i * kPipeWarps;
-        const int m = mb0 + r;
-        const int slot = i % D;
-        const uint32_t *sl = wring + slot * LINES * 32;
-        const uint32_t *cols = coltab + r * 8;
-        const int dc = dctab[r];
-        if (PAIR) {
-            switch (dc) {
+    // the row loop, for one row degree DCF known to the compiler (every row of this warp has
+    // it -- e.g. all but the first block of a DVB-S2-shaped code) or DCF = 0: a switch per row
+    auto row_loop = [&](auto dcf_tag) {
+        constexpr int DCF = decltype(dcf_tag)::value;
+        for (int i = 0; i < nmy; ++i) {
+            cp_async_wait<D - 1>();
+            __syncwarp();
+            const int r = warp + i * kPipeWarps;
+            const int m = mb0 + r;
+            const int slot = i % D;
+            const uint32_t *sl = wring + slot * LINES * 32;
+            const uint32_t *cols = coltab + r * 8;
+            if constexpr (DCF > 0) {
+                if (PAIR) pipe_row_i<DCF, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd);
+                else pipe_row_f<DCF, ES, FI>(a, sl, cols, m, lane, Xat, stt, sstride, frozen, synd);
+            } else {
+                const int dc = dctab[r];
+                if (PAIR) {
+                    switch (dc) {
 #define LDPC_PI(DD) \
-            case DD: pipe_row_i<DD, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
-            LDPC_PI(2) LDPC_PI(3) LDPC_PI(4) LDPC_PI(5) LDPC_PI(6) LDPC_PI(7) LDPC_PI(8)
+                    case DD: pipe_row_i<DD, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd); break;
+                    LDPC_PI(2) LDPC_PI(3) LDPC_PI(4) LDPC_PI(5) LDPC_PI(6) LDPC_PI(7) LDPC_PI(8)
 #undef LDPC_PI
-            }
-        } else {
-            switch (dc) {
+                    }
+                } else {
+                    switch (dc) {
 #define LDPC_PF(DD) \
-            case DD: pipe_row_f<DD, ES, FI>(a, sl, cols, m, lane, Xat, stt, sstride, frozen, synd); break;
-            LDPC_PF(2) LDPC_PF(3) LDPC_PF(4) LDPC_PF(5) LDPC_PF(6) LDPC_PF(7) LDPC_PF(8)
+                    case DD: pipe_row_f<DD, ES, FI>(a, sl, cols, m, lane, Xat, stt, sstride, frozen, synd); break;
+                    LDPC_PF(2) LDPC_PF(3) LDPC_PF(4) LDPC_PF(5) LDPC_PF(6) LDPC_PF(7) LDPC_PF(8)
 #undef LDPC_PF
+                    }
+                }
             }
+            __syncwarp();                                          // slot consumed before it is refilled
+            const int inext = i + D;
+            if (inext < nmy) {
+                const int rn = warp + inext * kPipeWarps;
+                pipe_issue_row<LPV, C::SB>(wring_s + (uint32_t)(slot * LINES * 128), Lsrc, stt, sstride,
+                                           coltab + rn * 8, dctab[rn], nst_copy, mb0 + rn, lane);
+            }
+            cp_async_commit();
         }
-        __syncwarp();                                          // slot consumed before it is refilled
-        const int inext = i + D;
-        if (inext < nmy) {
-            const int rn = warp + inext * kPipeWarps;
-            pipe_issue_row<LPV, C::SB>(wring_s + (uint32_t)(slot * LINES * 128), Lsrc, stt, sstride, coltab + rn * 8,
-                                       dctab[rn], nst_copy, mb0 + rn, lane);
-        }
-        cp_async_commit();
-    }
+    };
+    const int dc0 = nmy > 0 ? dctab[warp] : 0;
+    const bool uniform = __all_sync(0xFFFFFFFFu, lane >= nmy || dctab[warp + lane * kPipeWarps] == dc0);
+    if (uniform && dc0 == 7) row_loop(std::integral_constant<int, 7>{});   // the DVB-S2-shaped codes (cfg4/5)
+    else if (uniform && dc0 == 6) row_loop(std::integral_constant<int, 6>{});
+    else row_loop(std::integral_constant<int, 0>{});
     cp_async_wait<0>();
     if (ES && synd) atomicOr(a.synd + tile * 32 + lane, synd);
 }

@@ -129,3 +129,44 @@ def test_messages_unsupported():
         with pytest.raises(P.LdpcError) as e:
             dec.decode_messages(llr, params)
         assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("i", list(range(40)))
+def test_messages_random(i):
+    """Seeded random sweep of the message export: code shapes of tests/test_gpu_random.py,
+    integer (compact / 1-bit / FULL; resident, streaming pipeline, streaming register
+    kernels) and fp32 (flooding, two-scan), fixed iteration counts."""
+    from test_gpu_random import _code
+    rng = np.random.default_rng(7000 + i)
+    code = _code(rng, i)
+    if int(np.max(np.diff(code.row_ptr))) > 8:
+        pytest.skip("row degree > 8")
+    K = int(rng.integers(1, 16))
+    F = int(rng.choice([1, 3, 64, 65]))
+    s2 = g.ebn0_to_sigma2(float(rng.uniform(0.5, 3.5)), max(code.rate, 0.2))
+    kind = ["compact", "1bit", "full", "stream", "stream-reg", "f32", "f32-ts", "ts"][i % 8]
+    tuning = {"stream": {"path": P.LDPC_PATH_STREAM},
+              "stream-reg": {"path": P.LDPC_PATH_STREAM, "stream_register_kernels": 1}}.get(kind)
+    try:
+        if kind.startswith("f32"):
+            llr = g.llr(int(rng.integers(1, 1 << 30)), 0, F, code.n_vars, s2, g.LLR_F32)
+            sched, engine = (P.LDPC_SCHED_TWOSCAN, "twoscan") if kind == "f32-ts" else (P.LDPC_SCHED_SINGLESCAN, "compact")
+            params = P.make_params(K, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT,
+                                   sched)
+            check(code, llr, params, engine, "f32", K, 0, 0, 0, 0.75)
+        else:
+            onebit = kind == "1bit"
+            Q, lt, gk, frac = (127, P.LDPC_LLR_I8, g.LLR_I8, 2) if onebit else (511, P.LDPC_LLR_I16, g.LLR_I16, 3)
+            max_dv = int(np.max(np.bincount(code.col_idx, minlength=code.n_vars)))
+            if 2 * Q * (max_dv + 2) > 32767:
+                Q = 127
+            llr = g.llr(int(rng.integers(1, 1 << 30)), 0, F, code.n_vars, s2, gk, frac, Q)
+            fmt = {"1bit": P.LDPC_MSG_1BIT, "full": P.LDPC_MSG_FULL}.get(kind, P.LDPC_MSG_COMPACT)
+            sched = P.LDPC_SCHED_TWOSCAN if kind == "ts" else P.LDPC_SCHED_SINGLESCAN
+            engine = {"full": "singlescan", "ts": "twoscan"}.get(kind, "compact")
+            beta = int(rng.integers(0, 3))
+            params = P.make_params(K, 0, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, lt, fmt, sched, tuning=tuning)
+            check(code, llr, params, engine, "int", K, 0, beta, Q)
+    except P.LdpcError as e:
+        assert e.status == P.LDPC_ERR_UNSUPPORTED, str(e)
+        pytest.skip(f"unsupported: {e}")

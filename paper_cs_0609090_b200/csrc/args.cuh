@@ -100,6 +100,11 @@ struct StreamArgs {
     uint32_t *synd;              // [tile][32]: syndrome-fail bits found during the current launch
     uint32_t *done;              // [tile][32]: frames frozen (early stop)
     int32_t *it_ws;              // [tile*TILE] iterations used per frame
+    // fp32 on the pipelined kernel ("delta" accumulation, k_stream_pipe.cuh): the posterior
+    // of iteration k lives in Lb[k & 1] and the compact state of iteration k in plane k & 1
+    // (st, st2); 0 = the three rotating posterior buffers Lb[k % 3] and one state plane
+    int f32delta;
+    uint32_t *st2;
     uint8_t *ok_ws;              // [tile*TILE] syndrome ok per frame (frozen frames)
     uint32_t *hard_bits;
     void *post;

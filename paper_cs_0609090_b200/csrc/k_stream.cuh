@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256) k_stream_syndrome(const StreamArgs a, int
     const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int nwg = gridDim.x * (blockDim.x >> 5);
     const uint32_t *Lp = a.Lb[k % 3];
-    const long long *Xp = (const long long *)a.Lb[k % 3];
+    const long long *Xp = (const long long *)a.Lb[a.f32delta ? (k & 1) : k % 3];
     uint32_t synd = 0;
     for (int m = wg; m < a.M; m += nwg) {
         const int e0 = __ldg(a.row_ptr + m), e1 = __ldg(a.row_ptr + m + 1);
@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(256) k_stream_output(const StreamArgs a) {
             } else {
                 const int f = tile * 32 + lane;
                 const int kk = f < a.nframes ? a.it_ws[f] : a.K;
-                val = kk == 0 ? __ldcg(a.Z0 + idx) : __float_as_uint(val_of(__ldcg((const long long *)a.Lb[kk % 3] + idx)));
+                const int kb = a.f32delta ? (kk & 1) : kk % 3;
+                val = kk == 0 ? __ldcg(a.Z0 + idx) : __float_as_uint(val_of(__ldcg((const long long *)a.Lb[kb] + idx)));
             }
         }
         sh[v][lane] = val;
@@ -325,7 +326,8 @@ template <bool PAIR, int FMT>
 __global__ void __launch_bounds__(256) k_stream_export(const StreamArgs a) {
     const int tile = blockIdx.y, lane = threadIdx.x & 31;
     const int nst = PAIR ? StateIO<FMT>::kWords : 3;
-    const uint32_t *stt = a.st + (size_t)tile * nst * a.M * 32;
+    // fp32 delta accumulation: the state of iteration K is in plane K & 1
+    const uint32_t *stt = (!PAIR && a.f32delta && (a.K & 1) ? a.st2 : a.st) + (size_t)tile * nst * a.M * 32;
     const size_t ss = (size_t)a.M * 32;
     const int nwg = gridDim.x * (blockDim.x >> 5);
     for (int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); m < a.M; m += nwg) {
@@ -390,6 +392,7 @@ __global__ void k_stream_ingest_f(const StreamArgs a) {
         const size_t idx = ((size_t)tile * a.N + n) * 32 + lane;
         a.Z0[idx] = __float_as_uint(z);
         ((long long *)a.Lb[1])[idx] = grid_of(z);
+        if (a.f32delta) ((long long *)a.Lb[0])[idx] = grid_of(z);   // X_0: iteration 2's plane
     }
 }
 

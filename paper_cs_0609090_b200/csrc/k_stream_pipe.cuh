@@ -31,12 +31,13 @@ constexpr int kPipeRB = LDPC_PIPE_RB;   // rows per CTA
 constexpr int kPipeWarps = 8;      // warps per CTA
 // Ring slot of one row.  Integer pairs: 8 posterior lines (one 128-byte line of 32 lanes per
 // variable) + up to 3 state lines, kPipeD rows in flight.  fp32 (reading D28): a posterior is
-// an int64 grid value, two lines per variable: 16 + 3 lines, kPipeDF rows in flight (the
-// first iteration reads the fp32 Z^(0) plane, one line per variable).
+// an int64 grid value, two lines per variable: 16 lines, + 3 lines of the state of iteration
+// k-1 + 3 of iteration k-2 (the delta accumulation below), kPipeDF rows in flight (the first
+// iteration reads the fp32 Z^(0) plane, one line per variable).
 template <bool PAIR> struct PipeCfg {
     static constexpr int LPV = PAIR ? 1 : 2;          // lines per variable (later iterations)
     static constexpr int SB = 8 * LPV;                // first state line
-    static constexpr int LINES = SB + 3;
+    static constexpr int LINES = PAIR ? SB + 3 : SB + 6;
     static constexpr int D = PAIR ? LDPC_PIPE_D : LDPC_PIPE_DF;
 };
 
@@ -53,7 +54,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // (lane >> 3) + 4 s; branch-free source selection, predicated copies.
 template <int LPV, int SB>
 __device__ __forceinline__ void pipe_issue_row(uint32_t slot, const char *Lpt, const uint32_t *stt, size_t sstride,
-                                               const uint32_t *cols, int dc, int nst, int m, int lane) {
+                                               const uint32_t *cols, int dc, int nst, int m, int lane,
+                                               const uint32_t *stt2 = nullptr, int nst2 = 0) {
     const int chunk = lane & 7, l0 = lane >> 3;
 #pragma unroll
     for (int step = 0; step < 2 * LPV; ++step) {         // posterior lines
@@ -64,6 +66,10 @@ __device__ __forceinline__ void pipe_issue_row(uint32_t slot, const char *Lpt, c
     if (l0 < nst) {                                        // state lines
         const char *src = (const char *)(stt + (size_t)m * 32) + chunk * 16 + (size_t)l0 * sstride * 4;
         cp_async16(slot + (uint32_t)((SB + l0) * 128 + chunk * 16), src);
+    }
+    if (l0 < nst2) {                                       // fp32 delta: the state two iterations back
+        const char *src = (const char *)(stt2 + (size_t)m * 32) + chunk * 16 + (size_t)l0 * sstride * 4;
+        cp_async16(slot + (uint32_t)((SB + 3 + l0) * 128 + chunk * 16), src);
     }
 }
 
@@ -104,11 +110,19 @@ __device__ __forceinline__ void pipe_row_i(const StreamArgs &a, const uint32_t *
 }
 
 // fp32 row (reading D11 arithmetic, D28 exact accumulation): posteriors from the ring
-// (FI: fp32 Z^(0) lines; later: int64 grid values, rounded to fp32 here)
+// (FI: fp32 Z^(0) lines; later: int64 grid values, rounded to fp32 here).
+// Delta accumulation (a.f32delta): the plane of iteration k held the exact sum of iteration
+// k-2, X_{k-2} = grid(Z^(0)) + sum_m grid(L^(k-2)_mn), so adding grid(L^(k)_mn) -
+// grid(L^(k-2)_mn) for every edge leaves X_k = grid(Z^(0)) + sum_m grid(L^(k)_mn) -- the same
+// exact integer as a fresh accumulation (integer addition is exact and associative), with no
+// accumulator start to write: two posterior planes and two state planes instead of three
+// posterior planes, and no DRAM round trip of start values written one iteration ahead.
+// L^(k-2) is rebuilt from the state two iterations back (OLD2 = k >= 3; iterations 1 and 2
+// start from grid(Z^(0)) written by the ingest into both planes).
 template <int DC, bool ES, bool FI>
 __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *sl, const uint32_t *cols, int m,
                                            int lane, long long *Xat, uint32_t *stt, size_t ss, bool frozen,
-                                           uint32_t &synd) {
+                                           uint32_t &synd, bool old2 = false) {
     constexpr int SB = PipeCfg<false>::SB;
     float L[DC];
 #pragma unroll
@@ -137,9 +151,21 @@ __device__ __forceinline__ void pipe_row_f(const StreamArgs &a, const uint32_t *
     __stcg(stt + ss + so, __float_as_uint(B));
     __stcg(stt + 2 * ss + so, Wn);
     if (!frozen) {
+        if (old2) {
+            const uint32_t a2 = sl[(SB + 3) * 32 + lane], db2 = sl[(SB + 4) * 32 + lane] - a2;
+            const uint32_t W2 = sl[(SB + 5) * 32 + lane];
 #pragma unroll
-        for (int j = 0; j < DC; ++j)                                      // Z^(k)_n += L^(k)_mn, exact
-            atomicAdd((unsigned long long *)(Xat + (size_t)cols[j] * 32 + lane), (unsigned long long)grid_of(r[j]));
+            for (int j = 0; j < DC; ++j) {                                // + L^(k)_mn - L^(k-2)_mn, exact
+                const uint32_t mag = ((W2 << (15 - j)) >> 31) * db2 + a2;    // f(A,B,n,ñ) of iteration k-2
+                const float r2 = __uint_as_float(mag ^ ((W2 << (31 - j)) & 0x80000000u));
+                atomicAdd((unsigned long long *)(Xat + (size_t)cols[j] * 32 + lane),
+                          (unsigned long long)(grid_of(r[j]) - grid_of(r2)));
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < DC; ++j)                                  // Z^(k)_n += L^(k)_mn, exact
+                atomicAdd((unsigned long long *)(Xat + (size_t)cols[j] * 32 + lane), (unsigned long long)grid_of(r[j]));
+        }
     }
 }
 
@@ -160,12 +186,16 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
     const uint32_t *Lpt = a.Lb[(k - 1) % 3] + plane;
     uint32_t *Lat = a.Lb[k % 3] + plane;
     uint32_t *Lnt = a.Lb[(k + 1) % 3] + plane;
-    long long *Xat = (long long *)a.Lb[k % 3] + plane;
-    long long *Xnt = (long long *)a.Lb[(k + 1) % 3] + plane;
+    // fp32 (delta accumulation, pipe_row_f): posterior of iteration k in Lb[k & 1], compact
+    // state of iteration k in plane k & 1 (st / st2); the rows read the state of k-1 and of
+    // k-2 and overwrite the latter
+    long long *Xat = (long long *)a.Lb[k & 1] + plane;
     const char *Lsrc = PAIR ? (const char *)Lpt
-                            : (FI ? (const char *)(a.Z0 + plane) : (const char *)((const long long *)a.Lb[(k - 1) % 3] + plane));
+                            : (FI ? (const char *)(a.Z0 + plane) : (const char *)((const long long *)a.Lb[(k - 1) & 1] + plane));
     const int nst = PAIR ? StateIO<FMT>::kWords : 3;
-    uint32_t *stt = a.st + (size_t)tile * nst * a.M * 32;
+    uint32_t *stt = (PAIR ? a.st : ((k & 1) ? a.st2 : a.st)) + (size_t)tile * nst * a.M * 32;   // written (and k-2)
+    const uint32_t *stt_prev = (PAIR ? a.st : ((k & 1) ? a.st : a.st2)) + (size_t)tile * nst * a.M * 32;   // k-1
+    const bool old2 = !PAIR && k >= 3;
     const size_t sstride = (size_t)a.M * 32;
     // compact row tables of this warp's rows -> its part of shared memory (one 32 B entry
     // per row); warp-local, so no CTA barrier before the row pipeline starts
@@ -188,15 +218,12 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
         if (PAIR) keep = ((d & 1) ? 0x0000FFFFu : 0u) | ((d & 2) ? 0xFFFF0000u : 0u);
         else frozen = (d & 1u) != 0;
     }
-    // accumulator of the next iteration (it held Z^(k-2); not touched otherwise by this
-    // launch: no barrier needed)
-    if (k < a.K) {
+    // integer pairs: the accumulator of the next iteration (it held Z^(k-2); not touched
+    // otherwise by this launch: no barrier needed); fp32 needs none (delta accumulation)
+    if (PAIR && k < a.K) {
         const int wg = blockIdx.x * kPipeWarps + warp, nwg = gridDim.x * kPipeWarps;
-        const bool any_frozen = ES && __any_sync(0xFFFFFFFFu, keep != 0 || frozen);
-        if (!PAIR) {
-            if (!any_frozen) stream_init_next_f(a.Z0 + plane, Xnt, a.N, wg, nwg, lane);
-            else stream_init_next_f_lanes(a.Z0 + plane, Xnt, a.N, wg, nwg, lane, frozen);
-        } else if (!any_frozen) {
+        const bool any_frozen = ES && __any_sync(0xFFFFFFFFu, keep != 0);
+        if (!any_frozen) {
             stream_init_next(a.Z0 + plane, Lnt, a.N, wg, nwg, lane);
         } else {
             for (int n = wg; n < a.N; n += nwg) {
@@ -221,8 +248,8 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
     for (int i = 0; i < D; ++i) {
         if (i < nmy) {
             const int r = warp + i * kPipeWarps;
-            pipe_issue_row<LPV, C::SB>(wring_s + (uint32_t)(i * LINES * 128), Lsrc, stt, sstride, coltab + r * 8,
-                                       dctab[r], nst_copy, mb0 + r, lane);
+            pipe_issue_row<LPV, C::SB>(wring_s + (uint32_t)(i * LINES * 128), Lsrc, stt_prev, sstride, coltab + r * 8,
+                                       dctab[r], nst_copy, mb0 + r, lane, stt, old2 ? 3 : 0);
         }
         cp_async_commit();
     }
@@ -241,7 +268,7 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
             const uint32_t *cols = coltab + r * 8;
             if constexpr (DCF > 0) {
                 if (PAIR) pipe_row_i<DCF, FMT, ES, VM>(a, sl, cols, m, lane, Lat, stt, sstride, first_iter, keep, synd);
-                else pipe_row_f<DCF, ES, FI>(a, sl, cols, m, lane, Xat, stt, sstride, frozen, synd);
+                else pipe_row_f<DCF, ES, FI>(a, sl, cols, m, lane, Xat, stt, sstride, frozen, synd, old2);
             } else {
                 const int dc = dctab[r];
                 if (PAIR) {
@@ -254,7 +281,7 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
                 } else {
                     switch (dc) {
 #define LDPC_PF(DD) \
-                    case DD: pipe_row_f<DD, ES, FI>(a, sl, cols, m, lane, Xat, stt, sstride, frozen, synd); break;
+                    case DD: pipe_row_f<DD, ES, FI>(a, sl, cols, m, lane, Xat, stt, sstride, frozen, synd, old2); break;
                     LDPC_PF(2) LDPC_PF(3) LDPC_PF(4) LDPC_PF(5) LDPC_PF(6) LDPC_PF(7) LDPC_PF(8)
 #undef LDPC_PF
                     }
@@ -264,8 +291,8 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
             const int inext = i + D;
             if (inext < nmy) {
                 const int rn = warp + inext * kPipeWarps;
-                pipe_issue_row<LPV, C::SB>(wring_s + (uint32_t)(slot * LINES * 128), Lsrc, stt, sstride,
-                                           coltab + rn * 8, dctab[rn], nst_copy, mb0 + rn, lane);
+                pipe_issue_row<LPV, C::SB>(wring_s + (uint32_t)(slot * LINES * 128), Lsrc, stt_prev, sstride,
+                                           coltab + rn * 8, dctab[rn], nst_copy, mb0 + rn, lane, stt, old2 ? 3 : 0);
             }
             cp_async_commit();
         }

@@ -558,6 +558,8 @@ struct Plan {
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
     size_t off_msg = 0, off_zv = 0, off_hb = 0;   // two-scan: per-edge L_mn and Z_mn planes, hard-bit ballots
     size_t ws_bytes = 0;
+    bool f32delta = false;       // fp32 delta accumulation (second state plane at off_st2)
+    size_t off_st2 = 0;
     ldpc_tuning tn{};            // the call's plan overrides (zero = automatic)
 };
 
@@ -822,6 +824,11 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         } else {
             pl.off_st = off; off += align256((size_t)pl.ntiles * sw * c->M * 32 * 4);
         }
+        // fp32 single-scan on the pipelined kernel (row degree <= 8): the delta accumulation
+        // keeps a second compact-state plane (k_stream_pipe.cuh)
+        pl.f32delta = pl.path == PATH_STREAM_F && pl.sched == LDPC_SCHED_SINGLESCAN && c->max_dc <= 8 &&
+                      pl.tn.stream_register_kernels != 1;
+        if (pl.f32delta) { pl.off_st2 = off; off += align256((size_t)pl.ntiles * sw * c->M * 32 * 4); }
         pl.off_synd = off; off += align256((size_t)pl.ntiles * 32 * 4);
         pl.off_done = off; off += align256((size_t)pl.ntiles * 32 * 4);
         pl.off_it = off; off += align256((size_t)pl.ntiles * pl.tile * 4);
@@ -914,6 +921,8 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     a.Z0 = (uint32_t *)(w + pl.off_z0);
     for (int i = 0; i < 3; ++i) a.Lb[i] = (uint32_t *)(w + pl.off_lb[i]);
     a.st = (uint32_t *)(w + pl.off_st);
+    a.f32delta = pl.f32delta ? 1 : 0;
+    a.st2 = pl.f32delta ? (uint32_t *)(w + pl.off_st2) : nullptr;
     a.synd = (uint32_t *)(w + pl.off_synd);
     a.done = (uint32_t *)(w + pl.off_done);
     a.it_ws = (int32_t *)(w + pl.off_it);

@@ -100,6 +100,9 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
     // unless the register kernels are requested (tuning cross-check)
     const unsigned fgrid = (unsigned)((r.ntiles * 32 + 255) / 256);
     const bool use_pipe = r.max_dc <= 8 && !r.register_kernels;
+    // fp32 on the pipelined kernel uses the delta accumulation (k_stream_pipe.cuh); the
+    // planner laid out the second state plane for exactly that case
+    if (!pair && use_pipe != (a.f32delta != 0)) return cudaErrorInvalidValue;
     const size_t psmem = pair ? pipe_smem_bytes<true>() : pipe_smem_bytes<false>();
     if (use_pipe && (e = pipe_prepare()) != cudaSuccess) return e;
     // Frame tiles are decoded in CHUNKS whose per-iteration working set (Z^(0), the three
@@ -118,6 +121,7 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
         c.Z0 = a.Z0 + plane;
         for (int i = 0; i < 3; ++i) c.Lb[i] = a.Lb[i] + (pair ? plane : 2 * plane);   // fp32: int64 planes
         c.st = a.st + (size_t)t0 * nst * a.M * 32;
+        if (a.st2) c.st2 = a.st2 + (size_t)t0 * nst * a.M * 32;
         c.synd = a.synd + (size_t)t0 * 32;
         c.done = a.done + (size_t)t0 * 32;
         c.it_ws = a.it_ws + (size_t)t0 * tw;

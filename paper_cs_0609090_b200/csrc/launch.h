@@ -2,9 +2,24 @@
 // stream_launch.cu), called by the planner in ldpc_api.cu.  Split so the kernel
 // instantiations compile in parallel.
 #pragma once
+#include <mutex>
+
 #include "args.cuh"
 
 namespace ldpc {
+
+// Run f() once per CUDA device (function attributes are per device context): the first call
+// made with device d current runs it, later calls on d return its result.
+constexpr int kMaxDevices = 64;
+template <typename F>
+cudaError_t once_per_device(std::once_flag (&flags)[kMaxDevices], cudaError_t (&errs)[kMaxDevices], F f) {
+    int dev = 0;
+    const cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return f();
+    std::call_once(flags[dev], [&] { errs[dev] = f(); });
+    return errs[dev];
+}
 
 // Resident kernels.  i8 selects int8 channel LLRs (else int16).  kind: RES_BATCHED
 // (k_resident.cuh, flooding in conflict-free batches), RES_LAYERED (k_resident.cuh,

@@ -25,11 +25,11 @@ struct Kern {
     // (it is only a cap: occupancy follows the size each launch asks for), so concurrent
     // host threads never race on the attribute.
     static cudaError_t prepare() {
-        static std::once_flag once;
-        static cudaError_t err = cudaSuccess;
-        std::call_once(once, [] {
+        static std::once_flag flags[kMaxDevices];
+        static cudaError_t errs[kMaxDevices];
+        return once_per_device(flags, errs, [] {
             int dev = 0, optin = 0;
-            err = cudaGetDevice(&dev);
+            cudaError_t err = cudaGetDevice(&dev);
             if (err == cudaSuccess) err = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
             cudaFuncAttributes fa;
             if (err == cudaSuccess) err = cudaFuncGetAttributes(&fa, get());
@@ -37,8 +37,8 @@ struct Kern {
             if (err == cudaSuccess)
                 err = cudaFuncSetAttribute(get(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            optin - (int)fa.sharedSizeBytes);
+            return err;
         });
-        return err;
     }
 };
 

@@ -54,10 +54,11 @@ void set_iteration(StreamArgs &c, const StreamRun &r, int k) {
 // raise the dynamic shared memory cap of the pipelined kernels once (a cap only; each
 // launch asks for its own size), so concurrent host threads never race on the attribute
 cudaError_t pipe_prepare() {
-    static std::once_flag once;
-    static cudaError_t err = cudaSuccess;
-    std::call_once(once, [] {
-        auto set = [](auto kern, size_t bytes) {
+    static std::once_flag flags[kMaxDevices];
+    static cudaError_t errs[kMaxDevices];
+    return once_per_device(flags, errs, [] {
+        cudaError_t err = cudaSuccess;
+        auto set = [&err](auto kern, size_t bytes) {
             if (err == cudaSuccess) err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         };
         set(k_stream_pipe<true, FMT_C16, true>, pipe_smem_bytes<true>());
@@ -66,8 +67,8 @@ cudaError_t pipe_prepare() {
         set(k_stream_pipe<true, FMT_1BIT, false>, pipe_smem_bytes<true>());
         set(k_stream_pipe<false, FMT_C16, true>, pipe_smem_bytes<false>());
         set(k_stream_pipe<false, FMT_C16, false>, pipe_smem_bytes<false>());
+        return err;
     });
-    return err;
 }
 }  // namespace
 

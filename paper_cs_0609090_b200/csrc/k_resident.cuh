@@ -197,7 +197,22 @@ static __device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc,
 
 // TMEM columns of batch b for this thread: FMT_C16 uses (A,B) at 2b and W at 2*nb + b;
 // FMT_1BIT uses (X, W) at 2b.
-template <int FMT>
+// Index-coded ñ (FMT_1BIT) -> per-edge flags with a shared-memory table instead of shifts
+// (expand_idx): the byte offset of the lo frame's entry is the W nibble holding t(ñ_lo) as it
+// stands (16-byte stride), the hi frame's entry sits 256 bytes on.  A kernel that loads state
+// with TAB = true fills the table first (idx_tab_fill, before its first barrier).
+static __shared__ __align__(16) uint32_t g_idx_tab[128];
+__device__ __forceinline__ void idx_tab_fill() {
+    const int t = threadIdx.x;
+    if (t < 32) g_idx_tab[4 * t] = t < 16 ? (0x10u << t) & 0x0000F0F0u : (0x100000u << (t - 16)) & 0xF0F00000u;
+}
+__device__ __forceinline__ uint32_t expand_idx_tab(uint32_t W) {
+    const uint32_t ol = *(const uint32_t *)((const char *)g_idx_tab + (W & 0xF0u));
+    const uint32_t oh = *(const uint32_t *)((const char *)g_idx_tab + 256 + ((W >> 16) & 0xF0u));
+    return (W & 0x0F0F0F0Fu) | ol | oh;
+}
+
+template <int FMT, bool TAB = false>
 __device__ __forceinline__ void state_tmem_load(uint32_t tw, int b, int nb, RowState &st) {
     if (FMT == FMT_C16) {
         tmem_ld2(tw + 2 * b, st.A, st.B);
@@ -209,7 +224,7 @@ __device__ __forceinline__ void state_tmem_load(uint32_t tw, int b, int nb, RowS
         tmem_wait_ld_dep(X, st.W, st.W);
         st.A = prmt(X, 0u, 0x4240u);
         st.B = prmt(X, 0u, 0x4341u);
-        st.W = expand_idx(st.W);                 // index-coded ñ (rowcore.cuh)
+        st.W = TAB ? expand_idx_tab(st.W) : expand_idx(st.W);   // index-coded ñ (rowcore.cuh)
     }
 }
 template <int FMT>

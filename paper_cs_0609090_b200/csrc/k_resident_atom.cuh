@@ -231,7 +231,7 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
         for (; b < bend; ++b) {
             RowState st = {0u, 0u, 0u};
             LDPC_CHECK(b < nb && (uint32_t)((FMT == FMT_C16 ? 3 : 2) * nb) <= (uint32_t)a.cols_per_group);
-            if (!first_iter) state_tmem_load<FMT>(tw, b, nb, st);
+            if (!first_iter) state_tmem_load<FMT, true>(tw, b, nb, st);
             if (rloc < a.Z) atom_row<DC, true, ES, VM, FMT>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
             state_tmem_store<FMT>(tw, b, nb, st);
         }
@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
     const uint32_t r4 = 4u * (uint32_t)rloc;
     const int nb = QC ? t.nsb : a.nbatch;                // row slots per thread
     if (tid == 0) mbar_init(&zbar, 1);
+    if (FMT == FMT_1BIT) idx_tab_fill();                          // state_tmem_load<FMT, true>
     const uint32_t tbase = tmem_alloc_cta(&tslot, a.tmem_cols);   // includes a block barrier
     const uint32_t tw = tmem_warp_base(tbase) + (uint32_t)((tid >> 7) * a.cols_per_group);
     uint32_t *z0w = a.ws + (size_t)blockIdx.x * a.slot_words;
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
                         for (int b = 0; b < nb; ++b) {
                             const int p = b * nth + tid;
                             RowState st = {0u, 0u, 0u};
-                            if (!FI) state_tmem_load<FMT>(tw, b, nb, st);
+                            if (!FI) state_tmem_load<FMT, true>(tw, b, nb, st);
                             if (p < a.M)
                                 atom_row<DC, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, FI, st, synd, sct);
                             state_tmem_store<FMT>(tw, b, nb, st);
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
                             full_tmem_store<8>(tw + 8u * b, c);
                         } else {
                             RowState st = {0u, 0u, 0u};
-                            if (!FI) state_tmem_load<FMT>(tw, b, nb, st);
+                            if (!FI) state_tmem_load<FMT, true>(tw, b, nb, st);
                             if (p < a.M) atom_csr_dispatch<ES, VM, FMT, CSM>(a.dcT[p], a, t, vk, bp, ba, p, FI, st, synd, sct);
                             state_tmem_store<FMT>(tw, b, nb, st);
                         }

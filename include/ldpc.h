@@ -115,10 +115,13 @@ enum { LDPC_MSG_COMPACT = 0, LDPC_MSG_1BIT = 1,
  *               before it (layered / Gauss-Seidel schedule, reading D25).  Not
  *               equivalent to two-scan; usually converges in fewer iterations.  The row
  *               order of H defines the schedule (QC codes: base row by base row).
- *               Requires the resident kernel (a frame's N posteriors in shared
- *               memory, e.g. N <= ~27000), row degree <= 8 and at most 256 consecutive
- *               variable-disjoint rows per batch, else LDPC_ERR_UNSUPPORTED.  Integer and
- *               F32 LLRs (F32 layered is bit-exact with a sequential implementation). */
+ *               Codes whose posteriors fit in shared memory (e.g. N <= ~27000) run on the
+ *               resident kernel; longer codes (and tuning.path = LDPC_PATH_STREAM) on the
+ *               streaming layered kernel: one warp per 64-frame (F32: 32-frame) tile walks
+ *               the rows in order -- correct at any size but latency-bound (the schedule is
+ *               a chain of M dependent row updates per frame), constant
+ *               variant only.  Row degree <= 8, else LDPC_ERR_UNSUPPORTED.  Integer and F32
+ *               LLRs (F32 layered is bit-exact with a sequential implementation). */
 enum { LDPC_SCHED_SINGLESCAN = 0, LDPC_SCHED_TWOSCAN = 1, LDPC_SCHED_LAYERED = 2 };
 
 /* Optional plan overrides (kernel cross-checks and tuning).  A NULL ldpc_decode_params.tuning

@@ -105,6 +105,8 @@ struct StreamArgs {
     // (st, st2); 0 = the three rotating posterior buffers Lb[k % 3] and one state plane
     int f32delta;
     uint32_t *st2;
+    int layered;                 // LDPC_SCHED_LAYERED on the streaming layout (k_stream_layered.cuh): one
+                                 // posterior plane Lb[0], integer biased / fp32 plain floats
     uint8_t *ok_ws;              // [tile*TILE] syndrome ok per frame (frozen frames)
     uint32_t *hard_bits;
     void *post;

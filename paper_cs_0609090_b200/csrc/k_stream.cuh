@@ -278,14 +278,15 @@ __global__ void __launch_bounds__(256) k_stream_output(const StreamArgs a) {
                 const int f0 = tile * 64 + 2 * lane;
                 const int k0 = f0 < a.nframes ? a.it_ws[f0] : a.K;
                 const int k1 = f0 + 1 < a.nframes ? a.it_ws[f0 + 1] : a.K;
-                val = vadd(__ldcg(a.Lb[k0 % 3] + idx), 0xC000C000u);    // unbias
-                val2 = vadd(__ldcg(a.Lb[k1 % 3] + idx), 0xC000C000u);
+                val = vadd(__ldcg(a.Lb[a.layered ? 0 : k0 % 3] + idx), 0xC000C000u);    // unbias
+                val2 = vadd(__ldcg(a.Lb[a.layered ? 0 : k1 % 3] + idx), 0xC000C000u);
                 val = (val & 0xFFFFu) | (val2 & 0xFFFF0000u);
             } else {
                 const int f = tile * 32 + lane;
                 const int kk = f < a.nframes ? a.it_ws[f] : a.K;
                 const int kb = a.f32delta ? (kk & 1) : kk % 3;
-                val = kk == 0 ? __ldcg(a.Z0 + idx) : __float_as_uint(val_of(__ldcg((const long long *)a.Lb[kb] + idx)));
+                if (a.layered) val = __ldcg(a.Lb[0] + idx);               // plain fp32 (D25 / D11)
+                else val = kk == 0 ? __ldcg(a.Z0 + idx) : __float_as_uint(val_of(__ldcg((const long long *)a.Lb[kb] + idx)));
             }
         }
         sh[v][lane] = val;
@@ -393,6 +394,7 @@ __global__ void k_stream_ingest_f(const StreamArgs a) {
         a.Z0[idx] = __float_as_uint(z);
         ((long long *)a.Lb[1])[idx] = grid_of(z);
         if (a.f32delta) ((long long *)a.Lb[0])[idx] = grid_of(z);   // X_0: iteration 2's plane
+        if (a.layered) a.Lb[0][idx] = __float_as_uint(z);             // the one in-place array (D25)
     }
 }
 

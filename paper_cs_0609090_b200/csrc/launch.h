@@ -40,6 +40,7 @@ struct StreamRun {
     int max_iter, max_dc, ntiles;
     int chunk_tiles;      // tiles decoded together through all iterations (0 = all)
     bool register_kernels;  // integer / fp32 rows of degree <= 8: register kernels instead of the pipeline
+    bool layered;           // LDPC_SCHED_LAYERED on the streaming layout (k_stream_layered.cuh)
     size_t flags_bytes;   // bytes from a.synd to the end of the per-tile flag words (zeroed first)
     // per-iteration variants (host arrays of max_iter entries, NULL = the constants in a)
     const VarK *vk_sched;

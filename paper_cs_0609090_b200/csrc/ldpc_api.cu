@@ -650,16 +650,20 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         // accumulation (reading D28) is order-free; the layered schedule is resident
         pl.path = PATH_STREAM_F;
         if (pl.sched == LDPC_SCHED_LAYERED) {
-            // layered schedule (D25): resident only (k_resident_f32_lay, one posterior array)
-            if (!c->res_ok || c->max_dc > kMaxDC)
-                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule needs a code whose posteriors fit in shared memory "
-                                                  "(the resident kernel) and row degree <= %d", kMaxDC);
-            if (c->res_threads_lay > 256) return fail(LDPC_ERR_UNSUPPORTED, "layered batches wider than 256 rows");
-            if (!pl.alphas.empty() && p->max_iter > kMaxSched)
-                return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
-            pl.path = PATH_RESIDENT;
+            // layered schedule (D25): resident (k_resident_f32_lay, one posterior array) when the
+            // code fits, else (or with tuning.path = STREAM) the streaming layered kernel
+            if (c->max_dc > kMaxDC)
+                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule supports row degree <= %d", kMaxDC);
             pl.lay = true;
-            pl.kind = RES_F32_LAY;
+            if (c->res_ok && c->res_threads_lay <= 256 && pl.tn.path != LDPC_PATH_STREAM) {
+                if (!pl.alphas.empty() && p->max_iter > kMaxSched)
+                    return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
+                pl.path = PATH_RESIDENT;
+                pl.kind = RES_F32_LAY;
+            } else if (!pl.alphas.empty()) {
+                return fail(LDPC_ERR_UNSUPPORTED, "the streaming layered kernel takes a constant variant "
+                                                  "(no per-iteration schedules)");
+            }
         }
         pl.tile = 32;
     } else if (p->llr_type == LDPC_LLR_I16 || p->llr_type == LDPC_LLR_I8) {
@@ -704,13 +708,19 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
             return fail(LDPC_ERR_UNSUPPORTED, "streaming integer decode needs 2*Q*(max_dv+1) < 16384 (Q=%d, max_dv=%d)",
                         pl.Q, c->max_dv);
         if (pl.sched == LDPC_SCHED_LAYERED) {
-            if (!c->res_ok)
-                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule needs a code whose posteriors fit in shared memory "
-                                                  "(the resident kernel); N=%d is too long", c->N);
-            if (c->res_threads_lay > 256)
-                return fail(LDPC_ERR_UNSUPPORTED, "layered batches wider than 256 rows");
-            pl.path = PATH_RESIDENT;
+            // resident layered kernel when the code fits on chip, else (or with tuning.path =
+            // STREAM) the streaming layered kernel (k_stream_layered.cuh: one warp per frame tile)
             pl.lay = true;
+            if (c->res_ok && c->res_threads_lay <= 256 && pl.tn.path != LDPC_PATH_STREAM) {
+                pl.path = PATH_RESIDENT;
+            } else {
+                pl.path = PATH_STREAM_I;
+                if ((int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
+                    return fail(LDPC_ERR_UNSUPPORTED, "streaming layered decode needs 2*Q*(max_dv+1) < 16384");
+                if (!pl.vks.empty())
+                    return fail(LDPC_ERR_UNSUPPORTED, "the streaming layered kernel takes a constant variant "
+                                                      "(no per-iteration schedules)");
+            }
         }
         pl.tile = 64;
     } else {
@@ -745,23 +755,24 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         // general codes keep the state in shared memory instead ([3][M] words, by row)
         pl.cols_per_group = (pl.fmt == FMT_C16 ? 3 : 2) * pl.nbatch;
         if (pl.fmt == FMT_FULL) pl.cols_per_group = c->qc ? c->full_cols_qc : 8 * pl.nbatch;   // one word per edge
+        bool lay_smem_over = false;
         if (pl.lay && !c->qc) {
             pl.cols_per_group = 0;
             pl.smem += (size_t)3 * c->M * 4;
-            if (pl.smem > c->smem_optin)
-                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule: posteriors + state (%zu B) exceed shared memory",
-                            pl.smem);
+            lay_smem_over = pl.smem > c->smem_optin;   // -> the streaming layered kernel below
         }
         const int groups = (pl.threads + 127) / 128;   // 128-thread TMEM lane slices
         uint32_t need = (uint32_t)(pl.cols_per_group * groups), cols = 32;
         while (cols < need) cols <<= 1;
         pl.tmem_cols_needed = cols;
-        if (cols > 512) {
+        if (cols > 512 || lay_smem_over) {
             // more check rows per thread than an SM's 512 TMEM columns can hold state for:
             // the streaming kernels (state in HBM) take the decode where they apply
-            if (pl.lay || pl.fmt == FMT_FULL)
-                return fail(LDPC_ERR_UNSUPPORTED, "%s needs %u TMEM columns (> 512)",
-                            pl.lay ? "layered schedule" : "full per-edge messages", need);
+            if (pl.fmt == FMT_FULL)
+                return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages need %u TMEM columns (> 512)", need);
+            if (pl.lay && (!pl.vks.empty() || !pl.alphas.empty()))
+                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule: the compact state does not fit on chip and the "
+                                                  "streaming layered kernel takes no per-iteration schedules");
             const bool f32 = p->llr_type == LDPC_LLR_F32;
             if (!f32 && (int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
                 return fail(LDPC_ERR_UNSUPPORTED, "compact state needs %u TMEM columns (> 512) and the streaming "
@@ -948,6 +959,8 @@ cudaError_t run_stream(const ldpc_code *c, const Plan &pl, const ldpc_decode_par
     // bound, not HBM-bound, and chunks add launch tails), so all tiles run together by default.
     r.chunk_tiles = pl.tn.stream_chunk_tiles;
     r.register_kernels = pl.tn.stream_register_kernels == 1;
+    r.layered = pl.lay;
+    a.layered = pl.lay ? 1 : 0;
     int32_t n = 0;
     cudaError_t e;
     if (pl.sched == LDPC_SCHED_TWOSCAN) {

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <mutex>
 
+#include "k_stream_layered.cuh"
 #include "k_stream_pipe.cuh"
 #include "k_twoscan.cuh"
 #include "launch.h"
@@ -97,6 +98,27 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
         e = launch([&] { k_stream_ingest_f<<<gi, 256, 0, s>>>(a); }, nl);
     }
     if (e != cudaSuccess) return e;
+    if (r.layered) {
+        // one warp per frame tile walks the rows in order (k_stream_layered.cuh), then outputs
+        const dim3 gl((unsigned)((r.ntiles + 3) / 4));
+        if (pair) {
+            if (r.fmt == FMT_C16) e = es ? launch([&] { k_stream_layered<true, FMT_C16, true><<<gl, 128, 0, s>>>(a); }, nl)
+                                         : launch([&] { k_stream_layered<true, FMT_C16, false><<<gl, 128, 0, s>>>(a); }, nl);
+            else e = es ? launch([&] { k_stream_layered<true, FMT_1BIT, true><<<gl, 128, 0, s>>>(a); }, nl)
+                        : launch([&] { k_stream_layered<true, FMT_1BIT, false><<<gl, 128, 0, s>>>(a); }, nl);
+        } else {
+            e = es ? launch([&] { k_stream_layered<false, FMT_C16, true><<<gl, 128, 0, s>>>(a); }, nl)
+                   : launch([&] { k_stream_layered<false, FMT_C16, false><<<gl, 128, 0, s>>>(a); }, nl);
+        }
+        if (e != cudaSuccess) return e;
+        dim3 go((unsigned)a.wpf, (unsigned)r.ntiles);
+        e = pair ? launch([&] { k_stream_output<true><<<go, 256, 0, s>>>(a); }, nl)
+                 : launch([&] { k_stream_output<false><<<go, 256, 0, s>>>(a); }, nl);
+        if (e != cudaSuccess || !a.msg_out) return e;
+        if (!pair) return launch([&] { k_stream_export<false, FMT_C16><<<gr, 256, 0, s>>>(a); }, nl);
+        if (r.fmt == FMT_C16) return launch([&] { k_stream_export<true, FMT_C16><<<gr, 256, 0, s>>>(a); }, nl);
+        return launch([&] { k_stream_export<true, FMT_1BIT><<<gr, 256, 0, s>>>(a); }, nl);
+    }
     // software-pipelined iteration kernel (cp.async row prefetch) for rows of degree <= 8,
     // unless the register kernels are requested (tuning cross-check)
     const unsigned fgrid = (unsigned)((r.ntiles * 32 + 255) / 256);

@@ -65,11 +65,68 @@ def test_layered_mixed_convergence_cfg2_code():
     assert ref.iters[both].mean() < it[both].mean()
 
 
-def test_layered_unsupported_for_streaming_sizes():
-    code = g.CONFIGS[4].code()
-    dec = decoder(code)
+@pytest.mark.parametrize("code", small_codes(), ids=lambda c: c.name)
+@pytest.mark.parametrize("fmt", ["compact", "1bit", "f32"])
+def test_layered_streaming_kernel_small_codes(code, fmt):
+    """The streaming layered kernel (k_stream_layered.cuh: one warp per frame tile walking
+    the rows in order), forced onto small codes with tuning.path = STREAM: bit-exact with the
+    oracle's layered engine (D25) -- several tiles, a ragged last tile, early stop on and off."""
+    if int(np.max(np.diff(code.row_ptr))) > 8:
+        pytest.skip("row degree <= 8")
+    tn = {"path": P.LDPC_PATH_STREAM}
+    s2 = g.ebn0_to_sigma2(1.5, max(code.rate, 0.3))
+    for F in (1, 70):
+        for es, K in ((0, 9), (1, 14)):
+            if fmt == "f32":
+                llr = g.llr(800 + F, 0, F, code.n_vars, s2, g.LLR_F32)
+                params = P.make_params(K, es, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32,
+                                       P.LDPC_MSG_COMPACT, LAY, tuning=tn)
+                post, hb, ok, it = gpu_decode(code, llr, params)
+                ref = oracle.decode(code, llr, "layered", "f32", K, es, alpha=0.75, nthreads=NT)
+                np.testing.assert_array_equal(it, ref.iters)
+                np.testing.assert_array_equal(ok, ref.ok)
+                np.testing.assert_array_equal(post.view(np.uint32), ref.post.astype(np.float32).view(np.uint32))
+            else:
+                Q, lt, gk, frac = (127, P.LDPC_LLR_I8, g.LLR_I8, 2) if fmt == "1bit" else (511, P.LDPC_LLR_I16, g.LLR_I16, 3)
+                llr = g.llr(900 + F, 0, F, code.n_vars, s2, gk, frac, Q)
+                params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, Q, lt,
+                                       P.LDPC_MSG_1BIT if fmt == "1bit" else P.LDPC_MSG_COMPACT, LAY, tuning=tn)
+                assert_lay(code, llr, params, K, es, 1, Q)
+            assert P.ldpc_last_launch_count() > 1                    # the streaming layout
+
+
+@pytest.mark.parametrize("cfg_idx", [4, 5])
+def test_layered_long_codes(cfg_idx):
+    """Configs 4 (int16) and 5 (fp32) codes, N = 64,800: the layered schedule runs on the
+    streaming layered kernel (no longer UNSUPPORTED), bit-exact with the oracle on a few
+    frames and iterations (the schedule is a chain of 32,400 dependent row updates per
+    frame-iteration, so this is kept short), early stop on."""
+    cfg = g.CONFIGS[cfg_idx]
+    code = cfg.code()
+    s2 = g.ebn0_to_sigma2(1.5, code.rate)
+    if cfg.llr_kind == g.LLR_F32:
+        llr = g.llr(71, 0, 3, code.n_vars, s2, g.LLR_F32)
+        params = P.make_params(4, 1, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT,
+                               LAY)
+        post, hb, ok, it = gpu_decode(code, llr, params)
+        ref = oracle.decode(code, llr, "layered", "f32", 4, 1, alpha=0.75, nthreads=NT)
+        np.testing.assert_array_equal(it, ref.iters)
+        np.testing.assert_array_equal(post.view(np.uint32), ref.post.astype(np.float32).view(np.uint32))
+    else:
+        llr = g.llr(72, 0, 3, code.n_vars, s2, g.LLR_I16, 3, 511)
+        params = P.make_params(4, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT, LAY)
+        assert_lay(code, llr, params, 4, 1, 1, 511)
+
+
+def test_layered_streaming_unsupported_schedules():
+    """The streaming layered kernel takes a constant variant: per-iteration schedules on a
+    long code are rejected."""
+    cfg = g.CONFIGS[4]
+    dec = decoder(cfg.code())
+    params = P.make_params(4, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT, LAY,
+                           offset_per_iter=[1, 1, 0, 0])
     with pytest.raises(P.LdpcError) as e:
-        dec.workspace(64, P.params_for_config(g.CONFIGS[4], LAY))
+        dec.workspace(8, params)
     assert e.value.status == P.LDPC_ERR_UNSUPPORTED
 
 
@@ -109,11 +166,3 @@ def test_layered_f32_cfg2_code(es):
     params = P.make_params(15, es, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY,
                            alpha_per_iter=al)
     assert_lay_f32(code, llr, params, 15, es, 0.75, alpha_sched=al.astype(np.float64))
-
-
-def test_layered_f32_unsupported_for_streaming_sizes():
-    cfg = g.CONFIGS[5]
-    dec = decoder(cfg.code())
-    with pytest.raises(P.LdpcError) as e:
-        dec.workspace(64, P.params_for_config(cfg, LAY))
-    assert e.value.status == P.LDPC_ERR_UNSUPPORTED

@@ -404,8 +404,8 @@ def test_resident_size_boundary():
 def test_tmem_capacity_falls_back_to_streaming():
     """N = M = 24000 (4,4)-regular: the posteriors fit in shared memory but 94 rows per
     thread need 564 TMEM columns of compact state (> 512), so the planner streams the
-    decode (int16 and fp32); the per-edge and layered forms, which need TMEM / the resident
-    kernel, are rejected."""
+    decode (int16 and fp32) -- the layered schedule on the streaming layered kernel; the
+    per-edge form, which needs TMEM, is rejected."""
     code = g.regular(24000, 4, 4, seed=3, remove_4cycles=False)
     s2 = g.ebn0_to_sigma2(4.0, 0.5)
     llr = g.llr(8, 0, 3, code.n_vars, s2, g.LLR_I16, 3, 511)
@@ -419,11 +419,17 @@ def test_tmem_capacity_falls_back_to_streaming():
     ref = oracle.decode(code, z, "compact", "f32", 5, 0, alpha=0.75, nthreads=NT)
     assert_f32_exact(post, hb, ok, it, ref)
     dec = decoder(code)
-    for fmt, sched in ((P.LDPC_MSG_FULL, P.LDPC_SCHED_SINGLESCAN), (P.LDPC_MSG_COMPACT, P.LDPC_SCHED_LAYERED)):
-        bad = P.make_params(5, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, fmt, sched)
-        with pytest.raises(P.LdpcError) as e:
-            dec.workspace(3, bad)
-        assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+    bad = P.make_params(5, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_FULL)
+    with pytest.raises(P.LdpcError) as e:
+        dec.workspace(3, bad)
+    assert e.value.status == P.LDPC_ERR_UNSUPPORTED
+    # the layered schedule falls back to the streaming layered kernel
+    lay = P.make_params(5, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT,
+                        P.LDPC_SCHED_LAYERED)
+    post, hb, ok, it = gpu_decode(code, llr, lay)
+    ref = oracle.decode(code, llr.astype(np.int32), "layered", "int", 5, 1, 1, 511, nthreads=NT)
+    np.testing.assert_array_equal(post.astype(np.int32), ref.post)
+    np.testing.assert_array_equal(it, ref.iters)
 
 
 def test_high_column_degree_batched_kernel():

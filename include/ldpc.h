@@ -219,9 +219,11 @@ ldpc_status ldpc_decode_batch(const ldpc_code *code, const ldpc_decode_params *p
  *             for TWOSCAN the stored per-edge message of the last horizontal scan.
  * Defined for frames that ran all max_iter iterations (iterations_used == max_iter); the
  * entries of frames that stopped early are unspecified.  The same workspace as
- * ldpc_decode_batch.  LDPC_ERR_UNSUPPORTED for the LAYERED schedule and for the batched
- * resident kernel (tuning.path = LDPC_PATH_RESIDENT_BATCHED, or codes with
- * 2Q(max_dv+1) >= 16384 on the resident path). */
+ * ldpc_decode_batch.  LAYERED: the messages of the last iteration's row updates, on the
+ * streaming layered kernel (long codes, or tuning.path = LDPC_PATH_STREAM).
+ * LDPC_ERR_UNSUPPORTED on the resident layered and the batched resident kernels
+ * (tuning.path = LDPC_PATH_RESIDENT_BATCHED, or codes with 2Q(max_dv+1) >= 16384 on the
+ * resident path). */
 ldpc_status ldpc_decode_batch_messages(const ldpc_code *code, const ldpc_decode_params *params, int64_t n_frames,
                                        const void *llr, uint32_t *hard_bits, void *posteriors,
                                        uint8_t *syndrome_ok, int32_t *iterations_used, void *messages,

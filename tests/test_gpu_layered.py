@@ -166,3 +166,30 @@ def test_layered_f32_cfg2_code(es):
     params = P.make_params(15, es, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY,
                            alpha_per_iter=al)
     assert_lay_f32(code, llr, params, 15, es, 0.75, alpha_sched=al.astype(np.float64))
+
+
+@pytest.mark.parametrize("fmt", ["compact", "f32"])
+def test_layered_streaming_messages(fmt):
+    """Exit messages of the streaming layered kernel (ldpc_decode_batch_messages) against the
+    oracle's layered trace of the last iteration (messages rebuilt from the compact state)."""
+    code = small_codes()[6]
+    tn = {"path": P.LDPC_PATH_STREAM}
+    K = 7
+    dec = decoder(code)
+    if fmt == "f32":
+        llr = g.llr(31, 0, 70, code.n_vars, g.ebn0_to_sigma2(1.0, code.rate), g.LLR_F32)
+        params = P.make_params(K, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT,
+                               LAY, tuning=tn)
+        ref = oracle.decode(code, llr, "layered", "f32", K, 0, alpha=0.75, trace=True, nthreads=NT)
+    else:
+        llr = g.llr(32, 0, 70, code.n_vars, g.ebn0_to_sigma2(1.0, code.rate), g.LLR_I16, 3, 511)
+        params = P.make_params(K, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT, LAY,
+                               tuning=tn)
+        ref = oracle.decode(code, llr.astype(np.int32), "layered", "int", K, 0, 1, 511, trace=True, nthreads=NT)
+    out, msg = dec.decode_messages(torch.from_numpy(llr).cuda(), params)
+    torch.cuda.synchronize()
+    got = msg.cpu().numpy()
+    if fmt == "f32":
+        np.testing.assert_array_equal(got.view(np.uint32), ref.trace_msg[:, K - 1, :].astype(np.float32).view(np.uint32))
+    else:
+        np.testing.assert_array_equal(got.astype(np.int32), ref.trace_msg[:, K - 1, :])

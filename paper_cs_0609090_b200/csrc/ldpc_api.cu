@@ -702,11 +702,6 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         // tuning.path = LDPC_PATH_STREAM routes integer decodes through the streaming kernels
         pl.path = (c->res_ok && pl.tn.path != LDPC_PATH_STREAM && pl.sched == LDPC_SCHED_SINGLESCAN) ? PATH_RESIDENT
                                                                                                    : PATH_STREAM_I;
-        // the streaming integer kernels (and two-scan) keep posteriors as 2Z + 0x4000 per
-        // 16-bit lane (reading D26): needs 2Q(max_dv+1) < 0x4000
-        if (pl.path == PATH_STREAM_I && (int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
-            return fail(LDPC_ERR_UNSUPPORTED, "streaming integer decode needs 2*Q*(max_dv+1) < 16384 (Q=%d, max_dv=%d)",
-                        pl.Q, c->max_dv);
         if (pl.sched == LDPC_SCHED_LAYERED) {
             // resident layered kernel when the code fits on chip, else (or with tuning.path =
             // STREAM) the streaming layered kernel (k_stream_layered.cuh: one warp per frame tile)
@@ -715,13 +710,16 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                 pl.path = PATH_RESIDENT;
             } else {
                 pl.path = PATH_STREAM_I;
-                if ((int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
-                    return fail(LDPC_ERR_UNSUPPORTED, "streaming layered decode needs 2*Q*(max_dv+1) < 16384");
                 if (!pl.vks.empty())
                     return fail(LDPC_ERR_UNSUPPORTED, "the streaming layered kernel takes a constant variant "
                                                       "(no per-iteration schedules)");
             }
         }
+        // the streaming integer kernels (flooding, layered and two-scan) keep posteriors as
+        // 2Z + 0x4000 per 16-bit lane (reading D26): needs 2Q(max_dv+1) < 0x4000
+        if (pl.path == PATH_STREAM_I && (int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
+            return fail(LDPC_ERR_UNSUPPORTED, "streaming integer decode needs 2*Q*(max_dv+1) < 16384 (Q=%d, max_dv=%d)",
+                        pl.Q, c->max_dv);
         pl.tile = 64;
     } else {
         return fail(LDPC_ERR_INVALID_ARG, "bad llr_type %d", p->llr_type);

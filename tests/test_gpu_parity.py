@@ -439,6 +439,13 @@ def test_high_column_degree_batched_kernel():
     llr = g.llr(5, 0, 33, code.n_vars, 0.9, g.LLR_I16, 3, 511)
     params = P.make_params(8, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT)
     assert_int_parity(code, llr, params, 8, 1, 1, 511)
+    # the resident layered kernel keeps unbiased lanes too
+    lay = P.make_params(8, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT,
+                        P.LDPC_SCHED_LAYERED)
+    post, hb, ok, it = gpu_decode(code, llr, lay)
+    ref = oracle.decode(code, llr.astype(np.int32), "layered", "int", 8, 1, 1, 511, nthreads=NT)
+    np.testing.assert_array_equal(post.astype(np.int32), ref.post)
+    np.testing.assert_array_equal(it, ref.iters)
     dec = decoder(code)
     with pytest.raises(P.LdpcError) as e:
         dec.workspace(33, tuned(params, path=P.LDPC_PATH_STREAM))

@@ -513,3 +513,36 @@ def test_plain_c_consumer():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout
+
+
+@pytest.mark.parametrize("kind", ["int16", "int16-full", "1bit-msgs"])
+def test_resident_grid_loop(kind):
+    """tuning.resident_waves = 1 caps the resident grid at one wave (blocks/SM x SMs), so every
+    CTA loops over several frame pairs: outputs (and, for 1bit-msgs, the exported messages) of
+    all frames must still match."""
+    code = small_codes()[1]                        # regular (3,6), N = 96
+    F = 4 * 148 * 32 + 7                           # well above one wave at any occupancy, odd
+    s2 = g.ebn0_to_sigma2(2.0, code.rate)
+    tn = {"resident_waves": 1}
+    if kind == "1bit-msgs":
+        llr = g.llr(7, 0, F, code.n_vars, s2, g.LLR_I8, 2, 127)
+        params = P.make_params(8, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 127, P.LDPC_LLR_I8, P.LDPC_MSG_1BIT, tuning=tn)
+        dec = decoder(code)
+        out, msg = dec.decode_messages(torch.from_numpy(llr).cuda(), params)
+        torch.cuda.synchronize()
+        assert P.ldpc_last_launch_count() == 1
+        picks = np.r_[0:3, F - 3:F]
+        ref = oracle.decode(code, llr[picks].astype(np.int32), "compact", "int", 8, 0, 1, 127, trace=True, nthreads=NT)
+        np.testing.assert_array_equal(msg.cpu().numpy()[picks].astype(np.int32), ref.trace_msg[:, 7, :])
+        np.testing.assert_array_equal(out.posteriors.cpu().numpy()[picks].astype(np.int32), ref.post)
+        return
+    llr = g.llr(6, 0, F, code.n_vars, s2, g.LLR_I16, 3, 511)
+    fmt = P.LDPC_MSG_FULL if kind == "int16-full" else P.LDPC_MSG_COMPACT
+    params = P.make_params(8, 1, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, fmt, tuning=tn)
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    assert P.ldpc_last_launch_count() == 1
+    ref = oracle.decode(code, llr.astype(np.int32), "compact", "int", 8, 1, 1, 511, nthreads=NT)
+    np.testing.assert_array_equal(it, ref.iters)
+    np.testing.assert_array_equal(ok, ref.ok)
+    np.testing.assert_array_equal(post.astype(np.int32), ref.post)
+    np.testing.assert_array_equal(hb, oracle.pack_bits(ref.bits))

@@ -119,8 +119,8 @@ enum { LDPC_MSG_COMPACT = 0, LDPC_MSG_1BIT = 1,
  *               resident kernel; longer codes (and tuning.path = LDPC_PATH_STREAM) on the
  *               streaming layered kernel: one warp per 64-frame (F32: 32-frame) tile walks
  *               the rows in order -- correct at any size but latency-bound (the schedule is
- *               a chain of M dependent row updates per frame), constant
- *               variant only.  Row degree <= 8, else LDPC_ERR_UNSUPPORTED.  Integer and F32
+ *               a chain of M dependent row updates per frame).  Per-iteration
+ *               schedules: max_iter <= 64.  Row degree <= 8, else LDPC_ERR_UNSUPPORTED.  Integer and F32
  *               LLRs (F32 layered is bit-exact with a sequential implementation). */
 enum { LDPC_SCHED_SINGLESCAN = 0, LDPC_SCHED_TWOSCAN = 1, LDPC_SCHED_LAYERED = 2 };
 

@@ -20,10 +20,18 @@
 
 namespace ldpc {
 
+// per-iteration check-node variants of the single-launch layered kernel (lambda_k / beta_k,
+// P:179), passed by value: n = 0 -> the constants in StreamArgs
+struct LaySched {
+    int n;
+    VarK vk[kMaxSched];
+    float alpha[kMaxSched], beta[kMaxSched];
+};
+
 // one row, integer pairs: q = Z - L_old (biased words in, unbiased q), new state, Z <- q + L_new
 template <int DC, int FMT>
-__device__ __forceinline__ void lay_row_i(const StreamArgs &a, uint32_t *Lt, uint32_t *stt, size_t ss, int m,
-                                          const uint32_t (&col)[8], int lane, bool first, uint32_t keep) {
+__device__ __forceinline__ void lay_row_i(const StreamArgs &a, const VarK &vk, uint32_t *Lt, uint32_t *stt, size_t ss,
+                                          int m, const uint32_t (&col)[8], int lane, bool first, uint32_t keep) {
     uint32_t L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
@@ -40,7 +48,7 @@ __device__ __forceinline__ void lay_row_i(const StreamArgs &a, uint32_t *Lt, uin
         rebuild_q<DC, true>(L, st, q, a.rk);                               // Z_n - L^(k-1)_mn
     }
     uint32_t rn[DC];
-    new_state<DC, false, -1, FMT == FMT_1BIT>(q, a.vk, st, rn, a.rk);
+    new_state<DC, false, -1, FMT == FMT_1BIT>(q, vk, st, rn, a.rk);
     StateIO<FMT>::store(stt + lane, ss, (size_t)m * 32, st);
 #pragma unroll
     for (int j = 0; j < DC; ++j) {                                       // in place (D25); frozen lanes keep Z
@@ -51,8 +59,9 @@ __device__ __forceinline__ void lay_row_i(const StreamArgs &a, uint32_t *Lt, uin
 
 // one row, fp32 (D11: q = fl(Z - L_old), Z <- fl(q + L_new))
 template <int DC>
-__device__ __forceinline__ void lay_row_f(const StreamArgs &a, float *Lt, uint32_t *stt, size_t ss, int m,
-                                          const uint32_t (&col)[8], int lane, bool first, bool frozen) {
+__device__ __forceinline__ void lay_row_f(const StreamArgs &a, float alpha, float beta, float *Lt, uint32_t *stt,
+                                          size_t ss, int m, const uint32_t (&col)[8], int lane, bool first,
+                                          bool frozen) {
     float L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
@@ -69,7 +78,7 @@ __device__ __forceinline__ void lay_row_f(const StreamArgs &a, float *Lt, uint32
     }
     float A, B, r[DC], q[DC];
     uint32_t Wn;
-    f32_row_q<DC>(L, first, A0, B0, W0, a.alpha, a.beta, A, B, Wn, r, q);
+    f32_row_q<DC>(L, first, A0, B0, W0, alpha, beta, A, B, Wn, r, q);
     __stcg(stt + so, __float_as_uint(A));
     __stcg(stt + ss + so, __float_as_uint(B));
     __stcg(stt + 2 * ss + so, Wn);
@@ -120,7 +129,7 @@ __device__ __forceinline__ uint32_t lay_freeze(const StreamArgs &a, int tile, in
 }
 
 template <bool PAIR, int FMT, bool ES>
-__global__ void __launch_bounds__(128) k_stream_layered(const StreamArgs a) {
+__global__ void __launch_bounds__(128) k_stream_layered(const StreamArgs a, const __grid_constant__ LaySched sch) {
     const int lane = threadIdx.x & 31;
     const int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (tile >= a.ntiles) return;
@@ -136,6 +145,8 @@ __global__ void __launch_bounds__(128) k_stream_layered(const StreamArgs a) {
         if (ES && __all_sync(0xFFFFFFFFu, done == all)) break;
         const uint32_t keep = PAIR ? (((done & 1) ? 0x0000FFFFu : 0u) | ((done & 2) ? 0xFFFF0000u : 0u)) : 0u;
         const bool frozen = !PAIR && (done & 1);
+        const VarK vk = sch.n ? sch.vk[k - 1] : a.vk;            // iteration k's variant
+        const float alpha = sch.n ? sch.alpha[k - 1] : a.alpha, beta = sch.n ? sch.beta[k - 1] : a.beta;
         for (int m = 0; m < a.M; ++m) {                  // rows in ascending m (D25)
             const RowT rt = load_rowt(a.rowtab, m, a.M);
             uint32_t col[8];
@@ -144,8 +155,8 @@ __global__ void __launch_bounds__(128) k_stream_layered(const StreamArgs a) {
             switch (rt.dc) {
 #define LDPC_LR(D)                                                                                      \
     case D:                                                                                             \
-        if (PAIR) lay_row_i<D, FMT>(a, Lt, stt, ss, m, col, lane, k == 1, keep);                        \
-        else lay_row_f<D>(a, (float *)Lt, stt, ss, m, col, lane, k == 1, frozen);                       \
+        if (PAIR) lay_row_i<D, FMT>(a, vk, Lt, stt, ss, m, col, lane, k == 1, keep);                    \
+        else lay_row_f<D>(a, alpha, beta, (float *)Lt, stt, ss, m, col, lane, k == 1, frozen);          \
         break;
             LDPC_LR(2) LDPC_LR(3) LDPC_LR(4) LDPC_LR(5) LDPC_LR(6) LDPC_LR(7) LDPC_LR(8)
 #undef LDPC_LR

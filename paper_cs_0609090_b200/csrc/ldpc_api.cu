@@ -660,9 +660,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                     return fail(LDPC_ERR_UNSUPPORTED, "per-iteration schedules support max_iter <= %d", kMaxSched);
                 pl.path = PATH_RESIDENT;
                 pl.kind = RES_F32_LAY;
-            } else if (!pl.alphas.empty()) {
-                return fail(LDPC_ERR_UNSUPPORTED, "the streaming layered kernel takes a constant variant "
-                                                  "(no per-iteration schedules)");
+            } else if (!pl.alphas.empty() && p->max_iter > kMaxSched) {
+                return fail(LDPC_ERR_UNSUPPORTED, "layered per-iteration schedules support max_iter <= %d", kMaxSched);
             }
         }
         pl.tile = 32;
@@ -710,9 +709,9 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                 pl.path = PATH_RESIDENT;
             } else {
                 pl.path = PATH_STREAM_I;
-                if (!pl.vks.empty())
-                    return fail(LDPC_ERR_UNSUPPORTED, "the streaming layered kernel takes a constant variant "
-                                                      "(no per-iteration schedules)");
+                if (!pl.vks.empty() && p->max_iter > kMaxSched)
+                    return fail(LDPC_ERR_UNSUPPORTED, "layered per-iteration schedules support max_iter <= %d",
+                                kMaxSched);
             }
         }
         // the streaming integer kernels (flooding, layered and two-scan) keep posteriors as
@@ -768,9 +767,8 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
             // the streaming kernels (state in HBM) take the decode where they apply
             if (pl.fmt == FMT_FULL)
                 return fail(LDPC_ERR_UNSUPPORTED, "full per-edge messages need %u TMEM columns (> 512)", need);
-            if (pl.lay && (!pl.vks.empty() || !pl.alphas.empty()))
-                return fail(LDPC_ERR_UNSUPPORTED, "layered schedule: the compact state does not fit on chip and the "
-                                                  "streaming layered kernel takes no per-iteration schedules");
+            if (pl.lay && (!pl.vks.empty() || !pl.alphas.empty()) && p->max_iter > kMaxSched)
+                return fail(LDPC_ERR_UNSUPPORTED, "layered per-iteration schedules support max_iter <= %d", kMaxSched);
             const bool f32 = p->llr_type == LDPC_LLR_F32;
             if (!f32 && (int64_t)2 * pl.Q * (c->max_dv + 1) >= 0x4000)
                 return fail(LDPC_ERR_UNSUPPORTED, "compact state needs %u TMEM columns (> 512) and the streaming "

@@ -101,14 +101,24 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
     if (r.layered) {
         // one warp per frame tile walks the rows in order (k_stream_layered.cuh), then outputs
         const dim3 gl((unsigned)((r.ntiles + 3) / 4));
+        LaySched sch{};
+        if (r.vk_sched || r.alpha_sched || r.beta_sched) {
+            if (r.max_iter > kMaxSched) return cudaErrorInvalidValue;   // the planner rejects these
+            sch.n = r.max_iter;
+            for (int k = 1; k <= r.max_iter; ++k) {
+                sch.vk[k - 1] = r.vk_sched ? r.vk_sched[k - 1] : a.vk;
+                sch.alpha[k - 1] = r.alpha_sched ? r.alpha_sched[k - 1] : a.alpha;
+                sch.beta[k - 1] = r.beta_sched ? r.beta_sched[k - 1] : a.beta;
+            }
+        }
         if (pair) {
-            if (r.fmt == FMT_C16) e = es ? launch([&] { k_stream_layered<true, FMT_C16, true><<<gl, 128, 0, s>>>(a); }, nl)
-                                         : launch([&] { k_stream_layered<true, FMT_C16, false><<<gl, 128, 0, s>>>(a); }, nl);
-            else e = es ? launch([&] { k_stream_layered<true, FMT_1BIT, true><<<gl, 128, 0, s>>>(a); }, nl)
-                        : launch([&] { k_stream_layered<true, FMT_1BIT, false><<<gl, 128, 0, s>>>(a); }, nl);
+            if (r.fmt == FMT_C16) e = es ? launch([&] { k_stream_layered<true, FMT_C16, true><<<gl, 128, 0, s>>>(a, sch); }, nl)
+                                         : launch([&] { k_stream_layered<true, FMT_C16, false><<<gl, 128, 0, s>>>(a, sch); }, nl);
+            else e = es ? launch([&] { k_stream_layered<true, FMT_1BIT, true><<<gl, 128, 0, s>>>(a, sch); }, nl)
+                        : launch([&] { k_stream_layered<true, FMT_1BIT, false><<<gl, 128, 0, s>>>(a, sch); }, nl);
         } else {
-            e = es ? launch([&] { k_stream_layered<false, FMT_C16, true><<<gl, 128, 0, s>>>(a); }, nl)
-                   : launch([&] { k_stream_layered<false, FMT_C16, false><<<gl, 128, 0, s>>>(a); }, nl);
+            e = es ? launch([&] { k_stream_layered<false, FMT_C16, true><<<gl, 128, 0, s>>>(a, sch); }, nl)
+                   : launch([&] { k_stream_layered<false, FMT_C16, false><<<gl, 128, 0, s>>>(a, sch); }, nl);
         }
         if (e != cudaSuccess) return e;
         dim3 go((unsigned)a.wpf, (unsigned)r.ntiles);

@@ -118,54 +118,29 @@ def test_layered_long_codes(cfg_idx):
         assert_lay(code, llr, params, 4, 1, 1, 511)
 
 
-def test_layered_streaming_unsupported_schedules():
-    """The streaming layered kernel takes a constant variant: per-iteration schedules on a
-    long code are rejected."""
-    cfg = g.CONFIGS[4]
-    dec = decoder(cfg.code())
-    params = P.make_params(4, 0, P.LDPC_MINSUM_OFFSET, 1, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT, LAY,
-                           offset_per_iter=[1, 1, 0, 0])
-    with pytest.raises(P.LdpcError) as e:
-        dec.workspace(8, params)
-    assert e.value.status == P.LDPC_ERR_UNSUPPORTED
-
-
-def assert_lay_f32(code, llr, params, K, es, alpha=1.0, beta=0.0, **kw):
-    """fp32 layered: every variable is updated by one row at a time in ascending m with the
-    oracle's operations (D11: one rounding each), so the GPU is bit-exact with the oracle."""
+def test_layered_streaming_schedules():
+    """Per-iteration lambda_k / beta_k on the streaming layered kernel
+    (integer and fp32), bit-exact with the oracle's layered engine."""
+    code = small_codes()[5]
+    tn = {"path": P.LDPC_PATH_STREAM}
+    K = 8
+    bs = [2, 1, 1, 0, 0, 1, 0, 0]
+    al = [0.5, 0.75, 0.75, 1.0, 0.875, 1.0, 0.75, 1.0]
+    llr = g.llr(41, 0, 70, code.n_vars, g.ebn0_to_sigma2(1.5, code.rate), g.LLR_I16, 3, 511)
+    params = P.make_params(K, 1, P.LDPC_MINSUM_OFFSET, 0, 0.0, 1.0, 511, P.LDPC_LLR_I16, P.LDPC_MSG_COMPACT, LAY,
+                           offset_per_iter=bs, alpha_per_iter=al, tuning=tn)
     post, hb, ok, it = gpu_decode(code, llr, params)
-    assert P.ldpc_last_launch_count() == 1                      # resident layered kernel
-    ref = oracle.decode(code, llr, "layered", "f32", K, es, beta=beta, alpha=alpha, nthreads=NT, **kw)
+    ref = oracle.decode(code, llr.astype(np.int32), "layered", "int", K, 1, 0, 511, nthreads=NT, beta_sched=bs,
+                        alpha_sched=al)
+    np.testing.assert_array_equal(post.astype(np.int32), ref.post)
     np.testing.assert_array_equal(it, ref.iters)
-    np.testing.assert_array_equal(ok, ref.ok)
+    z = g.llr(42, 0, 40, code.n_vars, g.ebn0_to_sigma2(1.5, code.rate), g.LLR_F32)
+    alf = np.linspace(0.6, 0.95, K).astype(np.float32)
+    params = P.make_params(K, 0, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY,
+                           alpha_per_iter=alf, tuning=tn)
+    post, hb, ok, it = gpu_decode(code, z, params)
+    ref = oracle.decode(code, z, "layered", "f32", K, 0, alpha=0.75, nthreads=NT, alpha_sched=alf.astype(np.float64))
     np.testing.assert_array_equal(post.view(np.uint32), ref.post.astype(np.float32).view(np.uint32))
-    np.testing.assert_array_equal(hb, oracle.pack_bits((ref.post <= 0).astype(np.uint8)))
-
-
-@pytest.mark.parametrize("code", small_codes(), ids=lambda c: c.name)
-def test_layered_f32_small_codes(code):
-    if int(np.max(np.diff(code.row_ptr))) > 8:
-        pytest.skip("resident kernels: row degree <= 8")
-    for F in (1, 33, 130):
-        for ebn0 in (1.0, 3.0):
-            llr = g.llr(500 + F, 0, F, code.n_vars, g.ebn0_to_sigma2(ebn0, max(code.rate, 0.3)), g.LLR_F32)
-            for variant, alpha, beta, es, K in ((P.LDPC_MINSUM_NORMALIZED, 0.75, 0.0, 0, 10),
-                                                (P.LDPC_MINSUM_OFFSET, 1.0, 0.25, 1, 12),
-                                                (P.LDPC_MINSUM_NORMALIZED, 0.8125, 0.0, 1, 25)):
-                params = P.make_params(K, es, variant, 0, beta, alpha, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY)
-                assert_lay_f32(code, llr, params, K, es, alpha, beta)
-
-
-@pytest.mark.parametrize("es", [0, 1])
-def test_layered_f32_cfg2_code(es):
-    code = g.CONFIGS[2].code()
-    llr = g.llr(61 + es, 0, 64, code.n_vars, g.ebn0_to_sigma2(2.0, code.rate), g.LLR_F32)
-    params = P.make_params(15, es, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY)
-    assert_lay_f32(code, llr, params, 15, es, 0.75)
-    al = np.linspace(0.6, 0.95, 15).astype(np.float32)                 # lambda_k per iteration (P:179)
-    params = P.make_params(15, es, P.LDPC_MINSUM_NORMALIZED, 0, 0.0, 0.75, 0, P.LDPC_LLR_F32, P.LDPC_MSG_COMPACT, LAY,
-                           alpha_per_iter=al)
-    assert_lay_f32(code, llr, params, 15, es, 0.75, alpha_sched=al.astype(np.float64))
 
 
 @pytest.mark.parametrize("fmt", ["compact", "f32"])

@@ -237,9 +237,11 @@ ldpc_status ldpc_decode_host_workspace_size(const ldpc_code *code, int64_t n_fra
  * iterations_used are HOST pointers (pinned memory recommended).  Enqueues the
  * host->device copy, the decode and the device->host copies on `stream`, split in
  * frame chunks so copies overlap decoding; returns without synchronising -- the
- * host outputs are valid after cudaStreamSynchronize(stream).  The chunks run on
- * internal streams of the code object: concurrent calls on one code are accepted
- * (their enqueues are serialised by a lock) and execute one after the other. */
+ * host outputs are valid after cudaStreamSynchronize(stream).  Outputs are staged in the
+ * workspace and copied back by the copy engines (kernels writing straight into mapped
+ * host memory were measured slower: DESIGN.md §7).  The chunks run on internal streams of
+ * the code object: concurrent calls on one code are accepted (their enqueues are
+ * serialised by a lock) and execute one after the other. */
 ldpc_status ldpc_decode_batch_host(const ldpc_code *code, const ldpc_decode_params *params, int64_t n_frames,
                                    const void *llr_host, uint32_t *hard_bits_host, void *posteriors_host,
                                    uint8_t *syndrome_ok_host, int32_t *iterations_used_host,

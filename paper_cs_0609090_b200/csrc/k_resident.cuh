@@ -178,15 +178,25 @@ static __device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc,
             if (which & 2) a.post[(size_t)f1 * a.N + n] = (int16_t)((hi16(v) - bias) >> 1);
         }
     }
+    // hard bits: a warp forms 32 consecutive words (one ballot each) and lane j stores word j,
+    // so each frame's words leave as one 128-byte store instead of 32 scattered 4-byte ones
     const int lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
-    for (int w = warp; w < a.wpf; w += nw) {
-        const int n = w * 32 + lane;
-        const uint32_t v = n < a.N ? Lsrc[n] : pack2(bias + 2, bias + 2);
-        const uint32_t blo = __ballot_sync(0xFFFFFFFFu, lo16(v) - bias <= 0);
-        const uint32_t bhi = __ballot_sync(0xFFFFFFFFu, hi16(v) - bias <= 0);
-        if (lane == 0) {
-            if (which & 1) a.hard_bits[(size_t)f0 * a.wpf + w] = blo;
-            if (which & 2) a.hard_bits[(size_t)f1 * a.wpf + w] = bhi;
+    for (int w0 = warp * 32; w0 < a.wpf; w0 += nw * 32) {
+        uint32_t mlo = 0, mhi = 0;
+        const int nwd = min(32, a.wpf - w0);
+        for (int j = 0; j < nwd; ++j) {
+            const int n = (w0 + j) * 32 + lane;
+            const uint32_t v = n < a.N ? Lsrc[n] : pack2(bias + 2, bias + 2);
+            const uint32_t blo = __ballot_sync(0xFFFFFFFFu, lo16(v) - bias <= 0);
+            const uint32_t bhi = __ballot_sync(0xFFFFFFFFu, hi16(v) - bias <= 0);
+            if (lane == j) {
+                mlo = blo;
+                mhi = bhi;
+            }
+        }
+        if (lane < nwd) {
+            if (which & 1) a.hard_bits[(size_t)f0 * a.wpf + w0 + lane] = mlo;
+            if (which & 2) a.hard_bits[(size_t)f1 * a.wpf + w0 + lane] = mhi;
         }
     }
     if (tid == 0) {

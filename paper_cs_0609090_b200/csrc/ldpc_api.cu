@@ -1049,26 +1049,28 @@ struct HostLayout {
     size_t elt = 2, post_elt = 2, wpf = 0;
     size_t off_llr = 0, off_hb = 0, off_post = 0, off_ok = 0, off_it = 0, off_ws[4] = {0, 0, 0, 0};
     size_t chunk_ws = 0, total = 0;
+    Plan pl;                         // the plan of a full chunk (reused by every full chunk)
 };
 
 // Host-buffer decode: H2D copy, decode and D2H copies of frame chunks round-robin on up to
 // four streams, so the copies of one chunk overlap the decode of others.  Up to 16 chunks of
-// >= 256 frames (resident) / >= 64 frames (streaming) on 4 streams measured best (e2e cfg2
-// 7.4 -> 8.6, cfg4 2.1 -> 2.8, cfg1 3.7 -> 4.0 Gbit/s); LDPC_HOST_CHUNKS / LDPC_HOST_STREAMS
-// override (tuning hooks).
+// >= 512 frames (resident) / >= 64 frames (streaming) on up to 4 streams measured best
+// (tools/sweep_e2e.py); ldpc_tuning.host_chunks / host_streams override.
 ldpc_status host_layout(const ldpc_code *c, int64_t F, const ldpc_decode_params *p, HostLayout &h) {
     Plan pf;
     ldpc_status st0 = make_plan(c, F, p, pf);
     if (st0 != LDPC_OK) return st0;
-    // chunks of >= 256 frames (resident kernels) or >= one 64-frame tile (streaming), <= 16
-    const int64_t min_chunk = pf.path == PATH_RESIDENT ? 256 : 64;
+    // chunks of >= 512 frames (resident kernels) or >= one 64-frame tile (streaming), <= 16:
+    // every chunk costs ~25 us of host enqueue (one H2D, the decode, four D2H copies), which
+    // small batches cannot hide (cfg1, 1024 frames: 2 chunks 0.147 ms, 4 chunks 0.178 ms)
+    const int64_t min_chunk = pf.path == PATH_RESIDENT ? 512 : 64;
     h.nchunks = std::max<int64_t>(1, std::min<int64_t>(16, F / min_chunk));
     if (pf.tn.host_chunks > 0) h.nchunks = pf.tn.host_chunks;
     h.chunk = (F + h.nchunks - 1) / h.nchunks;
     h.chunk = ((h.chunk + 63) / 64) * 64;
     if (h.chunk == 0) h.chunk = 64;
     h.nchunks = (F + h.chunk - 1) / h.chunk;
-    Plan pl;
+    Plan &pl = h.pl;
     ldpc_status st = make_plan(c, h.chunk, p, pl);
     if (st != LDPC_OK) return st;
     h.elt = p->llr_type == LDPC_LLR_F32 ? 4 : (p->llr_type == LDPC_LLR_I8 ? 1 : 2);
@@ -1140,10 +1142,11 @@ extern "C" ldpc_status ldpc_decode_batch_host(const ldpc_code *code, const ldpc_
         int32_t *dit = iterations_used_host ? (int32_t *)(w + h.off_it) + f0 : nullptr;
         CUDA_TRY(cudaMemcpyAsync(dl, (const char *)llr_host + (size_t)f0 * N * h.elt, (size_t)nf * N * h.elt,
                                  cudaMemcpyHostToDevice, s));
-        Plan pl;
-        if ((st = make_plan(code, nf, params, pl)) != LDPC_OK) return st;
+        Plan tail;
+        if (nf != h.chunk && (st = make_plan(code, nf, params, tail)) != LDPC_OK) return st;
         g_launches = 0;
-        st = decode_device(code, params, nf, dl, dhb, dpost, dok, dit, w + h.off_ws[si], h.chunk_ws, s, pl);
+        st = decode_device(code, params, nf, dl, dhb, dpost, dok, dit, w + h.off_ws[si], h.chunk_ws, s,
+                           nf == h.chunk ? h.pl : tail);
         if (st != LDPC_OK) return st;
         launches += g_launches;
         CUDA_TRY(cudaMemcpyAsync(hard_bits_host + (size_t)f0 * h.wpf, dhb, (size_t)nf * h.wpf * 4,

@@ -24,6 +24,10 @@ struct Kern {
     // The dynamic shared memory cap is raised once per kernel to the device's opt-in limit
     // (it is only a cap: occupancy follows the size each launch asks for), so concurrent
     // host threads never race on the attribute.
+    static cudaFuncAttributes *attrs() {
+        static cudaFuncAttributes a[kMaxDevices];
+        return a;
+    }
     static cudaError_t prepare() {
         static std::once_flag flags[kMaxDevices];
         static cudaError_t errs[kMaxDevices];
@@ -37,8 +41,21 @@ struct Kern {
             if (err == cudaSuccess)
                 err = cudaFuncSetAttribute(get(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            optin - (int)fa.sharedSizeBytes);
+            if (err == cudaSuccess && dev >= 0 && dev < kMaxDevices) attrs()[dev] = fa;
             return err;
         });
+    }
+    // the kernel's attributes on the current device, queried once per device by prepare()
+    static cudaError_t attributes(cudaFuncAttributes &fa) {
+        cudaError_t e = prepare();
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        if (dev >= 0 && dev < kMaxDevices) {
+            fa = attrs()[dev];
+            return cudaSuccess;
+        }
+        return cudaFuncGetAttributes(&fa, get());
     }
 };
 
@@ -47,11 +64,9 @@ cudaError_t occ(size_t dyn_smem, size_t smem_per_sm, int threads, int *blocks) {
     // The occupancy API reports 1 block/SM for kernels that allocate TMEM; compute the
     // limit from the kernel's registers, shared memory and threads instead (TMEM is
     // accounted for by the caller).
-    auto kern = Kern<QC, ES, FMT, TIN, KIND>::get();
-    cudaError_t e = Kern<QC, ES, FMT, TIN, KIND>::prepare();
-    if (e != cudaSuccess) return e;
     cudaFuncAttributes fa;
-    if ((e = cudaFuncGetAttributes(&fa, kern)) != cudaSuccess) return e;
+    cudaError_t e = Kern<QC, ES, FMT, TIN, KIND>::attributes(fa);
+    if (e != cudaSuccess) return e;
     const size_t per_block_smem = dyn_smem + fa.sharedSizeBytes + 1024;   // + driver reserve
     const int by_smem = (int)(smem_per_sm / per_block_smem);
     const int regs = ((fa.numRegs + 7) / 8) * 8 * threads;

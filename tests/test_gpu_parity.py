@@ -278,6 +278,41 @@ def test_host_api_matches_device_api_and_counters():
     np.testing.assert_array_equal(cnt, want)
 
 
+@pytest.mark.parametrize("cfg_idx", [1, 2, 3, 4])
+@pytest.mark.parametrize("mode", ["pinned", "pageable"])
+def test_host_api_output_modes(cfg_idx, mode):
+    """ldpc_decode_batch_host with pinned and pageable host buffers, resident (cfg1-3) and
+    streaming (cfg4) kernels, a partial last chunk and the optional outputs omitted:
+    identical results to the device API."""
+    cfg = g.CONFIGS[cfg_idx]
+    code = cfg.code()
+    F = {1: 1100, 2: 1300, 3: 1100, 4: 150}[cfg_idx]
+    llr = cfg.llrs(code, 0, F)
+    params = _cfg_params(cfg)
+    post, hb, ok, it = gpu_decode(code, llr, params)
+    dec = decoder(code)
+
+    def buf(t):
+        return t if mode == "pageable" else t.pin_memory()
+
+    lh = buf(torch.from_numpy(llr))
+    hbh = buf(torch.full((F, dec.wpf), -1, dtype=torch.int32))
+    okh = buf(torch.full((F,), 7, dtype=torch.uint8))
+    ith = buf(torch.full((F,), -1, dtype=torch.int32))
+    ph = buf(torch.full((F, code.n_vars), 12345, dtype=torch.int16))
+    dec.decode_host(lh, params, hbh, okh, ith, ph)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(hbh.numpy().view(np.uint32), hb)
+    np.testing.assert_array_equal(okh.numpy(), ok)
+    np.testing.assert_array_equal(ith.numpy(), it)
+    np.testing.assert_array_equal(ph.numpy(), post)
+    # optional outputs omitted
+    hbh.fill_(-1)
+    dec.decode_host(lh, params, hbh, okh)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(hbh.numpy().view(np.uint32), hb)
+
+
 def test_batch_composition_invariance():
     """Per-frame outputs do not depend on how frames are batched (the analog of
     decoding a global frame range on 1 or on W GPUs)."""

@@ -21,7 +21,7 @@ hb = torch.empty((F, dec.wpf), dtype=torch.int32).pin_memory()
 ok = torch.empty(F, dtype=torch.uint8).pin_memory()
 it = torch.empty(F, dtype=torch.int32).pin_memory()
 post = torch.empty((F, code.n_vars), dtype=torch.float32 if llr.dtype == np.float32 else torch.int16).pin_memory()
-for chunks, streams in [(0, 0), (8, 2), (8, 4), (16, 4), (32, 4), (64, 4), (32, 2), (4, 4)]:
+for chunks, streams in [(0, 0), (1, 1), (2, 2), (2, 1), (4, 4), (8, 4), (16, 4)]:
     params = P.params_for_config(cfg)
     P.set_tuning(params, {"host_chunks": chunks, "host_streams": streams})
     for _ in range(2):
@@ -36,4 +36,13 @@ for chunks, streams in [(0, 0), (8, 2), (8, 4), (16, 4), (32, 4), (64, 4), (32, 
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = sorted(ts)[len(ts) // 2]
+    import time
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    for _ in range(20):
+        dec.decode_host(lh, params, hb, ok, it, post)
+    c1 = time.perf_counter()
+    torch.cuda.synchronize()
+    c2 = time.perf_counter()
+    print(f"   host enqueue {(c1 - c0) / 20 * 1e3:.3f} ms/call, back-to-back {(c2 - c0) / 20 * 1e3:.3f} ms/call")
     print(f"chunks {chunks} streams {streams}: {ms:.3f} ms, {F * code.K / (ms * 1e-3) / 1e9:.2f} Gbit/s", flush=True)

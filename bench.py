@@ -426,6 +426,16 @@ def measure_config(ctx, cfg, steps, warmup, want_e2e=True):
                 "frac": ach / ctx.peaks["hbm_gbs"], "traffic": None, "peak_source": ctx.peak_src,
                 "frac_of_nominal_8tbs": ach / 8000.0, "how": how, "kernel_ms_per_launch": it_ms,
                 "whole_step": hbm_model}
+        if it_ms and it_ms > 0 and cfg.llr_kind != g.LLR_F32:
+            # the integer streaming kernel issues the same 16x2 row arithmetic as the resident
+            # one; ncu shows it issue/ALU-limited as much as byte-limited, so
+            # the ALU-pipe fraction is reported beside the HBM one
+            clk = (clocks or {}).get("sm_mhz") or ctx.peaks.get("sm_max_mhz", 1965.0)
+            a_ach = ALG_OPS_PER_EU * eu_iter / (it_ms * 1e-3) / 1e12
+            a_peak = 148 * ALU_PIPE_PER_CLK * 2 * clk * 1e6 / 1e12
+            roof["alu_model"] = {"achieved": a_ach, "peak": a_peak, "unit": "Tops/s", "frac": a_ach / a_peak,
+                                 "how": f"{ALG_OPS_PER_EU} algorithmic 16-bit ops per edge-update, iteration-kernel "
+                                        f"launch duration; peak as the resident kernels' (DESIGN.md §5.2)"}
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cfg.idx}.json")   # tools/ncu_summary.py
     if os.path.exists(prof):
         with open(prof) as f:

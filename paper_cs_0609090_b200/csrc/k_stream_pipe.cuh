@@ -312,6 +312,13 @@ __device__ __forceinline__ void pipe_body(const StreamArgs &a, int k) {
 // check-node variant.
 template <bool PAIR, int FMT, bool ES>
 __global__ void __launch_bounds__(kPipeWarps * 32, LDPC_PIPE_MINB) k_stream_pipe(const StreamArgs a, int k) {
+    // Iteration k + 1 is launched as a programmatic dependent of iteration k
+    // (stream_launch.cu): its CTAs may be scheduled while k's last CTAs retire, so before
+    // touching any plane each CTA waits for the previous grid to complete and its writes
+    // to be visible; then it lets the next iteration's grid be scheduled.  Without the
+    // launch attribute both instructions are no-ops.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // the integer check-node variant (offset / normalized) of this launch's iteration is a
     // template parameter of the rows as well (fp32 rows take alpha / beta directly)
     if constexpr (!PAIR) {

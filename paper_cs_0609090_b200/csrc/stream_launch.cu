@@ -1,4 +1,5 @@
 // stream_launch.cu -- launches of the streaming kernels (long codes) and the error counter.
+#include <utility>
 #include <algorithm>
 #include <mutex>
 
@@ -45,6 +46,25 @@ cudaError_t launch(F f, int32_t *n) {
     f();
     ++*n;
     return cudaGetLastError();
+}
+// a launch that may overlap the retiring tail of the previous kernel in the stream
+// (programmatic dependent launch): the kernel itself waits (griddepcontrol.wait) before
+// reading anything the previous kernel wrote
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, int threads, size_t smem, cudaStream_t s, bool pdl,
+                       int32_t *n, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    ++*n;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 // the variant of iteration k (lambda_k, beta_k) for the launches of k
 void set_iteration(StreamArgs &c, const StreamRun &r, int k) {
@@ -166,17 +186,21 @@ cudaError_t stream_run(const StreamArgs &a, const StreamRun &r, cudaStream_t s, 
         const dim3 gr((unsigned)std::max(1, (a.M + rows_per_block - 1) / rows_per_block), (unsigned)nt);
         for (int k = 1; k <= r.max_iter && use_pipe; ++k) {
             set_iteration(c, r, k);
+            // iterations 2.. follow the previous iteration's kernel directly (no freeze kernel
+            // in between without early stop): programmatic dependent launches
+            const bool pdl = k > 1 && !es;
+            const int th = kPipeWarps * 32;
             if (pair) {
                 if (r.fmt == FMT_C16) {
-                    if (es) e = launch([&] { k_stream_pipe<true, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
-                    else e = launch([&] { k_stream_pipe<true, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
+                    if (es) e = launch_pdl(k_stream_pipe<true, FMT_C16, true>, gp, th, psmem, s, pdl, nl, c, k);
+                    else e = launch_pdl(k_stream_pipe<true, FMT_C16, false>, gp, th, psmem, s, pdl, nl, c, k);
                 } else {
-                    if (es) e = launch([&] { k_stream_pipe<true, FMT_1BIT, true><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
-                    else e = launch([&] { k_stream_pipe<true, FMT_1BIT, false><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
+                    if (es) e = launch_pdl(k_stream_pipe<true, FMT_1BIT, true>, gp, th, psmem, s, pdl, nl, c, k);
+                    else e = launch_pdl(k_stream_pipe<true, FMT_1BIT, false>, gp, th, psmem, s, pdl, nl, c, k);
                 }
             } else {
-                if (es) e = launch([&] { k_stream_pipe<false, FMT_C16, true><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
-                else e = launch([&] { k_stream_pipe<false, FMT_C16, false><<<gp, kPipeWarps * 32, psmem, s>>>(c, k); }, nl);
+                if (es) e = launch_pdl(k_stream_pipe<false, FMT_C16, true>, gp, th, psmem, s, pdl, nl, c, k);
+                else e = launch_pdl(k_stream_pipe<false, FMT_C16, false>, gp, th, psmem, s, pdl, nl, c, k);
             }
             if (e != cudaSuccess) return e;
             if (es) {

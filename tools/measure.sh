@@ -1,5 +1,5 @@
 #!/bin/bash
-# Full measurement pass on a B200 box (run under gpurun).  Writes gpurun_out/meas/.
+# Round-1 measurement pass (profiles/r01_*; superseded by tools/measure_r02.sh).  Run under gpurun; writes gpurun_out/meas/
 set -u
 OUT=gpurun_out/meas; mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1

@@ -600,7 +600,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
     if (!c) return fail(LDPC_ERR_INVALID_ARG, "code is NULL");
     if (!p) return fail(LDPC_ERR_INVALID_ARG, "params is NULL");
     if (F < 0) return fail(LDPC_ERR_INVALID_ARG, "n_frames < 0");
-    if (F > (int64_t)1 << 31) return fail(LDPC_ERR_UNSUPPORTED, "n_frames > 2^31");
+    if (F > INT32_MAX) return fail(LDPC_ERR_UNSUPPORTED, "n_frames > 2^31 - 1");
     if (p->max_iter < 1) return fail(LDPC_ERR_INVALID_ARG, "max_iter must be >= 1");
     if (p->early_stop != 0 && p->early_stop != 1) return fail(LDPC_ERR_INVALID_ARG, "early_stop must be 0 or 1");
     if (p->schedule != LDPC_SCHED_SINGLESCAN && p->schedule != LDPC_SCHED_TWOSCAN &&

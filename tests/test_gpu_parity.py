@@ -249,6 +249,13 @@ def test_unsupported_requests():
     with pytest.raises(P.LdpcError) as e:
         dec.workspace(8, P.make_params(0, 0))
     assert e.value.status == P.LDPC_ERR_INVALID_ARG
+    # frame counts: int32 frame indices on the device; the size query alone (no allocation)
+    params = _cfg_params(g.CONFIGS[1])
+    assert P.ldpc_decode_workspace_size(dec.handle, 2**31 - 1, params) > 0
+    for bad, status in ((2**31, P.LDPC_ERR_UNSUPPORTED), (-1, P.LDPC_ERR_INVALID_ARG)):
+        with pytest.raises(P.LdpcError) as e:
+            P.ldpc_decode_workspace_size(dec.handle, bad, params)
+        assert e.value.status == status
 
 
 def test_host_api_matches_device_api_and_counters():

@@ -75,7 +75,9 @@ def bytes_per_eu(cfg, code):
 
 
 def dtype_name(cfg):
-    return "f32" if cfg.llr_kind == g.LLR_F32 else ("int16x2" if cfg.llr_kind == g.LLR_I16 else "int8->int16x2")
+    """The arithmetic type of the path: 16-bit integer lanes (two frames per 32-bit register,
+    int8 inputs widened on load) or fp32 messages (posterior sums exact in int64, D28)."""
+    return "f32" if cfg.llr_kind == g.LLR_F32 else "int16"
 
 
 def load_peaks():

@@ -588,3 +588,50 @@ def test_resident_grid_loop(kind):
     np.testing.assert_array_equal(ok, ref.ok)
     np.testing.assert_array_equal(post.astype(np.int32), ref.post)
     np.testing.assert_array_equal(hb, oracle.pack_bits(ref.bits))
+
+
+@pytest.mark.parametrize("cfg_idx", [1, 2, 4, 5])
+def test_decode_inside_cuda_graph(cfg_idx):
+    """ldpc_decode_batch is stream-ordered and allocation-free, so it can be captured in a CUDA
+    graph (the bench times cfg1 that way): two batches captured back to back -- resident,
+    streaming with programmatic dependent launches (cfg4) and fp32 (cfg5) -- replayed, and
+    their outputs equal to direct decodes."""
+    cfg = g.CONFIGS[cfg_idx]
+    code = cfg.code()
+    F = {1: 300, 2: 200, 4: 70, 5: 40}[cfg_idx]
+    params = _cfg_params(cfg)
+    if cfg_idx >= 4:
+        params.max_iter = 12
+    dec = P.Decoder(code, 0)
+    llrs = [torch.from_numpy(cfg.llrs(code, 5000 * (b + 1), F)).cuda() for b in range(2)]
+    ref = []
+    for x in llrs:
+        o = dec.decode(x, params)
+        torch.cuda.synchronize()
+        ref.append((o.posteriors.clone(), o.hard_bits.clone(), o.syndrome_ok.clone(), o.iterations.clone()))
+    outs = [dec.alloc_outputs(F, params.llr_type, posteriors=True) for _ in range(2)]
+    dec2 = P.Decoder(code, 0)              # its own workspace per batch: both decodes in one graph
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dec.decode(llrs[0], params, outs[0])
+        dec2.decode(llrs[1], params, outs[1])
+    torch.cuda.synchronize()
+    for o in outs:
+        o.posteriors.zero_()
+        o.hard_bits.zero_()
+        o.iterations.fill_(-1)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        dec.decode(llrs[0], params, outs[0])
+        dec2.decode(llrs[1], params, outs[1])
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    for o, (rp, rh, rk, ri) in zip(outs, ref):
+        assert torch.equal(o.posteriors, rp)
+        assert torch.equal(o.hard_bits, rh)
+        assert torch.equal(o.syndrome_ok, rk)
+        assert torch.equal(o.iterations, ri)
+    dec2.close()
+    dec.close()

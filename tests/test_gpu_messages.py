@@ -131,7 +131,7 @@ def test_messages_unsupported():
         assert e.value.status == P.LDPC_ERR_UNSUPPORTED
 
 
-@pytest.mark.parametrize("i", list(range(40)))
+@pytest.mark.parametrize("i", list(range(80)))
 def test_messages_random(i):
     """Seeded random sweep of the message export: code shapes of tests/test_gpu_random.py,
     integer (compact / 1-bit / FULL; resident, streaming pipeline, streaming register

@@ -48,7 +48,7 @@ def _code(rng, i):
     return g.from_dense(H, name="rand")
 
 
-CASES = list(range(120))
+CASES = list(range(240))
 
 
 @pytest.mark.parametrize("i", CASES)
@@ -83,7 +83,15 @@ def test_random_case(i):
     ebn0 = float(rng.uniform(0.5, 4.0))
     llr = g.llr(int(rng.integers(1, 1 << 30)), 0, F, code.n_vars, g.ebn0_to_sigma2(ebn0, max(code.rate, 0.2)),
                 kind, frac, Q)
-    params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, lt, fmt, sched, tuning=tuning)
+    # per-iteration beta_k / lambda_k on a third of the cases, from a separate
+    # stream so the other parameters of each case stay as they were
+    rs = np.random.default_rng(5000 + i)
+    kw, okw = {}, {}
+    if rs.integers(0, 3) == 0:
+        okw["beta_sched"] = kw["offset_per_iter"] = [int(x) for x in rs.integers(0, 3, K)]
+        if rs.integers(0, 2) == 0:
+            okw["alpha_sched"] = kw["alpha_per_iter"] = [float(x) for x in rs.choice([1.0, 0.5, 0.75, 0.875], K)]
+    params = P.make_params(K, es, P.LDPC_MINSUM_OFFSET, beta, 0.0, 1.0, Q, lt, fmt, sched, tuning=tuning, **kw)
     try:
         post, hb, ok, it = gpu_decode(code, llr, params)
     except P.LdpcError as e:
@@ -91,9 +99,9 @@ def test_random_case(i):
         pytest.skip(f"unsupported: {e}")
     engine = {P.LDPC_SCHED_SINGLESCAN: "compact", P.LDPC_SCHED_LAYERED: "layered",
               P.LDPC_SCHED_TWOSCAN: "twoscan"}[sched]
-    ref = oracle.decode(code, llr.astype(np.int32), engine, "int", K, es, beta, Q, nthreads=NT)
+    ref = oracle.decode(code, llr.astype(np.int32), engine, "int", K, es, beta, Q, nthreads=NT, **okw)
     info = f"{code.name} N={code.n_vars} M={code.n_checks} sched={sched} env={env} K={K} es={es} beta={beta} Q={Q} " \
-           f"F={F} fmt={fmt} lt={lt}"
+           f"F={F} fmt={fmt} lt={lt} schedules={okw}"
     np.testing.assert_array_equal(it, ref.iters, err_msg=info)
     np.testing.assert_array_equal(ok, ref.ok, err_msg=info)
     np.testing.assert_array_equal(post.astype(np.int32), ref.post, err_msg=info)

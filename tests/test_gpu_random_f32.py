@@ -19,7 +19,7 @@ import paper_cs_0609090_b200 as P  # noqa: E402
 from test_gpu_parity import NT, assert_f32_exact, gpu_decode  # noqa: E402
 from test_gpu_random import _code  # noqa: E402
 
-CASES = list(range(60))
+CASES = list(range(120))
 
 
 @pytest.mark.parametrize("i", CASES)

@@ -1151,17 +1151,21 @@ extern "C" ldpc_status ldpc_decode_batch_host(const ldpc_code *code, const ldpc_
         launches += g_launches;
         CUDA_TRY(cudaMemcpyAsync(hard_bits_host + (size_t)f0 * h.wpf, dhb, (size_t)nf * h.wpf * 4,
                                  cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(syndrome_ok_host + f0, dok, (size_t)nf, cudaMemcpyDeviceToHost, s));
         if (dpost)
             CUDA_TRY(cudaMemcpyAsync((char *)posteriors_host + (size_t)f0 * N * h.post_elt, dpost,
                                      (size_t)nf * N * h.post_elt, cudaMemcpyDeviceToHost, s));
-        if (dit)
-            CUDA_TRY(cudaMemcpyAsync(iterations_used_host + f0, dit, (size_t)nf * 4, cudaMemcpyDeviceToHost, s));
     }
     for (int i = 0; i < h.nstreams; ++i) {
         CUDA_TRY(cudaEventRecord(code->ev[1 + i], code->aux[i]));
         CUDA_TRY(cudaStreamWaitEvent(us, code->ev[1 + i], 0));
     }
+    // the per-frame flags and iteration counts (a few KB) leave in one copy each once every
+    // chunk has decoded: per chunk, these small copies cost the bidirectional PCIe pipeline
+    // a fixed overhead each (cfg2 e2e 3.57 -> 3.29 ms; moving the hard bits here too was
+    // slower, 3.47 ms: their 7.7 MB then trail the last decode -- DESIGN.md §7)
+    CUDA_TRY(cudaMemcpyAsync(syndrome_ok_host, w + h.off_ok, (size_t)n_frames, cudaMemcpyDeviceToHost, us));
+    if (iterations_used_host)
+        CUDA_TRY(cudaMemcpyAsync(iterations_used_host, w + h.off_it, (size_t)n_frames * 4, cudaMemcpyDeviceToHost, us));
     g_launches = launches;
     return LDPC_OK;
 }

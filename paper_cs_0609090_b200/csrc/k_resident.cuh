@@ -208,18 +208,19 @@ static __device__ void res_write_outputs(const ResArgs &a, const uint32_t *Lsrc,
 // TMEM columns of batch b for this thread: FMT_C16 uses (A,B) at 2b and W at 2*nb + b;
 // FMT_1BIT uses (X, W) at 2b.
 // Index-coded ñ (FMT_1BIT) -> per-edge flags with a shared-memory table instead of shifts
-// (expand_idx): the byte offset of the lo frame's entry is the W nibble holding t(ñ_lo) as it
-// stands (16-byte stride), the hi frame's entry sits 256 bytes on.  A kernel that loads state
-// with TAB = true fills the table first (idx_tab_fill, before its first barrier).
+// (expand_idx): the byte offset of the lo frame's entry is 16 x the index nibble (W bits
+// 8-11, 16-byte stride), the hi frame's entry (W bits 24-27) sits 256 bytes on.  A kernel
+// that loads state with TAB = true fills the table first (idx_tab_fill, before its first
+// barrier).
 static __shared__ __align__(16) uint32_t g_idx_tab[128];
 __device__ __forceinline__ void idx_tab_fill() {
     const int t = threadIdx.x;
-    if (t < 32) g_idx_tab[4 * t] = t < 16 ? (0x10u << t) & 0x0000F0F0u : (0x100000u << (t - 16)) & 0xF0F00000u;
+    if (t < 32) g_idx_tab[4 * t] = t < 16 ? (0x100u << t) & 0x0000FF00u : (0x1000000u << (t - 16)) & 0xFF000000u;
 }
 __device__ __forceinline__ uint32_t expand_idx_tab(uint32_t W) {
-    const uint32_t ol = *(const uint32_t *)((const char *)g_idx_tab + (W & 0xF0u));
-    const uint32_t oh = *(const uint32_t *)((const char *)g_idx_tab + 256 + ((W >> 16) & 0xF0u));
-    return (W & 0x0F0F0F0Fu) | ol | oh;
+    const uint32_t ol = *(const uint32_t *)((const char *)g_idx_tab + ((W >> 4) & 0xF0u));
+    const uint32_t oh = *(const uint32_t *)((const char *)g_idx_tab + 256 + ((W >> 20) & 0xF0u));
+    return (W & 0x00FF00FFu) | ol | oh;
 }
 
 template <int FMT, bool TAB = false>

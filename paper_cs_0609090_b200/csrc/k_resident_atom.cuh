@@ -326,13 +326,11 @@ __device__ __forceinline__ void export_row_compact(const ResArgs &a, int m, int 
                                                    bool hi_valid) {
     const int64_t e0 = __ldg(a.row_ptr + m);
     for (int j = 0; j < dc; ++j) {
-        const int i = j >> 1, h = j & 1;
 #pragma unroll
         for (int fr = 0; fr < 2; ++fr) {
             if (fr == 1 && !hi_valid) break;
-            const int byte = h + 2 * fr;                       // W layout: rowcore.cuh header
-            const uint32_t wb = st.W >> (8 * byte);
-            const bool neg = (wb >> i) & 1u, isidx = (wb >> (4 + i)) & 1u;
+            const uint32_t wb = st.W >> (16 * fr);             // W layout: rowcore.cuh header
+            const bool neg = (wb >> j) & 1u, isidx = (wb >> (8 + j)) & 1u;
             const int mag = (int)(((isidx ? st.B : st.A) >> (16 * fr)) & 0xFFFFu);   // doubled magnitude
             a.msg_out[(size_t)(f0 + fr) * a.E + e0 + j] = (int16_t)((neg ? -mag : mag) / 2);
         }

@@ -342,8 +342,8 @@ __global__ void __launch_bounds__(256) k_stream_export(const StreamArgs a) {
                 LDPC_CHECK(e0 + dc <= a.E);
                 int16_t *out = (int16_t *)a.msg_out + (size_t)f * a.E + e0;
                 for (int j = 0; j < dc; ++j) {
-                    const uint32_t wb = st.W >> (8 * ((j & 1) + 2 * fr));
-                    const bool neg = (wb >> (j >> 1)) & 1u, isidx = (wb >> (4 + (j >> 1))) & 1u;
+                    const uint32_t wb = st.W >> (16 * fr);     // W layout: rowcore.cuh header
+                    const bool neg = (wb >> j) & 1u, isidx = (wb >> (8 + j)) & 1u;
                     const int mag = (int)(((isidx ? st.B : st.A) >> (16 * fr)) & 0xFFFFu);
                     out[j] = (int16_t)((neg ? -mag : mag) / 2);
                 }

@@ -9,18 +9,16 @@
 //
 // Compact state of a row (per frame pair), the paper's (A_m, B_m, ñ_m, s_mn):
 //   A, B : doubled magnitudes 2A_m, 2B_m in each 16-bit half (B >= A)
-//   W    : per-edge bits, byte-interleaved so one shift + PRMT expands them to
-//          16-bit masks.  For edge pair i (edges 2i, 2i+1):
-//            byte0 bit i  : s of edge 2i,   frame lo     byte0 bit 4+i : idx, edge 2i,   lo
-//            byte1 bit i  : s of edge 2i+1, frame lo     byte1 bit 4+i : idx, edge 2i+1, lo
-//            byte2 bit i  : s of edge 2i,   frame hi     byte2 bit 4+i : idx, edge 2i,   hi
-//            byte3 bit i  : s of edge 2i+1, frame hi     byte3 bit 4+i : idx, edge 2i+1, hi
-//          s bit = 1 means L_mn < 0; "idx" bit = 1 means n is an argmin (n = ñ_m).  dc <= 8.
+//   W    : per-edge bits, one 16-bit half per frame (lo frame bits 0-15, hi frame 16-31):
+//            half bit j     : s of edge j   (1 means L_mn < 0)
+//            half bit 8 + j : idx of edge j (1 means n is an argmin, n = ñ_m)          dc <= 8.
+//          One left shift by 7 - j puts edge j's two bits of both frames at bit 7 of every
+//          byte (sign: bytes 0 / 2, idx: bytes 1 / 3), so one PRMT per mask expands them.
+//          new_state builds W with IMADs on the FMA pipe only (pack_bits below).
 //   1-bit message format (FMT_1BIT, "1-bit messages"): the persistent W keeps only
 //          the sign bits (the only per-edge datum) and ñ_m as an INDEX per check and frame:
-//          byte0 bits 4-7 = t(ñ_lo), byte2 bits 4-7 = t(ñ_hi), bytes 1, 3 bits 4-7 = 0, with
-//          t(j) = 8 (j & 1) + (j >> 1) -- the position of j's flag in the layout above, so
-//          expand_idx() rebuilds the flags with two shifts when the state is loaded.
+//          half bits 0-7 = signs, half bits 8-12 = ñ (the edge number; see pack_bits for ties),
+//          so expand_idx() rebuilds the flags with two shifts when the state is loaded.
 #pragma once
 #include "args.cuh"
 #include "rowcore_types.cuh"
@@ -32,12 +30,33 @@ struct RowState {
     uint32_t A, B, W;
 };
 
-// index-coded ñ (FMT_1BIT) -> the per-edge flag layout the rebuild reads.  The masks keep
-// the flags inside the frame's own bytes: a tie in the minimum (several flags ORed into t)
-// can only happen when A == B, where the flag does not matter (reading D3).
+// index-coded ñ (FMT_1BIT) -> the per-edge flag layout the rebuild reads.  An index >= 8 (only
+// after a tie in the minimum, see pack_bits) sets no flag: a tie means A == B, where the flag
+// does not matter (reading D3).
 __device__ __forceinline__ uint32_t expand_idx(uint32_t W) {
-    const uint32_t tl = (W >> 4) & 15u, th = (W >> 20) & 15u;
-    return (W & 0x0F0F0F0Fu) | ((0x10u << tl) & 0x0000F0F0u) | ((0x100000u << th) & 0xF0F00000u);
+    const uint32_t tl = (W >> 8) & 15u, th = (W >> 24) & 15u;
+    return (W & 0x00FF00FFu) | ((0x100u << tl) & 0x0000FF00u) | ((0x1000000u << th) & 0xFF000000u);
+}
+
+// Bit packing on the FMA pipe.  For a 16x2 mask m (0xFFFF in the halves where a condition
+// holds: lo_m, hi_m in {0, 1}) and K = 2^p, p < 16, the 32-bit product is
+//   m K = lo_m (2^16 - 1) K + hi_m (2^32 - 2^16) K == 2^16 (lo_m - hi_m) K - lo_m K  (mod 2^32),
+// so a sum S of such products over distinct bit positions p is 2^16 (LO - HI) - LO with
+// LO = sum lo_m 2^p, HI = sum hi_m 2^p (both < 2^16), and
+//   -S (1 + 2^16) == LO + 2^16 HI  (mod 2^32):
+// one IMAD per mask (S += m K) and one per row (W = S * -(0x10001)) give the packed word
+// without an ALU-pipe instruction.  For an index code (FMT_1BIT) K = j 2^8 sums the edge
+// numbers of the argmin flags: exact for the unique argmin; after a tie the sum (< 2^5) may
+// be any value, which is harmless (expand_idx).
+__device__ __forceinline__ uint32_t mad_bits(uint32_t m, uint32_t K, uint32_t S) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(m), "r"(K), "r"(S));
+    return d;
+}
+__device__ __forceinline__ uint32_t unpack_bits(uint32_t S) {
+    uint32_t d;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(S), "r"(0xFFFEFFFFu));
+    return d;
 }
 
 // Rebuild L^(k-1)_mn = s f(A, B, n, ñ) and form
@@ -58,19 +77,11 @@ __device__ __forceinline__ void rebuild_q(const uint32_t (&L)[DC], const RowStat
         nB = vneg(st.B, k);
     }
 #pragma unroll
-    for (int i = 0; i < (DC + 1) / 2; ++i) {
-        const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte
-        const uint32_t wo = st.W << (3 - i);       // idx bits of pair i -> bit 7 of each byte
-        {
-            const uint32_t sm = prmt(ws, 0u, 0xAA88u), ix = prmt(wo, 0u, 0xAA88u);
-            const uint32_t mag = sel(ix, B, A), nmag = sel(ix, nB, nA);
-            q[2 * i] = vadd(L[2 * i], sel(sm, mag, nmag));      // Z - L_old: L_old = s*mag
-        }
-        if (2 * i + 1 < DC) {
-            const uint32_t sm = prmt(ws, 0u, 0xBB99u), ix = prmt(wo, 0u, 0xBB99u);
-            const uint32_t mag = sel(ix, B, A), nmag = sel(ix, nB, nA);
-            q[2 * i + 1] = vadd(L[2 * i + 1], sel(sm, mag, nmag));
-        }
+    for (int j = 0; j < DC; ++j) {
+        const uint32_t ws = st.W << (7 - j);       // edge j's bits -> bit 7 of each byte
+        const uint32_t sm = prmt(ws, 0u, 0xAA88u), ix = prmt(ws, 0u, 0xBB99u);
+        const uint32_t mag = sel(ix, B, A), nmag = sel(ix, nB, nA);
+        q[j] = vadd(L[j], sel(sm, mag, nmag));          // Z - L_old: L_old = s*mag
     }
 }
 
@@ -87,20 +98,13 @@ __device__ __forceinline__ void rebuild_q_b8(const uint32_t (&L)[DC], const RowS
     // argmin mask the other sign is one IMAD: 2 Q0 - (Q0 + mag)
     const uint32_t nA = fadd32(st.A, Q0, k), nB = fadd32(st.B, Q0, k);
 #pragma unroll
-    for (int i = 0; i < (DC + 1) / 2; ++i) {
-        const uint32_t ws = st.W << (7 - i);       // sign bits of pair i -> bit 7 of each byte
-        const uint32_t wo = st.W << (3 - i);       // idx bits of pair i -> bit 7 of each byte
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int j = 2 * i + h;
-            if (j >= DC) break;
-            const uint32_t s8 = h ? 0xBB99u : 0xAA88u;
-            const uint32_t sm = prmt(ws, 0u, s8), ix = prmt(wo, 0u, s8);
-            const uint32_t neg = sel(ix, nB, nA);                               // Q0 + mag
-            uint32_t pos;                                                       // Q0 - mag
-            asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(pos) : "r"(neg), "r"(k.m1), "r"(Q0 + Q0));
-            q[j] = fadd32(L[j], sel(sm, neg, pos), k);
-        }
+    for (int j = 0; j < DC; ++j) {
+        const uint32_t ws = st.W << (7 - j);       // edge j's bits -> bit 7 of each byte
+        const uint32_t sm = prmt(ws, 0u, 0xAA88u), ix = prmt(ws, 0u, 0xBB99u);
+        const uint32_t neg = sel(ix, nB, nA);                                   // Q0 + mag
+        uint32_t pos;                                                           // Q0 - mag
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(pos) : "r"(neg), "r"(k.m1), "r"(Q0 + Q0));
+        q[j] = fadd32(L[j], sel(sm, neg, pos), k);
     }
 }
 
@@ -181,7 +185,7 @@ __device__ __forceinline__ uint32_t variant_mag(uint32_t m, const VarK &v, const
 // unsigned, the per-lane sign mask is [q >= 0] (bit 15), and the returned messages are
 // "V form + 0x8000": r ^ 0x8000 in the low lane == V(r) + 0x8000 as a 32-bit integer, so a
 // 32-bit RED adds them exactly (the accumulator start value is lowered by dv_n 0x8000).
-// IDX = true (FMT_1BIT): ñ is stored as the index code t(ñ) (header), one LOP3 per edge.
+// IDX = true (FMT_1BIT): ñ is stored as an index code (header), one IMAD per edge.
 template <int DC, bool B8 = false, int VM = -1, bool IDX = false>
 __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &vk, RowState &st, uint32_t (&r)[DC],
                                           const RegK &k) {
@@ -220,7 +224,7 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
         Bneg = sel(Pm, Bc, nB);
     }
     const uint32_t cm1 = fnot(m1, k);                           // -m1 - 1
-    uint32_t W = 0, sqp = 0, ixp = 0, tacc = 0;
+    uint32_t S = 0;                                             // packed by IMADs (mad_bits)
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
         const uint32_t ix = vaddmin(mt[j], cm1, k.zero);          // min(m~ - m1 - 1, 0): 0xFFFF iff argmin
@@ -235,22 +239,12 @@ __device__ __forceinline__ void new_state(const uint32_t (&q)[DC], const VarK &v
         } else {
             r[j] = sel(sq, sel(ix, Bneg, Aneg), sel(ix, Bpos, Apos));
         }
-        if (IDX) tacc |= ix & ((uint32_t)(8 * (j & 1) + (j >> 1)) * 0x00010001u);   // t(j) where n_j = ñ
-        if ((j & 1) == 0) {
-            sqp = sq;
-            ixp = ix;
-            if (j == DC - 1) {
-                W |= prmt(sqp, 0u, 0x6240u) & (0x01010101u << (j >> 1));
-                if (!IDX) W |= prmt(ixp, 0u, 0x6240u) & (0x10101010u << (j >> 1));
-            }
-        } else {
-            W |= prmt(sqp, sq, 0x6240u) & (0x01010101u << (j >> 1));
-            if (!IDX) W |= prmt(ixp, ix, 0x6240u) & (0x10101010u << (j >> 1));
-        }
+        S = mad_bits(sq, 1u << j, S);                           // sign bit j
+        S = mad_bits(ix, IDX ? (uint32_t)j << 8 : 0x100u << j, S);   // idx flag 8 + j / index code
     }
-    if (IDX) W |= tacc << 4;                                     // t(ñ_lo) -> byte0 bits 4-7, t(ñ_hi) -> byte2
-    if (B8) W ^= ~Pm & 0x0F0F0F0Fu;                             // s = sgn(q) * product ([q>=0] bits stored)
-    else W ^= Pm & 0x0F0F0F0Fu;                                 // s = sgn(q) * product
+    uint32_t W = unpack_bits(S);
+    if (B8) W ^= ~Pm & 0x00FF00FFu;                             // s = sgn(q) * product ([q>=0] bits stored)
+    else W ^= Pm & 0x00FF00FFu;                                 // s = sgn(q) * product
     st.A = A;
     st.B = B;
     st.W = W;

@@ -47,7 +47,8 @@ class ldpc_tuning(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("resident_waves", ctypes.c_int32),
                 ("stream_chunk_tiles", ctypes.c_int32), ("stream_register_kernels", ctypes.c_int32),
                 ("host_chunks", ctypes.c_int32), ("host_streams", ctypes.c_int32),
-                ("resident_threads", ctypes.c_int32)]
+                ("resident_threads", ctypes.c_int32),
+                ("resident_fixed_bases", ctypes.c_int32)]
 
 
 class ldpc_decode_params(ctypes.Structure):

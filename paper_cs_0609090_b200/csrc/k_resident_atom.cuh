@@ -34,6 +34,14 @@ namespace ldpc {
 constexpr int kAtomBias = 0x3FFF;
 constexpr uint32_t kAtomQ0 = 0x40014001u;    // (0x8000 - bias) per lane: q + 0x8000 = word + Q0 - 2 L_old
 
+// Fixed buffer bases (ResArgs::qc_fix; QC codes with early stop, 4 Np <= kAtomFixOff): buffer 1
+// starts kAtomFixOff bytes after buffer 0 and the shift table is copied to shared memory with
+// the shared address of buffer 0 folded into its block offsets, so a row scan specialised on
+// the iteration parity FP addresses Z^(k-1) and Z^(k) as [d + imm] -- two IMADs fewer per edge
+// than adding the buffer bases held in registers (the early-stop kernel cannot keep them in
+// uniform registers, which is what the fixed-iteration kernels do: LDS / ATOMS [R + UR]).
+// kAtomFixOff: args.cuh (the planner sizes shared memory with it).
+
 // Hard-decision parity of a row from its biased words: bit 15 / 31 set iff odd.
 template <int DC>
 __device__ __forceinline__ uint32_t atom_row_parity(const uint32_t (&L)[DC]) {
@@ -46,14 +54,23 @@ __device__ __forceinline__ uint32_t atom_row_parity(const uint32_t (&L)[DC]) {
 
 // CSM (general codes): the [dc][M] column table was staged in shared memory at byte
 // address sct (ResArgs::csr_smem), so the per-edge offsets are shared-memory loads
-template <int DC, bool QC, bool ES, int VM, int FMT, bool CSM = false>
+// FP (QC only): -1 = buffer bases bp / ba in registers; 0 / 1 = fixed bases, iteration parity
+// (0: Z^(k-1) in buffer 0, Z^(k) in buffer 1; 1: the reverse), sct = shared address of the
+// shift table (entries (4 s, 4 j Z + base of buffer 0))
+template <int DC, bool QC, bool ES, int VM, int FMT, bool CSM = false, int FP = -1>
 __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba, int e0,
                                          uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd,
                                          uint32_t sct = 0) {
+    constexpr uint32_t OFF_L = FP == 1 ? kAtomFixOff : 0u, OFF_A = FP == 0 ? kAtomFixOff : 0u;
     uint32_t d[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        if (QC) {
+        if (QC && FP >= 0) {
+            uint32_t ex, ey;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(ex), "=r"(ey) : "r"(sct + 8u * (uint32_t)(e0 + j)));
+            const uint32_t u = r4 + ex;
+            d[j] = min(u - t.Z4, u) + ey;                 // base0 + 4 * (jZ + (r + s) mod Z)
+        } else if (QC) {
             const uint2 e = t.ent[e0 + j];
             const uint32_t u = r4 + e.x;
             d[j] = min(u - t.Z4, u) + e.y;                 // 4 * (jZ + (r + s) mod Z)
@@ -66,8 +83,13 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
     uint32_t L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        LDPC_CHECK(d[j] < 4u * (uint32_t)a.N && (d[j] & 3u) == 0);          // a variable of this code
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
+        if constexpr (QC && FP >= 0) {
+            LDPC_CHECK(d[j] - bp + OFF_L < 4u * (uint32_t)a.N && (d[j] & 3u) == 0);   // (bp: base of Z^(k-1))
+            asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(L[j]) : "r"(d[j]), "n"(OFF_L));
+        } else {
+            LDPC_CHECK(d[j] < 4u * (uint32_t)a.N && (d[j] & 3u) == 0);      // a variable of this code
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(L[j]) : "r"(d[j] + bp));
+        }
     }
     if (ES) synd |= atom_row_parity<DC>(L);
     uint32_t q[DC];                                                      // q_mn + 0x8000 per lane
@@ -80,8 +102,12 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
     uint32_t rn[DC];                                                     // V(L^(k)_mn) + 0x8000
     new_state<DC, true, VM, FMT == FMT_1BIT>(q, vk, st, rn, a.rk);
 #pragma unroll
-    for (int j = 0; j < DC; ++j)                                          // Z^(k)_n += L^(k)_mn
-        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");
+    for (int j = 0; j < DC; ++j) {                                        // Z^(k)_n += L^(k)_mn
+        if constexpr (QC && FP >= 0)
+            asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(d[j]), "r"(rn[j]), "n"(OFF_A) : "memory");
+        else
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");
+    }
 }
 
 // ---------------------------------------------------------------- FMT_FULL (§4)
@@ -194,10 +220,10 @@ __device__ __forceinline__ void atom_row_full_x2(const ResArgs &a, const QcTab &
     }
 }
 
-template <int DC, bool ES, int FMT, int VM>
+template <int DC, bool ES, int FMT, int VM, int FP = -1>
 __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t tw,
                                            int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba, bool first_iter,
-                                           uint32_t &synd) {
+                                           uint32_t &synd, uint32_t tabs = 0) {
     if constexpr (DC == 0) {
         return bend;
     } else if constexpr (FMT == FMT_FULL) {
@@ -232,26 +258,26 @@ __device__ __forceinline__ int atom_qc_run(int b, int bend, int g, const ResArgs
             RowState st = {0u, 0u, 0u};
             LDPC_CHECK(b < nb && (uint32_t)((FMT == FMT_C16 ? 3 : 2) * nb) <= (uint32_t)a.cols_per_group);
             if (!first_iter) state_tmem_load<FMT, true>(tw, b, nb, st);
-            if (rloc < a.Z) atom_row<DC, true, ES, VM, FMT>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd);
+            if (rloc < a.Z) atom_row<DC, true, ES, VM, FMT, false, FP>(a, t, vk, bp, ba, t.e0[b][g], r4, 0, first_iter, st, synd, tabs);
             state_tmem_store<FMT>(tw, b, nb, st);
         }
         return b;
     }
 }
 
-template <bool ES, int FMT, int VM>
+template <bool ES, int FMT, int VM, int FP = -1>
 __device__ __forceinline__ int atom_qc_dispatch(int dc, int b, int bend, int g, const ResArgs &a, const QcTab &t,
                                                 const VarK &vk, uint32_t tw, int nb, int rloc, uint32_t r4, uint32_t bp, uint32_t ba,
-                                                bool first_iter, uint32_t &synd) {
+                                                bool first_iter, uint32_t &synd, uint32_t tabs = 0) {
     switch (dc) {
-    case 2: return atom_qc_run<2, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 3: return atom_qc_run<3, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 4: return atom_qc_run<4, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 5: return atom_qc_run<5, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 6: return atom_qc_run<6, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 7: return atom_qc_run<7, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    case 8: return atom_qc_run<8, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
-    default: return atom_qc_run<0, ES, FMT, VM>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd);
+    case 2: return atom_qc_run<2, ES, FMT, VM, FP>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd, tabs);
+    case 3: return atom_qc_run<3, ES, FMT, VM, FP>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd, tabs);
+    case 4: return atom_qc_run<4, ES, FMT, VM, FP>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd, tabs);
+    case 5: return atom_qc_run<5, ES, FMT, VM, FP>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd, tabs);
+    case 6: return atom_qc_run<6, ES, FMT, VM, FP>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd, tabs);
+    case 7: return atom_qc_run<7, ES, FMT, VM, FP>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd, tabs);
+    case 8: return atom_qc_run<8, ES, FMT, VM, FP>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd, tabs);
+    default: return atom_qc_run<0, ES, FMT, VM, FP>(b, bend, g, a, t, vk, tw, nb, rloc, r4, bp, ba, first_iter, synd, tabs);
     }
 }
 
@@ -388,7 +414,9 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint32_t tslot;
     __shared__ __align__(8) uint64_t zbar;
-    uint32_t *buf0 = smem, *buf1 = smem + a.Np;
+    constexpr bool FIXK = QC && ES && FMT != FMT_FULL;   // kernels with the fixed-base row scans
+    const bool fix = FIXK && a.qc_fix;
+    uint32_t *buf0 = smem, *buf1 = smem + (fix ? kAtomFixOff / 4 : (uint32_t)a.Np);
     const int tid = threadIdx.x, nth = blockDim.x;
     const int grp = QC ? (a.group_threads == 128 ? (tid >> 7) : 0) : 0;
     const int rloc = QC ? tid - grp * a.group_threads : tid;
@@ -409,6 +437,14 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
     const uint32_t sct = s0 + 8u * (uint32_t)a.Np;
     if (!QC && a.csr_smem)
         for (int i = tid; i < a.csr_dc * a.M; i += nth) smem[2 * a.Np + i] = __ldg(a.colT + i);
+    // fixed bases: the shift table after buffer 1 (8-byte aligned), block offsets + base of buffer 0
+    const uint32_t tabw = (kAtomFixOff / 4 + (uint32_t)a.Np + 1u) & ~1u;
+    const uint32_t tabs = s0 + 4u * tabw;
+    if (fix)
+        for (int i = tid; i < t.nent; i += nth) {
+            smem[tabw + 2 * i] = t.ent[i].x;
+            smem[tabw + 2 * i + 1] = t.ent[i].y + s0;
+        }
 
     for (int pair = blockIdx.x; pair < a.npairs; pair += gridDim.x) {
         const int f0 = 2 * pair, f1 = f0 + 1;
@@ -427,15 +463,16 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             const VarK vk = a.nsched ? a.vk_sched[k - 1] : a.vk;   // lambda_k / beta_k
             // one scan over this thread's rows; the check-node variant (offset / normalized)
             // is fixed per iteration, so it is a template parameter of the row code
-            auto scan = [&](auto vm_tag, auto fi_tag, auto cs_tag) {
+            auto scan = [&](auto vm_tag, auto fi_tag, auto cs_tag, auto fp_tag) __attribute__((always_inline)) {
                 constexpr int VM = decltype(vm_tag)::value;
                 constexpr bool FI = decltype(fi_tag)::value;   // first iteration: no rebuild, no state load
                 constexpr bool CSM = decltype(cs_tag)::value;  // general codes: column table in shared memory
+                constexpr int FP = decltype(fp_tag)::value;    // fixed bases: iteration parity (-1: off)
                 if (QC) {
 #pragma unroll 1
                     for (int b = 0; b < nb;) {
-                        if (grp == 0) b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, bp, ba, FI, synd);
-                        else b = atom_qc_dispatch<ES, FMT, VM>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, bp, ba, FI, synd);
+                        if (grp == 0) b = atom_qc_dispatch<ES, FMT, VM, FP>(t.dc[b][0], b, t.run_end[b][0], 0, a, t, vk, tw, nb, rloc, r4, bp, ba, FI, synd, tabs);
+                        else b = atom_qc_dispatch<ES, FMT, VM, FP>(t.dc[b][1], b, t.run_end[b][1], 1, a, t, vk, tw, nb, rloc, r4, bp, ba, FI, synd, tabs);
                     }
                 } else if (FMT != FMT_FULL && a.dc_uniform) {
                     // row-regular code (e.g. config 1's (3,6)-regular H): one dispatch on the
@@ -482,13 +519,21 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             };
             using F1 = std::integral_constant<bool, true>;
             using F0 = std::integral_constant<bool, false>;
-            auto run = [&](auto vm) {
+            using PN = std::integral_constant<int, -1>;
+            auto run = [&](auto vm) __attribute__((always_inline)) {
                 if (!QC && FMT != FMT_FULL && a.csr_smem) {
-                    if (first_iter) scan(vm, F1{}, F1{});
-                    else scan(vm, F0{}, F1{});
+                    if (first_iter) scan(vm, F1{}, F1{}, PN{});
+                    else scan(vm, F0{}, F1{}, PN{});
+                } else if (FIXK && fix) {
+                    // parity 0: odd k reads buffer 0 and accumulates into buffer 1
+                    using P0 = std::integral_constant<int, FIXK ? 0 : -1>;
+                    using P1 = std::integral_constant<int, FIXK ? 1 : -1>;
+                    if (first_iter) scan(vm, F1{}, F0{}, P0{});
+                    else if (k & 1) scan(vm, F0{}, F0{}, P0{});
+                    else scan(vm, F0{}, F0{}, P1{});
                 } else {
-                    if (first_iter) scan(vm, F1{}, F0{});
-                    else scan(vm, F0{}, F0{});
+                    if (first_iter) scan(vm, F1{}, F0{}, PN{});
+                    else scan(vm, F0{}, F0{}, PN{});
                 }
             };
             if (vk.norm) run(std::integral_constant<int, 1>{});

@@ -273,6 +273,7 @@ extern "C" ldpc_status ldpc_code_create(const ldpc_code_desc *desc, int cuda_dev
                     ++e;
                 }
             }
+            t.nent = e;
             // super-batches: pairs of base rows with disjoint column blocks (their Z rows
             // each touch distinct variables), processed by two 128-thread groups at once.
             const int groups = c->Z <= 128 ? 2 : 1;
@@ -553,6 +554,7 @@ struct Plan {
     uint32_t tmem_cols = 0, tmem_cols_needed = 0;
     int cols_per_group = 0;
     int csr_smem = 0;            // barrier-free kernel, general codes: column table in shared memory
+    int qc_fix = 0;              // barrier-free kernel, QC codes with early stop: fixed buffer bases
     // stream
     int tile = 64, ntiles = 0;
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
@@ -612,7 +614,7 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
         return fail(LDPC_ERR_INVALID_ARG, "bad tuning.path %d", pl.tn.path);
     if (pl.tn.resident_waves < 0 || pl.tn.stream_chunk_tiles < 0 || pl.tn.host_chunks < 0 || pl.tn.host_streams < 0 ||
         pl.tn.host_streams > 4 || pl.tn.resident_threads < 0 || pl.tn.resident_threads > 256 ||
-        pl.tn.resident_threads % 32 != 0)
+        pl.tn.resident_threads % 32 != 0 || pl.tn.resident_fixed_bases < -1 || pl.tn.resident_fixed_bases > 0)
         return fail(LDPC_ERR_INVALID_ARG, "bad tuning value");
     if (pl.sched == LDPC_SCHED_TWOSCAN) {
         if (p->msg_format != LDPC_MSG_COMPACT)
@@ -803,6 +805,21 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                 pl.smem = ps.smem;
             }
         }
+        // barrier-free kernel, QC code, early stop: buffer 1 at a fixed offset and the shift table in
+        // shared memory, so the row scans address both buffers with immediate offsets
+        // (k_resident_atom.cuh) -- when the buffer fits below the offset and it costs no occupancy
+        if (pl.kind == RES_ATOM && c->qc && p->early_stop && pl.fmt != FMT_FULL && pl.tn.resident_fixed_bases == 0 &&
+            (size_t)4 * ((c->N + 3) & ~3) <= kAtomFixOff) {
+            Plan ps = pl;
+            const size_t np4 = (size_t)4 * ((c->N + 3) & ~3);
+            ps.smem = kAtomFixOff + ((np4 + 7) & ~(size_t)7) + (size_t)8 * c->qtab_atom->nent;
+            int bs = 0;
+            if (ps.smem <= c->smem_optin && res_occupancy_any(c, p, ps, &bs) == cudaSuccess &&
+                std::min(bs, (int)(512 / cols)) >= blocks) {
+                pl.qc_fix = 1;
+                pl.smem = ps.smem;
+            }
+        }
         if (blocks < 1) return fail(LDPC_ERR_UNSUPPORTED, "resident kernel does not fit on an SM");
         // One frame pair per CTA (grid = pairs, up to 64 waves): the block scheduler then
         // balances the SMs dynamically.  Measured against a persistent grid of `blocks x SMs`
@@ -877,6 +894,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.dcT = natural ? c->d_dcT_lay : c->d_dcT;
     a.cpar = pl.kind == RES_ATOM ? 0xBFFFC000u : 0xFFFEFFFFu;   // -(bias + 1) per lane (atom: bias 0x3FFF)
     a.csr_smem = pl.csr_smem;
+    a.qc_fix = pl.qc_fix;
     a.dc_uniform = c->dc_uniform;
     a.csr_dc = c->max_dc;
     a.alpha = pl.alpha;

@@ -390,6 +390,27 @@ def test_qc_odd_batch_and_mixed_convergence():
     assert_int_parity(g.CONFIGS[2].code(), llr, _cfg_params(g.CONFIGS[2]), 15, 1, 1, 511)
 
 
+@pytest.mark.parametrize("fixed", [0, -1], ids=["fixed-bases", "register-bases"])
+@pytest.mark.parametrize("fmt", ["compact", "1bit"])
+def test_qc_early_stop_buffer_bases(fixed, fmt):
+    """The QC early-stop resident kernel with the posterior buffers at a fixed distance and the
+    shift table in shared memory (immediate-offset addressing, the default when the code fits)
+    and with the buffer bases in registers (tuning.resident_fixed_bases = -1): both bit-exact
+    with the oracle on an odd batch whose frames stop at spread-out iterations."""
+    code = g.CONFIGS[2].code()
+    s2 = g.ebn0_to_sigma2(2.25, code.rate)
+    if fmt == "compact":
+        llr = g.llr(123, 0, 301, code.n_vars, s2, g.LLR_I16, 3, 511)
+        params = P.make_params(15, 1, P.LDPC_MINSUM_OFFSET, 1, llr_type=P.LDPC_LLR_I16)
+        Q = 511
+    else:
+        llr = g.llr(124, 0, 301, code.n_vars, s2, g.LLR_I8, 2, 127)
+        params = P.make_params(15, 1, P.LDPC_MINSUM_OFFSET, 1, llr_type=P.LDPC_LLR_I8, msg_format=P.LDPC_MSG_1BIT)
+        Q = 127
+    ref = assert_int_parity(code, llr, tuned(params, resident_fixed_bases=fixed), 15, 1, 1, Q)
+    assert len(np.unique(ref.iters)) >= 4
+
+
 @pytest.mark.parametrize("chunk", [1, 2])
 def test_stream_l2_chunks(chunk):
     """Streaming kernels decoding the frame tiles in chunks (tuning.stream_chunk_tiles,

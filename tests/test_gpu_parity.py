@@ -249,6 +249,11 @@ def test_unsupported_requests():
     with pytest.raises(P.LdpcError) as e:
         dec.workspace(8, P.make_params(0, 0))
     assert e.value.status == P.LDPC_ERR_INVALID_ARG
+    for bad in ({"resident_fixed_bases": 1}, {"resident_fixed_bases": -2}, {"resident_threads": 48},
+                {"host_streams": 5}, {"path": 7}):
+        with pytest.raises(P.LdpcError) as e:
+            dec.workspace(8, P.make_params(5, 1, P.LDPC_MINSUM_OFFSET, 1, tuning=bad))
+        assert e.value.status == P.LDPC_ERR_INVALID_ARG, bad
     # frame counts: int32 frame indices on the device; the size query alone (no allocation)
     params = _cfg_params(g.CONFIGS[1])
     assert P.ldpc_decode_workspace_size(dec.handle, 2**31 - 1, params) > 0

@@ -416,6 +416,19 @@ def test_qc_early_stop_buffer_bases(fixed, fmt):
     assert len(np.unique(ref.iters)) >= 4
 
 
+@pytest.mark.parametrize("mb,nb,Z", [(32, 64, 128), (24, 64, 129)], ids=["N8192-fixed", "N8256-registers"])
+def test_qc_early_stop_fixed_bases_size_boundary(mb, nb, Z):
+    """Largest QC code whose posterior buffer fits below the fixed 32 KB offset (N = 8192: 4N =
+    32768, fixed bases) and one just above it (N = 8256: buffer bases in registers), both with
+    early stop at spread-out iterations, bit-exact with the oracle."""
+    code = g.qc(mb, nb, Z, np.full(nb, 3, np.int32), seed=21)
+    s2 = g.ebn0_to_sigma2(2.5, code.rate)
+    llr = g.llr(125, 0, 96, code.n_vars, s2, g.LLR_I16, 3, 511)
+    params = P.make_params(15, 1, P.LDPC_MINSUM_OFFSET, 1, llr_type=P.LDPC_LLR_I16)
+    ref = assert_int_parity(code, llr, params, 15, 1, 1, 511)
+    assert len(np.unique(ref.iters)) >= 2
+
+
 @pytest.mark.parametrize("chunk", [1, 2])
 def test_stream_l2_chunks(chunk):
     """Streaming kernels decoding the frame tiles in chunks (tuning.stream_chunk_tiles,

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Sweep the host-buffer decode's chunking (ldpc_tuning.host_chunks / host_streams) on a
-BASELINE config: pinned host LLRs in, hard bits / posteriors / flags / iterations out."""
+BASELINE config: pinned host LLRs in, hard bits / posteriors / flags / iterations out.
+    python tools/sweep_e2e.py CFG [CHUNKS,STREAMS ...]   (0,0 = the library's default)"""
 import os
 import sys
 
@@ -21,7 +22,7 @@ hb = torch.empty((F, dec.wpf), dtype=torch.int32).pin_memory()
 ok = torch.empty(F, dtype=torch.uint8).pin_memory()
 it = torch.empty(F, dtype=torch.int32).pin_memory()
 post = torch.empty((F, code.n_vars), dtype=torch.float32 if llr.dtype == np.float32 else torch.int16).pin_memory()
-for chunks, streams in [(0, 0), (1, 1), (2, 2), (2, 1), (4, 4), (8, 4), (16, 4)]:
+for chunks, streams in [(int(a), int(b)) for a, b in (x.split(",") for x in sys.argv[2:])] or [(0, 0), (1, 1), (2, 2), (2, 1), (4, 4), (8, 4), (16, 4)]:
     params = P.params_for_config(cfg)
     P.set_tuning(params, {"host_chunks": chunks, "host_streams": streams})
     for _ in range(2):

@@ -416,7 +416,8 @@ def test_qc_early_stop_buffer_bases(fixed, fmt):
     assert len(np.unique(ref.iters)) >= 4
 
 
-@pytest.mark.parametrize("mb,nb,Z", [(32, 64, 128), (24, 64, 129)], ids=["N8192-fixed", "N8256-registers"])
+@pytest.mark.parametrize("mb,nb,Z", [(32, 64, 128), (20, 40, 200), (24, 64, 129)],
+                         ids=["N8192-fixed", "N8000-Z200-fixed-one-group", "N8256-registers"])
 def test_qc_early_stop_fixed_bases_size_boundary(mb, nb, Z):
     """Largest QC code whose posterior buffer fits below the fixed 32 KB offset (N = 8192: 4N =
     32768, fixed bases) and one just above it (N = 8256: buffer bases in registers), both with

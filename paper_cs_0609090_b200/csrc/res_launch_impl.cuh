@@ -85,19 +85,28 @@ cudaError_t launch(int grid, int threads, size_t dyn_smem, const ResArgs &a, con
     return cudaGetLastError();
 }
 
-// dispatch over the remaining template parameters for one (QC, ES) combination
-template <template <bool, bool, int, typename, int> class K, bool Q, bool E, typename... Args>
+// dispatch over the remaining template parameters for one (QC, ES) combination.  PART splits
+// the instantiations over translation units so they compile in parallel: -1 = all, 0 = the
+// COMPACT format and the fp32 layered kernel, 1 = the 1-bit and full-message formats
+// (res_part_of below picks the part of a call).
+inline int res_part_of(int fmt, int kind) { return (fmt == FMT_C16 || kind == 4) ? 0 : 1; }
+template <template <bool, bool, int, typename, int> class K, bool Q, bool E, int PART, typename... Args>
 cudaError_t dispatch_qe(int fmt, bool i8, int kind, Args... args) {
 #define LDPC_RES_KIND(F, KK) \
     if (kind == KK) return i8 ? K<Q, E, F, int8_t, KK>::run(args...) : K<Q, E, F, int16_t, KK>::run(args...);
 #define LDPC_RES_CASE(F) \
     if (fmt == F) { LDPC_RES_KIND(F, 0) LDPC_RES_KIND(F, 1) LDPC_RES_KIND(F, 2) }
-    LDPC_RES_CASE(FMT_C16) LDPC_RES_CASE(FMT_1BIT)
-    // FMT_FULL (§4 per-edge messages) exists for the barrier-free kernel only
-    if (fmt == FMT_FULL && kind == 2)
-        return i8 ? K<Q, E, FMT_FULL, int8_t, 2>::run(args...) : K<Q, E, FMT_FULL, int16_t, 2>::run(args...);
-    // fp32 LLRs, layered schedule: one frame per CTA (k_resident_f32.cuh)
-    if (kind == 4) return K<Q, E, FMT_C16, float, 4>::run(args...);
+    if constexpr (PART != 1) {
+        LDPC_RES_CASE(FMT_C16)
+        // fp32 LLRs, layered schedule: one frame per CTA (k_resident_f32.cuh)
+        if (kind == 4) return K<Q, E, FMT_C16, float, 4>::run(args...);
+    }
+    if constexpr (PART != 0) {
+        LDPC_RES_CASE(FMT_1BIT)
+        // FMT_FULL (§4 per-edge messages) exists for the barrier-free kernel only
+        if (fmt == FMT_FULL && kind == 2)
+            return i8 ? K<Q, E, FMT_FULL, int8_t, 2>::run(args...) : K<Q, E, FMT_FULL, int16_t, 2>::run(args...);
+    }
 #undef LDPC_RES_CASE
 #undef LDPC_RES_KIND
     return cudaErrorInvalidValue;
@@ -116,23 +125,27 @@ struct Launch {
 
 }  // namespace resimpl
 
-// per-(QC, ES) entry points, defined in res_launch_q*e*.cu
-#define LDPC_RES_QE_DECL(Q, E)                                                                                   \
-    cudaError_t res_occupancy_q##Q##e##E(int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,         \
-                                         int threads, int *blocks);                                              \
-    cudaError_t res_launch_q##Q##e##E(int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,         \
-                                      const ResArgs &a, const QcTab &t, cudaStream_t s);
-LDPC_RES_QE_DECL(0, 0) LDPC_RES_QE_DECL(0, 1) LDPC_RES_QE_DECL(1, 0) LDPC_RES_QE_DECL(1, 1)
+// per-(QC, ES, part) entry points, defined in res_launch_q*e*[_p*].cu (P = 2: all parts in one
+// translation unit, the general-code combinations; the QC ones are split in two)
+#define LDPC_RES_QE_DECL(Q, E, P)                                                                                \
+    cudaError_t res_occupancy_q##Q##e##E##p##P(int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,   \
+                                               int threads, int *blocks);                                        \
+    cudaError_t res_launch_q##Q##e##E##p##P(int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,   \
+                                            const ResArgs &a, const QcTab &t, cudaStream_t s);
+LDPC_RES_QE_DECL(0, 0, 2) LDPC_RES_QE_DECL(0, 1, 2)
+LDPC_RES_QE_DECL(1, 0, 0) LDPC_RES_QE_DECL(1, 0, 1) LDPC_RES_QE_DECL(1, 1, 0) LDPC_RES_QE_DECL(1, 1, 1)
 #undef LDPC_RES_QE_DECL
 
-#define LDPC_RES_QE_DEF(Q, E)                                                                                    \
-    cudaError_t res_occupancy_q##Q##e##E(int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,         \
-                                         int threads, int *blocks) {                                             \
-        return resimpl::dispatch_qe<resimpl::Occ, (Q != 0), (E != 0)>(fmt, i8, kind, dyn_smem, smem_per_sm, threads, blocks);   \
+#define LDPC_RES_QE_DEF(Q, E, P)                                                                                 \
+    cudaError_t res_occupancy_q##Q##e##E##p##P(int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,   \
+                                               int threads, int *blocks) {                                       \
+        return resimpl::dispatch_qe<resimpl::Occ, (Q != 0), (E != 0), (P == 2 ? -1 : P)>(fmt, i8, kind, dyn_smem,  \
+                                                                                          smem_per_sm, threads, blocks); \
     }                                                                                                            \
-    cudaError_t res_launch_q##Q##e##E(int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,         \
-                                      const ResArgs &a, const QcTab &t, cudaStream_t s) {                        \
-        return resimpl::dispatch_qe<resimpl::Launch, (Q != 0), (E != 0)>(fmt, i8, kind, grid, threads, dyn_smem, &a, &t, s);    \
+    cudaError_t res_launch_q##Q##e##E##p##P(int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,   \
+                                            const ResArgs &a, const QcTab &t, cudaStream_t s) {                  \
+        return resimpl::dispatch_qe<resimpl::Launch, (Q != 0), (E != 0), (P == 2 ? -1 : P)>(fmt, i8, kind, grid,  \
+                                                                                             threads, dyn_smem, &a, &t, s); \
     }
 
 }  // namespace ldpc

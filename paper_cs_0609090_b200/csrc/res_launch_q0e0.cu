@@ -2,5 +2,5 @@
 #include "res_launch_impl.cuh"
 
 namespace ldpc {
-LDPC_RES_QE_DEF(0, 0)
+LDPC_RES_QE_DEF(0, 0, 2)
 }  // namespace ldpc

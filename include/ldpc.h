@@ -143,7 +143,8 @@ typedef struct {
     int32_t host_streams;    /* ldpc_decode_batch_host: internal streams, 1..4 (0 = automatic) */
     int32_t resident_threads; /* general (non-QC) codes on the barrier-free resident kernel: threads
                                  per CTA, a multiple of 32 in [32, 256] (0 = automatic) */
-    int32_t resident_fixed_bases; /* QC codes with early stop on the barrier-free resident kernel:
+    int32_t resident_fixed_bases; /* early stop on the barrier-free resident kernel (QC codes, and
+                                     general codes whose column table is staged in shared memory):
                                      -1 = posterior buffer bases in registers (cross-check),
                                      0 = automatic (fixed bases, immediate-offset addressing, when
                                      4*N <= 32768 and it costs no occupancy) */

@@ -50,7 +50,7 @@ struct QcTab {
     uint2 ent[kQcMaxEnt];               // (4 * shift, 4 * (j * Z)) per base-matrix entry
 };
 
-// barrier-free resident kernel, fixed buffer bases (ResArgs::qc_fix): byte offset of buffer 1
+// barrier-free resident kernel, fixed buffer bases (ResArgs::fixed_bases): byte offset of buffer 1
 constexpr uint32_t kAtomFixOff = 32768;
 
 constexpr int kMaxSched = 64;   // per-iteration variant table of the resident kernels
@@ -81,9 +81,9 @@ struct ResArgs {
     RegK rk;                          // register constants (simd16.cuh)
     uint32_t cpar;                    // row_parity constant (-(0x00010001), biased: -(0x40014001))
     int csr_smem, csr_dc;             // barrier-free kernel, general codes: colT rows [0, csr_dc) staged in smem
-    int qc_fix;                       // barrier-free kernel, QC codes with early stop: second posterior buffer
-                                      // at the fixed byte offset kAtomFixOff and the shift table in shared
-                                      // memory (k_resident_atom.cuh, "fixed buffer bases")
+    int fixed_bases;                  // barrier-free kernel with early stop: second posterior buffer at the
+                                      // fixed byte offset kAtomFixOff, shift / column table in shared memory
+                                      // with buffer 0's address folded in (k_resident_atom.cuh)
     int dc_uniform;                   // general codes: the row degree if every row has it, else 0
     // message export (ldpc_decode_batch_messages): the exit messages L_mn rebuilt from each
     // row's state, int16 [nframes][E] in CSR edge order; nullptr = no export

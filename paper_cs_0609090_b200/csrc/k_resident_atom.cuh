@@ -34,29 +34,33 @@ namespace ldpc {
 constexpr int kAtomBias = 0x3FFF;
 constexpr uint32_t kAtomQ0 = 0x40014001u;    // (0x8000 - bias) per lane: q + 0x8000 = word + Q0 - 2 L_old
 
-// Fixed buffer bases (ResArgs::qc_fix; QC codes with early stop, 4 Np <= kAtomFixOff): buffer 1
-// starts kAtomFixOff bytes after buffer 0 and the shift table is copied to shared memory with
-// the shared address of buffer 0 folded into its block offsets, so a row scan specialised on
-// the iteration parity FP addresses Z^(k-1) and Z^(k) as [d + imm] -- two IMADs fewer per edge
-// than adding the buffer bases held in registers (the early-stop kernel cannot keep them in
-// uniform registers, which is what the fixed-iteration kernels do: LDS / ATOMS [R + UR]).
+// Fixed buffer bases (ResArgs::fixed_bases; early stop, 4 Np <= kAtomFixOff, QC codes or general
+// codes with the column table in shared memory): buffer 1 starts kAtomFixOff bytes after
+// buffer 0 and the shift / column table is copied to shared memory with the shared address of
+// buffer 0 folded into its offsets, so a row scan specialised on the iteration parity FP
+// addresses Z^(k-1) and Z^(k) as [d + imm] -- two IMADs fewer per edge than adding the buffer
+// bases held in registers (the early-stop kernel cannot keep them in uniform registers, which
+// is what the fixed-iteration kernels do: LDS / ATOMS [R + UR]).
 // kAtomFixOff: args.cuh (the planner sizes shared memory with it).
 
-// Hard-decision parity of a row from its biased words: bit 15 / 31 set iff odd.
+// Hard-decision parity of a row from its biased words: bit 14 / 30 set iff odd (the other bits
+// are garbage).  OR-ed into the early-stop syndrome word as it stands: bit 14 of an OR is the OR
+// of the rows' bits 14, so the bits need no shift or mask per row (kAtomSyndLo / kAtomSyndHi).
+constexpr uint32_t kAtomSyndLo = 0x00004000u, kAtomSyndHi = 0x40000000u;
 template <int DC>
 __device__ __forceinline__ uint32_t atom_row_parity(const uint32_t (&L)[DC]) {
     uint32_t x = L[0];
 #pragma unroll
     for (int j = 1; j < DC; ++j) x ^= L[j];
-    x = (x << 1) & 0x80008000u;                         // XOR of bit 14 -> bit 15 (and 30 -> 31)
-    return (DC & 1) ? (x ^ 0x80008000u) : x;            // [Z <= 0] = NOT bit 14
+    return (DC & 1) ? ~x : x;                           // [Z <= 0] = NOT bit 14 (30)
 }
 
 // CSM (general codes): the [dc][M] column table was staged in shared memory at byte
 // address sct (ResArgs::csr_smem), so the per-edge offsets are shared-memory loads
-// FP (QC only): -1 = buffer bases bp / ba in registers; 0 / 1 = fixed bases, iteration parity
-// (0: Z^(k-1) in buffer 0, Z^(k) in buffer 1; 1: the reverse), sct = shared address of the
-// shift table (entries (4 s, 4 j Z + base of buffer 0))
+// FP (QC, or CSM): -1 = buffer bases bp / ba in registers; 0 / 1 = fixed bases, iteration
+// parity (0: Z^(k-1) in buffer 0, Z^(k) in buffer 1; 1: the reverse); sct = shared address of
+// the shift table (QC: entries (4 s, 4 j Z + base of buffer 0)) or of the column table (CSM:
+// byte offsets, + base of buffer 0 when FP >= 0)
 template <int DC, bool QC, bool ES, int VM, int FMT, bool CSM = false, int FP = -1>
 __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba, int e0,
                                          uint32_t r4, int p, bool first_iter, RowState &st, uint32_t &synd,
@@ -83,7 +87,8 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
     uint32_t L[DC];
 #pragma unroll
     for (int j = 0; j < DC; ++j) {
-        if constexpr (QC && FP >= 0) {
+        if constexpr (FP >= 0) {
+            static_assert(QC || CSM, "fixed buffer bases need the shift / column table in shared memory");
             LDPC_CHECK(d[j] - bp + OFF_L < 4u * (uint32_t)a.N && (d[j] & 3u) == 0);   // (bp: base of Z^(k-1))
             asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(L[j]) : "r"(d[j]), "n"(OFF_L));
         } else {
@@ -103,7 +108,7 @@ __device__ __forceinline__ void atom_row(const ResArgs &a, const QcTab &t, const
     new_state<DC, true, VM, FMT == FMT_1BIT>(q, vk, st, rn, a.rk);
 #pragma unroll
     for (int j = 0; j < DC; ++j) {                                        // Z^(k)_n += L^(k)_mn
-        if constexpr (QC && FP >= 0)
+        if constexpr (FP >= 0)
             asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(d[j]), "r"(rn[j]), "n"(OFF_A) : "memory");
         else
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(d[j] + ba), "r"(rn[j]) : "memory");
@@ -281,17 +286,17 @@ __device__ __forceinline__ int atom_qc_dispatch(int dc, int b, int bend, int g, 
     }
 }
 
-template <bool ES, int VM, int FMT, bool CSM>
+template <bool ES, int VM, int FMT, bool CSM, int FP = -1>
 __device__ __forceinline__ void atom_csr_dispatch(int dc, const ResArgs &a, const QcTab &t, const VarK &vk, uint32_t bp, uint32_t ba,
                                                   int p, bool first_iter, RowState &st, uint32_t &synd, uint32_t sct) {
     switch (dc) {
-    case 2: atom_row<2, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 3: atom_row<3, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 4: atom_row<4, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 5: atom_row<5, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 6: atom_row<6, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 7: atom_row<7, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
-    case 8: atom_row<8, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 2: atom_row<2, false, ES, VM, FMT, CSM, FP>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 3: atom_row<3, false, ES, VM, FMT, CSM, FP>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 4: atom_row<4, false, ES, VM, FMT, CSM, FP>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 5: atom_row<5, false, ES, VM, FMT, CSM, FP>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 6: atom_row<6, false, ES, VM, FMT, CSM, FP>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 7: atom_row<7, false, ES, VM, FMT, CSM, FP>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
+    case 8: atom_row<8, false, ES, VM, FMT, CSM, FP>(a, t, vk, bp, ba, 0, 0, p, first_iter, st, synd, sct); break;
     }
 }
 
@@ -414,8 +419,8 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint32_t tslot;
     __shared__ __align__(8) uint64_t zbar;
-    constexpr bool FIXK = QC && ES && FMT != FMT_FULL;   // kernels with the fixed-base row scans
-    const bool fix = FIXK && a.qc_fix;
+    constexpr bool FIXK = ES && FMT != FMT_FULL;   // kernels with the fixed-base row scans
+    const bool fix = FIXK && a.fixed_bases;
     uint32_t *buf0 = smem, *buf1 = smem + (fix ? kAtomFixOff / 4 : (uint32_t)a.Np);
     const int tid = threadIdx.x, nth = blockDim.x;
     const int grp = QC ? (a.group_threads == 128 ? (tid >> 7) : 0) : 0;
@@ -434,13 +439,15 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
     // general codes: stage the [dc][M] column table after the posterior buffers (planner:
     // ResArgs::csr_smem when it fits without costing occupancy); visible after the first
     // barrier of the pair loop
-    const uint32_t sct = s0 + 8u * (uint32_t)a.Np;
-    if (!QC && a.csr_smem)
-        for (int i = tid; i < a.csr_dc * a.M; i += nth) smem[2 * a.Np + i] = __ldg(a.colT + i);
-    // fixed bases: the shift table after buffer 1 (8-byte aligned), block offsets + base of buffer 0
+    // fixed bases: the shift / column table after buffer 1 (8-byte aligned), offsets + base of buffer 0
     const uint32_t tabw = (kAtomFixOff / 4 + (uint32_t)a.Np + 1u) & ~1u;
     const uint32_t tabs = s0 + 4u * tabw;
-    if (fix)
+    const uint32_t sct = fix ? tabs : s0 + 8u * (uint32_t)a.Np;
+    if (!QC && a.csr_smem) {
+        const uint32_t w0 = fix ? tabw : 2u * (uint32_t)a.Np, add = fix ? s0 : 0u;
+        for (int i = tid; i < a.csr_dc * a.M; i += nth) smem[w0 + i] = __ldg(a.colT + i) + add;
+    }
+    if (QC && fix)
         for (int i = tid; i < t.nent; i += nth) {
             smem[tabw + 2 * i] = t.ent[i].x;
             smem[tabw + 2 * i + 1] = t.ent[i].y + s0;
@@ -485,7 +492,7 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
                             RowState st = {0u, 0u, 0u};
                             if (!FI) state_tmem_load<FMT, true>(tw, b, nb, st);
                             if (p < a.M)
-                                atom_row<DC, false, ES, VM, FMT, CSM>(a, t, vk, bp, ba, 0, 0, p, FI, st, synd, sct);
+                                atom_row<DC, false, ES, VM, FMT, CSM, (CSM ? FP : -1)>(a, t, vk, bp, ba, 0, 0, p, FI, st, synd, sct);
                             state_tmem_store<FMT>(tw, b, nb, st);
                         }
                     };
@@ -511,7 +518,7 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
                         } else {
                             RowState st = {0u, 0u, 0u};
                             if (!FI) state_tmem_load<FMT, true>(tw, b, nb, st);
-                            if (p < a.M) atom_csr_dispatch<ES, VM, FMT, CSM>(a.dcT[p], a, t, vk, bp, ba, p, FI, st, synd, sct);
+                            if (p < a.M) atom_csr_dispatch<ES, VM, FMT, CSM, (CSM ? FP : -1)>(a.dcT[p], a, t, vk, bp, ba, p, FI, st, synd, sct);
                             state_tmem_store<FMT>(tw, b, nb, st);
                         }
                     }
@@ -520,14 +527,20 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             using F1 = std::integral_constant<bool, true>;
             using F0 = std::integral_constant<bool, false>;
             using PN = std::integral_constant<int, -1>;
+            // fixed bases: parity 0 = odd k reads buffer 0 and accumulates into buffer 1
+            using P0 = std::integral_constant<int, FIXK ? 0 : -1>;
+            using P1 = std::integral_constant<int, FIXK ? 1 : -1>;
             auto run = [&](auto vm) __attribute__((always_inline)) {
                 if (!QC && FMT != FMT_FULL && a.csr_smem) {
-                    if (first_iter) scan(vm, F1{}, F1{}, PN{});
-                    else scan(vm, F0{}, F1{}, PN{});
-                } else if (FIXK && fix) {
-                    // parity 0: odd k reads buffer 0 and accumulates into buffer 1
-                    using P0 = std::integral_constant<int, FIXK ? 0 : -1>;
-                    using P1 = std::integral_constant<int, FIXK ? 1 : -1>;
+                    if (FIXK && fix) {
+                        if (first_iter) scan(vm, F1{}, F1{}, P0{});
+                        else if (k & 1) scan(vm, F0{}, F1{}, P0{});
+                        else scan(vm, F0{}, F1{}, P1{});
+                    } else {
+                        if (first_iter) scan(vm, F1{}, F1{}, PN{});
+                        else scan(vm, F0{}, F1{}, PN{});
+                    }
+                } else if (QC && FIXK && fix) {
                     if (first_iter) scan(vm, F1{}, F0{}, P0{});
                     else if (k & 1) scan(vm, F0{}, F0{}, P0{});
                     else scan(vm, F0{}, F0{}, P1{});
@@ -543,8 +556,8 @@ __global__ void __launch_bounds__(256, FMT == FMT_FULL ? 2 : 3) k_resident_atom(
             if (ES) {
                 // syndrome of Z^(k-1), gathered during this scan (1-iteration lag); the
                 // __syncthreads_or is also the end-of-iteration barrier
-                const int fail_lo = __syncthreads_or((synd & 0x00008000u) != 0);
-                const int fail_hi = __syncthreads_or((synd & 0x80000000u) != 0);
+                const int fail_lo = __syncthreads_or((synd & kAtomSyndLo) != 0);
+                const int fail_hi = __syncthreads_or((synd & kAtomSyndHi) != 0);
                 const int newly = ((fail_lo ? 0 : 1) | (fail_hi ? 0 : 2)) & ~done;
                 if (newly) {
                     res_write_outputs(a, (const uint32_t *)Lpb, f0, newly, k - 1, 0, 0, kAtomBias);

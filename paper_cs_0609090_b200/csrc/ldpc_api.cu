@@ -554,7 +554,7 @@ struct Plan {
     uint32_t tmem_cols = 0, tmem_cols_needed = 0;
     int cols_per_group = 0;
     int csr_smem = 0;            // barrier-free kernel, general codes: column table in shared memory
-    int qc_fix = 0;              // barrier-free kernel, QC codes with early stop: fixed buffer bases
+    int fixed_bases = 0;         // barrier-free kernel with early stop: fixed buffer bases
     // stream
     int tile = 64, ntiles = 0;
     size_t off_z0 = 0, off_lb[3] = {0, 0, 0}, off_st = 0, off_synd = 0, off_done = 0, off_it = 0, off_ok = 0;
@@ -805,18 +805,20 @@ ldpc_status make_plan(const ldpc_code *c, int64_t F, const ldpc_decode_params *p
                 pl.smem = ps.smem;
             }
         }
-        // barrier-free kernel, QC code, early stop: buffer 1 at a fixed offset and the shift table in
-        // shared memory, so the row scans address both buffers with immediate offsets
+        // barrier-free kernel, early stop: buffer 1 at a fixed offset and the shift table (QC) or
+        // column table (general codes, when it is staged in shared memory) after it with buffer
+        // 0's address folded in, so the row scans address both buffers with immediate offsets
         // (k_resident_atom.cuh) -- when the buffer fits below the offset and it costs no occupancy
-        if (pl.kind == RES_ATOM && c->qc && p->early_stop && pl.fmt != FMT_FULL && pl.tn.resident_fixed_bases == 0 &&
-            (size_t)4 * ((c->N + 3) & ~3) <= kAtomFixOff) {
+        if (pl.kind == RES_ATOM && (c->qc || pl.csr_smem) && p->early_stop && pl.fmt != FMT_FULL &&
+            pl.tn.resident_fixed_bases == 0 && (size_t)4 * ((c->N + 3) & ~3) <= kAtomFixOff) {
             Plan ps = pl;
             const size_t np4 = (size_t)4 * ((c->N + 3) & ~3);
-            ps.smem = kAtomFixOff + ((np4 + 7) & ~(size_t)7) + (size_t)8 * c->qtab_atom->nent;
+            const size_t tab = c->qc ? (size_t)8 * c->qtab_atom->nent : (size_t)4 * c->max_dc * c->M;
+            ps.smem = kAtomFixOff + ((np4 + 7) & ~(size_t)7) + tab;
             int bs = 0;
             if (ps.smem <= c->smem_optin && res_occupancy_any(c, p, ps, &bs) == cudaSuccess &&
                 std::min(bs, (int)(512 / cols)) >= blocks) {
-                pl.qc_fix = 1;
+                pl.fixed_bases = 1;
                 pl.smem = ps.smem;
             }
         }
@@ -894,7 +896,7 @@ cudaError_t run_resident(const ldpc_code *c, const Plan &pl, const ldpc_decode_p
     a.dcT = natural ? c->d_dcT_lay : c->d_dcT;
     a.cpar = pl.kind == RES_ATOM ? 0xBFFFC000u : 0xFFFEFFFFu;   // -(bias + 1) per lane (atom: bias 0x3FFF)
     a.csr_smem = pl.csr_smem;
-    a.qc_fix = pl.qc_fix;
+    a.fixed_bases = pl.fixed_bases;
     a.dc_uniform = c->dc_uniform;
     a.csr_dc = c->max_dc;
     a.alpha = pl.alpha;

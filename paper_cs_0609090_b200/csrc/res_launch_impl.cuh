@@ -125,14 +125,14 @@ struct Launch {
 
 }  // namespace resimpl
 
-// per-(QC, ES, part) entry points, defined in res_launch_q*e*[_p*].cu (P = 2: all parts in one
-// translation unit, the general-code combinations; the QC ones are split in two)
+// per-(QC, ES, part) entry points, defined in res_launch_q*e*_p*.cu (each combination split in
+// two translation units by format group; P = 2 would instantiate both parts in one unit)
 #define LDPC_RES_QE_DECL(Q, E, P)                                                                                \
     cudaError_t res_occupancy_q##Q##e##E##p##P(int fmt, bool i8, int kind, size_t dyn_smem, size_t smem_per_sm,   \
                                                int threads, int *blocks);                                        \
     cudaError_t res_launch_q##Q##e##E##p##P(int fmt, bool i8, int kind, int grid, int threads, size_t dyn_smem,   \
                                             const ResArgs &a, const QcTab &t, cudaStream_t s);
-LDPC_RES_QE_DECL(0, 0, 2) LDPC_RES_QE_DECL(0, 1, 2)
+LDPC_RES_QE_DECL(0, 0, 0) LDPC_RES_QE_DECL(0, 0, 1) LDPC_RES_QE_DECL(0, 1, 0) LDPC_RES_QE_DECL(0, 1, 1)
 LDPC_RES_QE_DECL(1, 0, 0) LDPC_RES_QE_DECL(1, 0, 1) LDPC_RES_QE_DECL(1, 1, 0) LDPC_RES_QE_DECL(1, 1, 1)
 #undef LDPC_RES_QE_DECL
 

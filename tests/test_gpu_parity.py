@@ -416,6 +416,27 @@ def test_qc_early_stop_buffer_bases(fixed, fmt):
     assert len(np.unique(ref.iters)) >= 4
 
 
+@pytest.mark.parametrize("fixed", [0, -1], ids=["fixed-bases", "register-bases"])
+@pytest.mark.parametrize("fmt", ["compact", "1bit"])
+@pytest.mark.parametrize("code_id", ["reg1008", "dvbs2_600"])
+def test_general_code_early_stop_buffer_bases(fixed, fmt, code_id):
+    """General (CSR) codes with early stop on the barrier-free kernel: column table in shared
+    memory with the fixed buffer bases (default) or the register bases, bit-exact with the
+    oracle; a row-regular code (one degree dispatch per iteration) and an irregular one."""
+    code = g.CONFIGS[1].code() if code_id == "reg1008" else g.dvbs2like(600, 300, 120, 8, 3, seed=6)
+    s2 = g.ebn0_to_sigma2(2.5, code.rate)
+    if fmt == "compact":
+        llr = g.llr(126, 0, 257, code.n_vars, s2, g.LLR_I16, 3, 511)
+        params = P.make_params(20, 1, P.LDPC_MINSUM_OFFSET, 1, llr_type=P.LDPC_LLR_I16)
+        Q = 511
+    else:
+        llr = g.llr(127, 0, 257, code.n_vars, s2, g.LLR_I8, 2, 127)
+        params = P.make_params(20, 1, P.LDPC_MINSUM_OFFSET, 1, llr_type=P.LDPC_LLR_I8, msg_format=P.LDPC_MSG_1BIT)
+        Q = 127
+    ref = assert_int_parity(code, llr, tuned(params, resident_fixed_bases=fixed), 20, 1, 1, Q)
+    assert len(np.unique(ref.iters)) >= 3
+
+
 @pytest.mark.parametrize("mb,nb,Z", [(32, 64, 128), (20, 40, 200), (24, 64, 129)],
                          ids=["N8192-fixed", "N8000-Z200-fixed-one-group", "N8256-registers"])
 def test_qc_early_stop_fixed_bases_size_boundary(mb, nb, Z):
